@@ -1,0 +1,392 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 SHLR hot path (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1], the headline): parallel-MRI SHLR-S on a
+256 x 256 x 8-coil seeded phantom, R = 5 Gaussian Cartesian mask with 24 ACS
+lines, Hankel window K = 15 (pencil 242 -> 512 lifted 242 x 120 matrices per
+outer iteration), SPIRiT 5 x 5 (lambda1 = 1e2, Tikhonov 1e-4), lambda = 1e4,
+beta = tau = 1, CG 15 / 1e-8, 50 outer iterations.
+
+A "step" is one ADMM outer iteration (RHS, 15-iteration capped CG with the
+SPIRiT term, lifted spectra, 512 fused Hankel-SVT + dual updates, stop rule).
+`value` = outer iterations / s with every buffer resident in HBM, timed with
+CUDA events on the plan's stream over exactly --steps iterations after
+--warmup iterations, max over ranks.  The per-iteration working set (duals
+119 MB + SPIRiT P 33.5 MB + vectors) exceeds the 126 MB L2, so no explicit
+flush is done ("inputs larger than L2").
+
+Multi-GPU: the path is one reconstruction per GPU ("replicas only",
+DESIGN.md): each rank runs its own replica, `value` = N * steps / max time.
+
+`--impl reference` times the reference C++ implementation compiled from its
+own sources (oracle/_ref/ref_driver) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import shutil
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+REF_DRIVER = os.path.join(ROOT, "oracle", "_ref", "ref_driver")
+
+CFG2 = dict(M=256, N=256, J=8, K=15, rate=0.2, acs=24, spirit=True, kernel=5, tikhonov=1e-4,
+            lam=1e4, lambda1=1e2, beta=1.0, tau=1.0, cg_max=15, cg_tol=1e-8, outer=50)
+WORKLOAD = ("config2: 256x256x8 coils, SHLR-S (SPIRiT 5x5, lambda1=1e2), R=5 Gaussian Cartesian "
+            "+ 24 ACS lines, Hankel window K=15 (pencil 242, 512 lifted 242x120 matrices/iter), "
+            "lambda=1e4, beta=tau=1, CG 15/1e-8, 50 outer iterations")
+
+
+def svt_flops(e: int, d: int) -> float:
+    """Algorithmic FLOPs of one Hankel-SVT matrix:
+    Gram 8ed^2 + Hermitian eig 36d^3 + W 8d^3 + Z = AW 8ed^2."""
+    return 16.0 * e * d * d + 44.0 * d ** 3
+
+
+def make_inputs(cfg=CFG2):
+    from paper_2107_11650_b200 import api as A
+    from paper_2107_11650_b200 import synth
+    ph = synth.pi_phantom(cfg["M"], cfg["N"], cfg["J"])
+    mask = A.mask_gauss_cartesian(cfg["N"], cfg["rate"], cfg["acs"], synth.SEED_MASK)
+    y = np.where(mask.bits[0][None, :, None].astype(bool), ph.kspace, 0)
+    g = None
+    if cfg["spirit"]:
+        a0, a1 = A.acs_range(cfg["N"], cfg["acs"])
+        g = A.spirit_calibrate(y[:, a0:a1, :], cfg["kernel"], cfg["tikhonov"])
+    hcfg = A.HankelConfig(pencil=cfg["N"] - cfg["K"] + 1)
+    return y, mask, g, hcfg
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int = 0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        if not shutil.which("nvidia-smi"):
+            return
+        self.proc = subprocess.Popen(
+            ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+             "--format=csv,noheader,nounits", "-lms", "100"],
+            stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world <= 1:
+        return None, 0, 1, 0
+    import torch
+    import torch.distributed as dist
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    backend = "nccl" if torch.cuda.is_available() else "gloo"
+    if backend == "nccl":
+        torch.cuda.set_device(local)
+    dist.init_process_group(backend)
+    return dist, rank, world, local
+
+
+def max_over_ranks(dist, value: float) -> float:
+    if dist is None:
+        return value
+    import torch
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([value], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+# ---------------------------------------------------------------- CPU leg
+def write_ref_inputs(tmp: str, y, mask, g) -> None:
+    from paper_2107_11650_b200.cplx_io import write_cplx, write_mask
+    write_cplx(y, os.path.join(tmp, "y.cplx"))
+    write_mask(mask.bits, os.path.join(tmp, "m.cplx"),
+               dict(generator="gauss_cartesian", seed=mask.seed, rate=mask.rate, acs=mask.acs))
+    if g is not None:
+        write_cplx(g.weights, os.path.join(tmp, "k.cplx"))
+
+
+def run_reference(tmp: str, procs: int, iters: int, budget_s: float, cfg=CFG2):
+    """Runs `procs` concurrent reference processes (oracle/_ref/ref_driver,
+    the reference's own solvers.cpp through the instrumented replay that is
+    bitwise equal to shlr_pi_reconstruct) for up to `iters` outer iterations
+    each, stopping at `budget_s`.  Returns per-process lists of per-iteration
+    seconds (setup excluded)."""
+    cmd = [REF_DRIVER, "pi", "y=y.cplx", "mask=m.cplx", "kernels=k.cplx", "spirit=1",
+           f"pencil={cfg['N'] - cfg['K'] + 1}", f"max_outer={iters}", "tol=1e-300", "replay=1",
+           "time=1"]
+    ps = []
+    for i in range(procs):
+        ps.append(subprocess.Popen(cmd + [f"out=ref{i}"], cwd=tmp, stdout=subprocess.PIPE,
+                                   stderr=subprocess.DEVNULL, text=True,
+                                   env=dict(os.environ, OMP_NUM_THREADS="1")))
+    results = [[] for _ in ps]
+
+    def reader(i, p):
+        for line in p.stdout:
+            if line.startswith("iter_seconds="):
+                results[i].append(float(line.split("=")[1]))
+
+    threads = [threading.Thread(target=reader, args=(i, p), daemon=True) for i, p in enumerate(ps)]
+    for t in threads:
+        t.start()
+    t0 = time.time()
+    while any(p.poll() is None for p in ps):
+        if time.time() - t0 > budget_s and all(len(r) >= 1 for r in results):
+            break
+        time.sleep(0.5)
+    for p in ps:
+        if p.poll() is None:
+            p.kill()
+    for t in threads:
+        t.join(timeout=5)
+    return results
+
+
+def cpu_baseline(y, mask, g, procs: int, iters: int, budget_s: float):
+    if not os.path.exists(REF_DRIVER):
+        return None
+    tmp = tempfile.mkdtemp(prefix="shlr_ref_")
+    try:
+        write_ref_inputs(tmp, y, mask, g)
+        res = run_reference(tmp, procs, iters, budget_s)
+    finally:
+        shutil.rmtree(tmp, ignore_errors=True)
+    per_proc = [statistics.mean(r) for r in res if r]
+    if not per_proc:
+        return None
+    done = sum(len(r) for r in res)
+    # throughput of `procs` concurrent single-threaded reference processes
+    value = sum(1.0 / s for s in per_proc)
+    return {"value": value, "unit": "iterations/s", "cores": len(per_proc), "kind": "reference",
+            "sample": (f"{len(per_proc)} concurrent single-threaded reference processes "
+                       f"(oracle/_ref/ref_driver: proj/src/*.cpp unmodified + builder Eigen subset), "
+                       f"{done} outer iterations of config 2 in total, setup excluded; "
+                       f"mean {statistics.mean(per_proc):.2f} s per iteration per process")}
+
+
+# ---------------------------------------------------------------- GPU arm
+def gpu_arm(args, dist, rank, world, local):
+    from paper_2107_11650_b200 import api as A
+    if A.device_count() < 1:
+        raise SystemExit("bench.py: no CUDA device visible (the product path has no CPU fallback)")
+    cfg = CFG2
+    y, mask, g, hcfg = make_inputs(cfg)
+    iters_total = args.warmup + args.steps
+    acfg = A.AdmmConfig(lam=cfg["lam"], lambda1=cfg["lambda1"], beta=cfg["beta"], tau=cfg["tau"],
+                        max_outer=max(iters_total, cfg["outer"]), tol=1e-300,
+                        cg_max=cfg["cg_max"], cg_tol=cfg["cg_tol"], enable_spirit=True)
+    plan = A.PiPlan(y, mask, g, hcfg, acfg)
+    # warm-up iterations (graph capture happens on the first run call)
+    plan.run(args.warmup)
+    plan.sync()
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.start()
+    barrier(dist)
+    plan.run(args.steps)
+    plan.sync()
+    _, total_ms, launches = plan.timing()
+    barrier(dist)
+    clocks = sampler.stop() if sampler else None
+    t_max_ms = max_over_ranks(dist, total_ms)
+    x, stats = plan.download()
+    assert stats.outer_iters == iters_total, (stats.outer_iters, iters_total)
+
+    # Hankel-SVT kernel alone: CUDA events around its launch in timing mode
+    plan.reset()
+    plan.set_timing(True)
+    plan.run(1)   # one untimed iteration so the duals are not the all-ones start state
+    plan.sync()
+    reps = 5
+    plan.run(reps)
+    plan.sync()
+    svt_ms_total, _, _ = plan.timing()
+    svt_ms = svt_ms_total / reps
+    plan.set_timing(False)
+    plan.close()
+
+    m, n, j, k = cfg["M"], cfg["N"], cfg["J"], cfg["K"]
+    p = n - k + 1
+    e, d = max(p, j * k), min(p, j * k)
+    flops = (m + n) * svt_flops(e, d)
+    fp32_peak = A.fp32_peak_tflops()
+    achieved_tf = flops / (svt_ms * 1e-3) / 1e12
+
+    # e2e: the public call with host buffers, H2D of y and D2H of x inside
+    e2e = None
+    if not args.no_e2e:
+        acfg_e2e = A.AdmmConfig(lam=cfg["lam"], lambda1=cfg["lambda1"], beta=cfg["beta"], tau=cfg["tau"],
+                                max_outer=cfg["outer"], tol=1e-300, cg_max=cfg["cg_max"],
+                                cg_tol=cfg["cg_tol"], enable_spirit=True)
+        A.shlr_pi_reconstruct(y[:32, :32, :2], A.SamplingMask(1, 32, mask.bits[:, :32]), None,
+                              A.HankelConfig(pencil=18), A.AdmmConfig(max_outer=1))  # context warm
+        barrier(dist)
+        t0 = time.perf_counter()
+        st = A.SolveStats()
+        A.shlr_pi_reconstruct(y, mask, g, hcfg, acfg_e2e, stats=st)
+        t_e2e = time.perf_counter() - t0
+        t_e2e = max_over_ranks(dist, t_e2e)
+        e2e = {"value": world * st.outer_iters / t_e2e, "unit": "iterations/s",
+               "h2d_bytes_per_step": int(y.size * 16 + mask.bits.size + (g.weights.size * 16 if g else 0)),
+               "d2h_bytes_per_step": int(y.size * 16),
+               "step": "one full 50-iteration shlr_cuda_pi_reconstruct call (host complex128 y, "
+                       "mask, SPIRiT kernels in; host complex128 x out; plan setup incl. SPIRiT "
+                       "map build inside)"}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        cpu = cpu_baseline(y, mask, g, procs=1, iters=2, budget_s=args.cpu_budget)
+
+    value = world * args.steps / (t_max_ms * 1e-3)
+    out = {
+        "metric": "recon iterations/sec (256x256x8 coils, SHLR-S, K=15)",
+        "value": value,
+        "unit": "iterations/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": t_max_ms / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "c64 (fp32 complex; fp64 reductions and setup)",
+        "data": "synthetic: seeded BASELINE phantom (10 ellipses, smooth phase, 8 Gaussian coils, 40 dB)",
+        "impl": "b200",
+        "config": {"workload": WORKLOAD, "parallelism": f"replicas x{world}",
+                   "l2": "inputs larger than L2: 119 MB duals + 33.5 MB SPIRiT P streamed per step",
+                   "lifted_matrix": f"{p}x{j * k}", "matrices_per_step": m + n},
+        "hankel_svt": {"matrices_per_s": (m + n) / (svt_ms * 1e-3), "kernel_ms": svt_ms,
+                       "share_of_step": svt_ms / (t_max_ms / args.steps)},
+        "roofline": {"bound": "fp32", "achieved": achieved_tf, "peak": fp32_peak, "unit": "TFLOP/s",
+                     "frac": achieved_tf / fp32_peak, "traffic": None,
+                     "kernel": "hankel_svt_kernel<120,32>",
+                     "algorithmic": f"{m + n} x (16 e d^2 + 44 d^3), e={e}, d={d}: {flops / 1e9:.2f} GFLOP/launch",
+                     "peak_source": "measured FP32 FMA probe on this GPU (MEASURED_PEAKS.json has no FP32 figure)"},
+        "gpu_launches": launches * args.steps,
+        "clocks": clocks,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+    }
+    if rank == 0:
+        print(json.dumps(out))
+
+
+def reference_arm(args, dist, rank, world):
+    if rank != 0:
+        return
+    if not os.path.exists(REF_DRIVER):
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "oracle/_ref/ref_driver not built (run __graft_entry__.build())"}))
+        return
+    y, mask, g, _ = make_inputs(CFG2)
+    procs = max(1, min(os.cpu_count() or 1, args.ref_procs))
+    tmp = tempfile.mkdtemp(prefix="shlr_ref_")
+    try:
+        write_ref_inputs(tmp, y, mask, g)
+        iters = max(1, min(args.steps, 50))
+        res = run_reference(tmp, procs, iters, args.cpu_budget)
+    finally:
+        shutil.rmtree(tmp, ignore_errors=True)
+    per_proc = [statistics.mean(r) for r in res if r]
+    done = sum(len(r) for r in res)
+    value = sum(1.0 / s for s in per_proc) if per_proc else 0.0
+    out = {
+        "metric": "recon iterations/sec (256x256x8 coils, SHLR-S, K=15)",
+        "value": value, "unit": "iterations/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 / value if value else None,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128 (fp64)",
+        "data": "synthetic: seeded BASELINE phantom", "impl": "reference",
+        "config": {"workload": WORKLOAD, "parallelism": f"{len(per_proc)} host processes"},
+        "cpu_baseline": {"value": value, "unit": "iterations/s", "cores": len(per_proc),
+                         "kind": "reference",
+                         "sample": f"{len(per_proc)} concurrent single-threaded reference processes, "
+                                   f"{done} outer iterations timed (setup excluded), budget {args.cpu_budget:.0f} s"},
+        "e2e": {"value": value, "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=150.0)
+    ap.add_argument("--ref-procs", type=int, default=16)
+    args = ap.parse_args()
+    if args.warmup < 1 or args.steps < 1:
+        raise SystemExit("need --steps >= 1 and --warmup >= 1")
+    dist, rank, world, local = dist_setup()
+    try:
+        if args.impl == "reference":
+            reference_arm(args, dist, rank, world)
+        else:
+            gpu_arm(args, dist, rank, world, local)
+    finally:
+        if dist is not None:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

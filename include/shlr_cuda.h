@@ -1,0 +1,164 @@
+/*
+ * shlr_cuda.h -- C-ABI boundary of the B200-native SHLR hot path.
+ *
+ * This is the drop-in boundary for the per-iteration separable-Hankel ADMM
+ * step of arXiv 2107.11650's reference C++ library.  A maintainer keeps the
+ * reference's public C++ API (proj/include/shlr/solvers.hpp) and replaces the
+ * bodies of its solver entry points with calls into the functions below
+ * (the C++ mirror in include/shlr_b200/ does exactly
+ * that).  Plain pointers and sizes only -- no torch, no C++ types.
+ *
+ * Conventions (mirroring the reference):
+ *   - complex data is interleaved (re, im) IEEE double, row-major, last
+ *     dimension fastest, exactly as shlr::ComplexTensor stores
+ *     std::complex<double> (proj/include/shlr/tensor.hpp:16-119);
+ *   - masks are uint8 rows x cols, rows == 1 for line masks that broadcast
+ *     along dim 0 (proj/include/shlr/sampling.hpp:33-52);
+ *   - every call is synchronous with respect to the host, runs on its own
+ *     stream/device state, and holds no global mutable state besides the
+ *     last-error string (thread-local);
+ *   - return codes: SHLR_OK, SHLR_EINVAL (-> std::invalid_argument),
+ *     SHLR_EDIVERGE (-> shlr::DivergenceError), SHLR_ECUDA (CUDA failure,
+ *     including "no device"), SHLR_EUNSUPPORTED (valid for the reference but
+ *     outside what this build implements; never a silent CPU fallback).
+ */
+#ifndef SHLR_CUDA_H
+#define SHLR_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SHLR_OK 0
+#define SHLR_EINVAL 1
+#define SHLR_EDIVERGE 4
+#define SHLR_ECUDA 5
+#define SHLR_EUNSUPPORTED 6
+
+#define SHLR_ABI_VERSION 1
+
+/* Library/ABI identification. */
+int shlr_cuda_abi_version(void);
+/* Last error message of the calling thread ("" if none). */
+const char* shlr_cuda_last_error(void);
+/* Number of visible CUDA devices (0 on a CPU-only host; never fails). */
+int shlr_cuda_device_count(void);
+
+/* Progress callback: one call per outer iteration with the exact text the
+ * reference writes (proj/src/solvers.cpp:71-78, without the newline). */
+typedef void (*shlr_log_fn)(void* ctx, const char* line);
+
+typedef struct shlr_stats {
+  size_t outer_iters;       /* SolveStats::outer_iters  (solvers.hpp:36-39) */
+  double final_rel_change;  /* SolveStats::final_rel_change */
+} shlr_stats;
+
+/* Arguments of shlr_pi_reconstruct (proj/include/shlr/solvers.hpp:64-70)
+ * after the host-side validation the reference does (solvers.cpp:101-123).
+ * Pencils are already resolved with HankelConfig::pencil_for
+ * (proj/src/hankel.cpp:10-18): pencil_row = pencil_for(N), pencil_col =
+ * pencil_for(M). */
+typedef struct shlr_pi_args {
+  size_t m, n, j;              /* y is m x n x j                              */
+  const double* y;             /* interleaved complex, m*n*j                  */
+  const uint8_t* mask;         /* mask_rows x n                               */
+  size_t mask_rows;            /* 1 (line mask) or m                          */
+  const double* spirit_weights;/* k*k*j*j interleaved complex, the flat index
+                                  of SpiritKernels::raw() (spirit.hpp:21-29),
+                                  or NULL when enable_spirit == 0             */
+  size_t spirit_k;             /* kernel size (odd)                           */
+  const double* taps;          /* HankelConfig::filter_taps, interleaved      */
+  size_t ntaps;
+  size_t pencil_row, pencil_col;
+  double lambda, lambda1, beta, tau, tol, cg_tol;
+  size_t max_outer, cg_max;
+  int enable_spirit, enable_vc;
+  int debug_sv_iter;           /* >0: record singular values of L + D/beta at
+                                  this 1-based outer iteration (parity hook)  */
+} shlr_pi_args;
+
+/* Full parallel-imaging reconstruction, host buffers in and out.
+ * x_out: m*n*j interleaved complex (image domain, like the reference).
+ * sv_out (optional, with debug_sv_iter > 0): (m + n) * d doubles, rows first
+ * then columns, each row of d sorted descending, d = min(p, blocks*q) of that
+ * direction (row and column matrices must then share d).  log_cb may be NULL. */
+int shlr_cuda_pi_reconstruct(const shlr_pi_args* args, double* x_out,
+                             double* sv_out, shlr_stats* stats,
+                             shlr_log_fn log_cb, void* log_ctx);
+
+/* Resident-plan API: the same computation split into setup / iterate /
+ * download so that a caller (bench.py, a serving loop) keeps every buffer in
+ * HBM.  plan_run executes `iters` outer iterations (bounded by max_outer and
+ * the early-stop rule) on the plan's stream; it does not synchronise. */
+typedef struct shlr_pi_plan shlr_pi_plan;
+int shlr_cuda_pi_plan_create(const shlr_pi_args* args, shlr_pi_plan** out);
+int shlr_cuda_pi_plan_reset(shlr_pi_plan* plan);          /* back to iteration 0 */
+int shlr_cuda_pi_plan_run(shlr_pi_plan* plan, size_t iters);
+int shlr_cuda_pi_plan_sync(shlr_pi_plan* plan);
+/* Device time (ms) of the Hankel-SVT kernel over the last plan_run call
+ * (CUDA events on the plan's stream; 0 if not measured). */
+int shlr_cuda_pi_plan_timing(shlr_pi_plan* plan, double* svt_ms, double* total_ms,
+                             int* launches_per_iter);
+/* Timing mode: plan_run launches kernels directly (no CUDA graph) and times
+ * the Hankel-SVT launch of every iteration with CUDA events. */
+int shlr_cuda_pi_plan_set_timing(shlr_pi_plan* plan, int on);
+int shlr_cuda_pi_plan_download(shlr_pi_plan* plan, double* x_out, shlr_stats* stats,
+                               shlr_log_fn log_cb, void* log_ctx);
+void shlr_cuda_pi_plan_destroy(shlr_pi_plan* plan);
+
+/* Batched Hankel-SVT unit (BASELINE config 5): for each of `batch` matrices,
+ * lift_plain (proj/src/operators.cpp:93-103) the nc vectors of length n with
+ * pencil p, svt with threshold tau (solvers.cpp:11-21), adjoint_lift_plain
+ * (operators.cpp:105-119).  All pointers are DEVICE pointers to complex64
+ * (float2) data: vecs and out are batch x nc x n; sv_out (nullable) is
+ * batch x d floats, descending.  stream is a cudaStream_t (NULL = default). */
+int shlr_cuda_hankel_svt_batched(const void* vecs, int batch, int nc, int n, int p,
+                                 float tau, void* out, float* sv_out, void* stream);
+/* Same, host complex128 buffers in and out (the e2e path). */
+int shlr_cuda_hankel_svt_batched_host(const double* vecs, int batch, int nc, int n, int p,
+                                      double tau, double* out, double* sv_out);
+
+/* Hankel lift index map used by the device kernels, for bit-exact parity of
+ * the lift (operators.cpp:25-58, hankel.cpp:31-41,99-113).  For a p x
+ * (blocks*q) matrix built from `coils` vectors of length n (blocks = coils *
+ * (vc ? 2 : 1)), writes for every element (i, c), row-major, three int32:
+ * source coil, source index into that coil's spectrum, conj flag (1 for the
+ * conjugate-flipped virtual-coil blocks).  map must hold p*blocks*q*3 ints.
+ * Computed on the device with the kernels' own index function. */
+int shlr_cuda_lift_index_map(int n, int p, int coils, int vc, int32_t* map);
+
+/* Centered unitary FFT along one axis of a host complex128 tensor
+ * (proj/src/fft.cpp:100-128), computed on the device in complex64.
+ * dims has ndim entries; data is transformed in place. */
+int shlr_cuda_fft_along_axis(double* data, const size_t* dims, int ndim, int axis,
+                             int inverse);
+
+/* Measured FP32 CUDA-core peak of the current device (TFLOP/s): a
+ * register-resident FMA chain over all SMs, timed with CUDA events.  Used as
+ * the roofline denominator of the FP32 Hankel-SVT kernel. */
+int shlr_cuda_fp32_peak_tflops(double* tflops);
+
+/* Host-side helpers of the boundary (no GPU needed): the reference's mask
+ * generators (proj/src/sampling.cpp:31-173), bit-exact. */
+int shlr_mask_gauss_cartesian(size_t n, double rate, size_t acs, uint64_t seed,
+                              uint8_t* bits_out);
+int shlr_mask_random2d(size_t rows, size_t cols, double rate, size_t center,
+                       uint64_t seed, uint8_t* bits_out);
+int shlr_acs_range(size_t n, size_t acs, size_t* start, size_t* end);
+size_t shlr_pencil_for(size_t pencil, size_t len);
+/* SPIRiT kernel calibration (proj/src/spirit.cpp:22-94) on an a x b x j ACS
+ * block (interleaved complex, row-major): the Tikhonov filter
+ * s / (s^2 + mu^2), mu = tikhonov * s_max, computed as the equivalent ridge
+ * solve in FP64 on the host.  weights_out: k*k*j*j interleaved complex in
+ * SpiritKernels::raw() order.  Setup only (not on the per-iteration path). */
+int shlr_spirit_calibrate(const double* acs, size_t a, size_t b, size_t j, size_t k,
+                          double tikhonov, double* weights_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SHLR_CUDA_H */

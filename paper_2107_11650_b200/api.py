@@ -1,0 +1,329 @@
+"""Python mirror of the reference's reconstruction API over the C-ABI.
+
+Same names, argument meaning and error behaviour as ``proj/include/shlr``:
+
+* ``HankelConfig``   -- ``hankel.hpp:15-25`` (``pencil_for``: ``hankel.cpp:10-18``)
+* ``AdmmConfig``     -- ``solvers.hpp:16-34`` (``validate``: ``:29-33``)
+* ``SamplingMask``   -- ``sampling.hpp:33-52``
+* ``SpiritKernels``  -- ``spirit.hpp:12-36`` (weights ``(k, k, J, J)`` =
+  the flat index ``((di+h)*k + (dj+h))*J + src)*J + dst``)
+* ``shlr_pi_reconstruct`` -- ``solvers.hpp:64-70``; raises ``ValueError``
+  where the reference throws ``std::invalid_argument`` and
+  ``DivergenceError`` for ``shlr::DivergenceError``.
+* ``hankel_svt_batched`` -- the config-5 lift_plain -> svt -> adjoint unit.
+
+Everything numerical runs in ``lib/libshlr_b200.so`` on the GPU; this module
+only marshals arrays.  Complex inputs are complex128 (the reference's
+``std::complex<double>``); the device computes in complex64.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Callable, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from ._lib import (LOG_FN, SHLR_EDIVERGE, SHLR_EINVAL, SHLR_EUNSUPPORTED, SHLR_OK, ShlrPiArgs,
+                   ShlrStats, last_error, lib)
+
+
+class DivergenceError(RuntimeError):
+    """``shlr::DivergenceError`` (``solvers.hpp:41-43``)."""
+
+
+class CudaError(RuntimeError):
+    """CUDA failure or no device (the product path has no CPU fallback)."""
+
+
+def _check(rc: int, what: str) -> None:
+    if rc == SHLR_OK:
+        return
+    msg = f"{what}: {last_error()}"
+    if rc == SHLR_EINVAL:
+        raise ValueError(msg)
+    if rc == SHLR_EDIVERGE:
+        raise DivergenceError(msg)
+    if rc == SHLR_EUNSUPPORTED:
+        raise NotImplementedError(msg)
+    raise CudaError(msg)
+
+
+def device_count() -> int:
+    return int(lib.shlr_cuda_device_count())
+
+
+@dataclass
+class HankelConfig:
+    pencil: int = 0
+    pencil_param: int = 0
+    filter_taps: Sequence[complex] = (1.0 + 0j, -1.0 + 0j)
+    virtual_coil: bool = False
+
+    def pencil_for(self, length: int) -> int:
+        p = int(lib.shlr_pencil_for(self.pencil, length))
+        if p == 0:
+            raise ValueError("HankelConfig: pencil exceeds signal length")
+        return p
+
+
+@dataclass
+class AdmmConfig:
+    lam: float = 1e4
+    lambda1: float = 1e2
+    lambda2: float = 2.0
+    beta: float = 1.0
+    tau: float = 1.0
+    max_outer: int = 50
+    tol: float = 1e-6
+    cg_max: int = 15
+    cg_tol: float = 1e-8
+    enable_spirit: bool = False
+    enable_vc: bool = False
+
+    def validate(self) -> None:
+        if (self.lam <= 0 or self.lambda1 < 0 or self.lambda2 < 0 or self.beta <= 0
+                or self.tau <= 0 or self.tol <= 0 or self.cg_tol <= 0):
+            raise ValueError("AdmmConfig: invalid parameter")
+
+
+@dataclass
+class SamplingMask:
+    rows: int
+    cols: int
+    bits: np.ndarray  # uint8 (rows, cols)
+    generator: str = ""
+    seed: int = 0
+    rate: float = 0.0
+    acs: int = 0
+
+    def count(self) -> int:
+        return int(np.count_nonzero(self.bits))
+
+
+@dataclass
+class SpiritKernels:
+    kernel_size: int
+    coils: int
+    weights: np.ndarray  # complex (k, k, J, J)
+
+
+@dataclass
+class SolveStats:
+    outer_iters: int = 0
+    final_rel_change: float = 0.0
+
+
+def acs_range(n: int, acs: int) -> Tuple[int, int]:
+    a0, a1 = C.c_size_t(), C.c_size_t()
+    _check(lib.shlr_acs_range(n, acs, C.byref(a0), C.byref(a1)), "acs_range")
+    return a0.value, a1.value
+
+
+def mask_gauss_cartesian(n: int, rate: float, acs: int, seed: int) -> SamplingMask:
+    bits = np.zeros(n, np.uint8)
+    _check(lib.shlr_mask_gauss_cartesian(n, rate, acs, seed,
+                                         bits.ctypes.data_as(C.POINTER(C.c_uint8))),
+           "mask_gauss_cartesian")
+    return SamplingMask(1, n, bits.reshape(1, n), "gauss_cartesian", seed, rate, acs)
+
+
+def mask_random2d(rows: int, cols: int, rate: float, center: int, seed: int) -> SamplingMask:
+    bits = np.zeros(rows * cols, np.uint8)
+    _check(lib.shlr_mask_random2d(rows, cols, rate, center, seed,
+                                  bits.ctypes.data_as(C.POINTER(C.c_uint8))), "mask_random2d")
+    return SamplingMask(rows, cols, bits.reshape(rows, cols), "random2d", seed, rate, center)
+
+
+def spirit_calibrate(acs: np.ndarray, kernel_size: int = 5, tikhonov: float = 1e-4) -> SpiritKernels:
+    """``shlr::spirit_calibrate`` (``spirit.hpp:62-64``) on an a x b x J ACS block."""
+    blk = _c128(acs)
+    if blk.ndim != 3:
+        raise ValueError("spirit_calibrate: expected a x b x J ACS")
+    a, b, j = blk.shape
+    w = np.zeros((kernel_size, kernel_size, j, j), np.complex128)
+    _check(lib.shlr_spirit_calibrate(_dptr(blk), a, b, j, kernel_size, tikhonov, _dptr(w)),
+           "spirit_calibrate")
+    return SpiritKernels(kernel_size, j, w)
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _c128(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.complex128))
+
+
+def _pi_args(y: np.ndarray, mask: SamplingMask, g: Optional[SpiritKernels], hcfg: HankelConfig,
+             acfg: AdmmConfig, debug_sv_iter: int, keep: list) -> ShlrPiArgs:
+    acfg.validate()
+    if y.ndim != 3:
+        raise ValueError("shlr_pi_reconstruct: expected M x N x J")
+    if acfg.enable_spirit and g is None:
+        raise ValueError("shlr_pi_reconstruct: spirit enabled without kernels")
+    m, n, j = y.shape
+    if mask.cols != n or (mask.rows != 1 and mask.rows != m):
+        raise ValueError("shlr_pi_reconstruct: mask dims mismatch")
+    use_spirit = acfg.enable_spirit and acfg.lambda1 > 0.0
+    if use_spirit and g.coils != j:
+        raise ValueError("shlr_pi_reconstruct: kernel coil mismatch")
+    yc = _c128(y)
+    bits = np.ascontiguousarray(mask.bits, dtype=np.uint8)
+    taps = _c128(list(hcfg.filter_taps))
+    keep += [yc, bits, taps]
+    a = ShlrPiArgs()
+    a.m, a.n, a.j = m, n, j
+    a.y = _dptr(yc)
+    a.mask = bits.ctypes.data_as(C.POINTER(C.c_uint8))
+    a.mask_rows = mask.rows
+    if use_spirit:
+        w = _c128(g.weights)
+        keep.append(w)
+        a.spirit_weights = _dptr(w)
+        a.spirit_k = g.kernel_size
+    a.taps = _dptr(taps)
+    a.ntaps = len(hcfg.filter_taps)
+    a.pencil_row = hcfg.pencil_for(n)
+    a.pencil_col = hcfg.pencil_for(m)
+    a.lam, a.lambda1, a.beta, a.tau = acfg.lam, acfg.lambda1, acfg.beta, acfg.tau
+    a.tol, a.cg_tol = acfg.tol, acfg.cg_tol
+    a.max_outer, a.cg_max = acfg.max_outer, acfg.cg_max
+    a.enable_spirit, a.enable_vc = int(acfg.enable_spirit), int(acfg.enable_vc)
+    a.debug_sv_iter = int(debug_sv_iter)
+    return a
+
+
+def shlr_pi_reconstruct(y: np.ndarray, mask: SamplingMask, g: Optional[SpiritKernels],
+                        hcfg: HankelConfig, acfg: AdmmConfig,
+                        log: Optional[List[str]] = None, stats: Optional[SolveStats] = None,
+                        debug_sv_iter: int = 0, sv_out: Optional[list] = None) -> np.ndarray:
+    """``shlr::shlr_pi_reconstruct`` (``solvers.hpp:64-70``) on the GPU."""
+    keep: list = []
+    a = _pi_args(y, mask, g, hcfg, acfg, debug_sv_iter, keep)
+    m, n, j = y.shape
+    x = np.empty((m, n, j), np.complex128)
+    st = ShlrStats()
+    lines: List[str] = []
+
+    @LOG_FN
+    def _cb(_ctx, line):
+        lines.append(line.decode())
+
+    sv = None
+    if debug_sv_iter > 0:
+        qr = n - a.pencil_row + 1
+        blocks = j * (2 if acfg.enable_vc else 1)
+        d = min(a.pencil_row, blocks * qr)
+        sv = np.zeros((m + n, d), np.float64)
+    rc = lib.shlr_cuda_pi_reconstruct(C.byref(a), _dptr(x), _dptr(sv) if sv is not None else None,
+                                      C.byref(st), _cb, None)
+    if log is not None:
+        log.extend(lines)
+    if stats is not None:
+        stats.outer_iters = int(st.outer_iters)
+        stats.final_rel_change = float(st.final_rel_change)
+    _check(rc, "shlr_pi_reconstruct")
+    if sv_out is not None and sv is not None:
+        sv_out.append(sv)
+    return x
+
+
+class PiPlan:
+    """Resident plan (``shlr_cuda_pi_plan_*``): inputs uploaded once, the
+    ADMM iterations run on-device, results downloaded on demand."""
+
+    def __init__(self, y, mask, g, hcfg, acfg):
+        self._keep: list = []
+        self._args = _pi_args(y, mask, g, hcfg, acfg, 0, self._keep)
+        self.shape = y.shape
+        self._h = C.c_void_p()
+        _check(lib.shlr_cuda_pi_plan_create(C.byref(self._args), C.byref(self._h)), "plan_create")
+
+    def reset(self):
+        _check(lib.shlr_cuda_pi_plan_reset(self._h), "plan_reset")
+
+    def run(self, iters: int):
+        _check(lib.shlr_cuda_pi_plan_run(self._h, iters), "plan_run")
+
+    def sync(self):
+        _check(lib.shlr_cuda_pi_plan_sync(self._h), "plan_sync")
+
+    def set_timing(self, on: bool):
+        _check(lib.shlr_cuda_pi_plan_set_timing(self._h, int(on)), "plan_set_timing")
+
+    def timing(self):
+        s, t, n = C.c_double(), C.c_double(), C.c_int()
+        _check(lib.shlr_cuda_pi_plan_timing(self._h, C.byref(s), C.byref(t), C.byref(n)), "timing")
+        return s.value, t.value, n.value
+
+    def download(self, log: Optional[List[str]] = None) -> Tuple[np.ndarray, SolveStats]:
+        x = np.empty(self.shape, np.complex128)
+        st = ShlrStats()
+        lines: List[str] = []
+
+        @LOG_FN
+        def _cb(_ctx, line):
+            lines.append(line.decode())
+
+        rc = lib.shlr_cuda_pi_plan_download(self._h, _dptr(x), C.byref(st), _cb, None)
+        if log is not None:
+            log.extend(lines)
+        _check(rc, "plan_download")
+        return x, SolveStats(int(st.outer_iters), float(st.final_rel_change))
+
+    def close(self):
+        if self._h:
+            lib.shlr_cuda_pi_plan_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def fp32_peak_tflops() -> float:
+    v = C.c_double()
+    _check(lib.shlr_cuda_fp32_peak_tflops(C.byref(v)), "fp32_peak")
+    return v.value
+
+
+def hankel_svt_batched(vecs: np.ndarray, p: int, tau: float) -> Tuple[np.ndarray, np.ndarray]:
+    """Config-5 unit on host complex128 arrays: vecs (B, Nc, N) ->
+    (adjoint vectors (B, Nc, N), singular values (B, d) descending)."""
+    v = _c128(vecs)
+    b, nc, n = v.shape
+    q = n - p + 1
+    d = min(p, nc * q)
+    out = np.empty_like(v)
+    sv = np.empty((b, d), np.float64)
+    _check(lib.shlr_cuda_hankel_svt_batched_host(_dptr(v), b, nc, n, p, tau, _dptr(out), _dptr(sv)),
+           "hankel_svt_batched")
+    return out, sv
+
+
+def hankel_svt_batched_device(vecs_ptr: int, batch: int, nc: int, n: int, p: int, tau: float,
+                              out_ptr: int, sv_ptr: int = 0, stream: int = 0) -> None:
+    """Device-pointer variant (complex64 data already resident in HBM)."""
+    _check(lib.shlr_cuda_hankel_svt_batched(C.c_void_p(vecs_ptr), batch, nc, n, p, tau,
+                                            C.c_void_p(out_ptr), C.c_void_p(sv_ptr or None),
+                                            C.c_void_p(stream or None)), "hankel_svt_batched")
+
+
+def lift_index_map(n: int, p: int, coils: int, vc: bool) -> np.ndarray:
+    q = n - p + 1
+    blocks = coils * (2 if vc else 1)
+    out = np.empty((p, blocks * q, 3), np.int32)
+    _check(lib.shlr_cuda_lift_index_map(n, p, coils, int(vc), out.ctypes.data_as(C.POINTER(C.c_int32))),
+           "lift_index_map")
+    return out
+
+
+def fft_along_axis(x: np.ndarray, axis: int, inverse: bool) -> np.ndarray:
+    a = _c128(x).copy()
+    dims = (C.c_size_t * a.ndim)(*a.shape)
+    _check(lib.shlr_cuda_fft_along_axis(_dptr(a), dims, a.ndim, axis, int(inverse)),
+           "fft_along_axis")
+    return a

@@ -1,0 +1,293 @@
+// extern "C" boundary (include/shlr_cuda.h).  Every entry point converts C++
+// exceptions into return codes; no CPU fallback exists anywhere behind it.
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/shlr_cuda.h"
+#include "pi_solver.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+template <class Fn>
+int guarded(Fn&& fn) {
+  g_last_error.clear();
+  try {
+    return fn();
+  } catch (const shlr_b200::InvalidArg& e) {
+    return fail(SHLR_EINVAL, e.what());
+  } catch (const shlr_b200::Unsupported& e) {
+    return fail(SHLR_EUNSUPPORTED, e.what());
+  } catch (const shlr_b200::CudaError& e) {
+    return fail(SHLR_ECUDA, e.what());
+  } catch (const std::exception& e) {
+    return fail(SHLR_ECUDA, e.what());
+  }
+}
+
+int require_device() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    throw shlr_b200::CudaError("no CUDA device visible: the SHLR B200 path has no CPU fallback");
+  }
+  return n;
+}
+
+// Mirrors AdmmConfig::validate (solvers.hpp:29-33) and the argument checks
+// of shlr_pi_reconstruct (solvers.cpp:101-123).
+void validate_pi(const shlr_pi_args* a) {
+  using shlr_b200::InvalidArg;
+  if (!a) throw InvalidArg("shlr_pi_reconstruct: null args");
+  if (a->lambda <= 0 || a->lambda1 < 0 || a->beta <= 0 || a->tau <= 0 || a->tol <= 0 ||
+      a->cg_tol <= 0)
+    throw InvalidArg("AdmmConfig: invalid parameter");
+  if (a->m == 0 || a->n == 0 || a->j == 0 || !a->y)
+    throw InvalidArg("shlr_pi_reconstruct: expected M x N x J");
+  if (a->enable_spirit && !a->spirit_weights)
+    throw InvalidArg("shlr_pi_reconstruct: spirit enabled without kernels");
+  if (!a->mask || (a->mask_rows != 1 && a->mask_rows != a->m))
+    throw InvalidArg("shlr_pi_reconstruct: mask dims mismatch");
+  if (a->pencil_row < 1 || a->pencil_row > a->n || a->pencil_col < 1 || a->pencil_col > a->m)
+    throw InvalidArg("HankelConfig: pencil exceeds signal length");
+  if (!a->taps || a->ntaps == 0 || a->ntaps > a->n || a->ntaps > a->m)
+    throw InvalidArg("weights_from_filter: taps invalid");
+  if (a->enable_spirit && (a->spirit_k % 2 == 0 || a->spirit_k == 0))
+    throw InvalidArg("SpiritKernels: kernel size must be odd");
+}
+
+shlr_b200::PiConfig config_of(const shlr_pi_args* a) {
+  shlr_b200::PiConfig c{};
+  c.M = (int)a->m;
+  c.N = (int)a->n;
+  c.J = (int)a->j;
+  c.Pr = (int)a->pencil_row;
+  c.Pc = (int)a->pencil_col;
+  c.vc = a->enable_vc != 0;
+  // solvers.cpp:118-119: lambda1 is used only with SPIRiT enabled and > 0.
+  c.spirit = a->enable_spirit != 0 && a->lambda1 > 0.0;
+  c.lambda = a->lambda;
+  c.lambda1 = c.spirit ? a->lambda1 : 0.0;
+  c.beta = a->beta;
+  c.tau = a->tau;
+  c.tol = a->tol;
+  c.cg_tol = a->cg_tol;
+  c.max_outer = (int)a->max_outer;
+  c.cg_max = (int)a->cg_max;
+  c.debug_sv_iter = a->debug_sv_iter;
+  return c;
+}
+
+}  // namespace
+
+struct shlr_pi_plan {
+  shlr_b200::PiPlan* impl;
+};
+
+extern "C" {
+
+int shlr_cuda_abi_version(void) { return SHLR_ABI_VERSION; }
+
+const char* shlr_cuda_last_error(void) { return g_last_error.c_str(); }
+
+int shlr_cuda_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int shlr_cuda_pi_plan_create(const shlr_pi_args* args, shlr_pi_plan** out) {
+  return guarded([&] {
+    validate_pi(args);
+    if (!out) throw shlr_b200::InvalidArg("null plan pointer");
+    require_device();
+    auto cfg = config_of(args);
+    auto* impl = new shlr_b200::PiPlan(cfg, args->y, args->mask, args->mask_rows, args->taps,
+                                       args->ntaps, cfg.spirit ? args->spirit_weights : nullptr,
+                                       args->spirit_k);
+    *out = new shlr_pi_plan{impl};
+    return SHLR_OK;
+  });
+}
+
+int shlr_cuda_pi_plan_reset(shlr_pi_plan* plan) {
+  return guarded([&] {
+    if (!plan) throw shlr_b200::InvalidArg("null plan");
+    plan->impl->reset();
+    return SHLR_OK;
+  });
+}
+
+int shlr_cuda_pi_plan_run(shlr_pi_plan* plan, size_t iters) {
+  return guarded([&] {
+    if (!plan) throw shlr_b200::InvalidArg("null plan");
+    plan->impl->run(iters);
+    return SHLR_OK;
+  });
+}
+
+int shlr_cuda_pi_plan_sync(shlr_pi_plan* plan) {
+  return guarded([&] {
+    if (!plan) throw shlr_b200::InvalidArg("null plan");
+    plan->impl->sync();
+    return SHLR_OK;
+  });
+}
+
+int shlr_cuda_pi_plan_timing(shlr_pi_plan* plan, double* svt_ms, double* total_ms,
+                             int* launches_per_iter) {
+  return guarded([&] {
+    if (!plan) throw shlr_b200::InvalidArg("null plan");
+    if (svt_ms) *svt_ms = plan->impl->svt_ms();
+    if (total_ms) *total_ms = plan->impl->total_ms();
+    if (launches_per_iter) *launches_per_iter = plan->impl->launches_per_iter();
+    return SHLR_OK;
+  });
+}
+
+int shlr_cuda_pi_plan_download(shlr_pi_plan* plan, double* x_out, shlr_stats* stats,
+                               shlr_log_fn log_cb, void* log_ctx) {
+  return guarded([&] {
+    if (!plan || !x_out) throw shlr_b200::InvalidArg("null plan/output");
+    size_t outer = 0;
+    double rel = 0;
+    int err = 0;
+    std::vector<std::string> lines;
+    plan->impl->download(x_out, &outer, &rel, &lines, &err);
+    if (log_cb)
+      for (const auto& l : lines) log_cb(log_ctx, l.c_str());
+    if (stats) {
+      stats->outer_iters = outer;
+      stats->final_rel_change = rel;
+    }
+    if (err == 1) return fail(SHLR_EDIVERGE, "cg_solve: non-finite residual");
+    if (err == 2) return fail(SHLR_EDIVERGE, "cg_solve: operator not positive definite");
+    return SHLR_OK;
+  });
+}
+
+int shlr_cuda_pi_plan_set_timing(shlr_pi_plan* plan, int on) {
+  return guarded([&] {
+    if (!plan) throw shlr_b200::InvalidArg("null plan");
+    plan->impl->set_timing(on != 0);
+    return SHLR_OK;
+  });
+}
+
+int shlr_cuda_fp32_peak_tflops(double* tflops) {
+  return guarded([&] {
+    if (!tflops) throw shlr_b200::InvalidArg("null output");
+    require_device();
+    *tflops = shlr_b200::fp32_peak_probe();
+    return SHLR_OK;
+  });
+}
+
+void shlr_cuda_pi_plan_destroy(shlr_pi_plan* plan) {
+  if (!plan) return;
+  delete plan->impl;
+  delete plan;
+}
+
+int shlr_cuda_pi_reconstruct(const shlr_pi_args* args, double* x_out, double* sv_out,
+                             shlr_stats* stats, shlr_log_fn log_cb, void* log_ctx) {
+  shlr_pi_plan* plan = nullptr;
+  int rc = shlr_cuda_pi_plan_create(args, &plan);
+  if (rc != SHLR_OK) return rc;
+  rc = shlr_cuda_pi_plan_run(plan, args->max_outer);
+  if (rc == SHLR_OK) rc = shlr_cuda_pi_plan_sync(plan);
+  if (rc == SHLR_OK) rc = shlr_cuda_pi_plan_download(plan, x_out, stats, log_cb, log_ctx);
+  if ((rc == SHLR_OK || rc == SHLR_EDIVERGE) && sv_out && args->debug_sv_iter > 0) {
+    const int rc2 = guarded([&] {
+      plan->impl->download_sv(sv_out);
+      return SHLR_OK;
+    });
+    if (rc == SHLR_OK) rc = rc2;
+  }
+  std::string err = g_last_error;
+  shlr_cuda_pi_plan_destroy(plan);
+  g_last_error = err;
+  return rc;
+}
+
+int shlr_cuda_hankel_svt_batched(const void* vecs, int batch, int nc, int n, int p, float tau,
+                                 void* out, float* sv_out, void* stream) {
+  return guarded([&] {
+    if (batch < 0 || nc < 1 || n < 1 || p < 1 || p > n || tau < 0 || !vecs || !out)
+      throw shlr_b200::InvalidArg("hankel_svt_batched: invalid arguments");
+    require_device();
+    shlr_b200::hankel_svt_batched_device(static_cast<const float2*>(vecs), batch, nc, n, p, tau,
+                                         static_cast<float2*>(out), sv_out,
+                                         static_cast<cudaStream_t>(stream));
+    return SHLR_OK;
+  });
+}
+
+int shlr_cuda_hankel_svt_batched_host(const double* vecs, int batch, int nc, int n, int p,
+                                      double tau, double* out, double* sv_out) {
+  return guarded([&] {
+    if (batch < 0 || nc < 1 || n < 1 || p < 1 || p > n || tau < 0 || !vecs || !out)
+      throw shlr_b200::InvalidArg("hankel_svt_batched: invalid arguments");
+    require_device();
+    const size_t tot = (size_t)batch * nc * n;
+    const int q = n - p + 1;
+    const int d = std::min(p, nc * q);
+    std::vector<float2> h(tot);
+    for (size_t i = 0; i < tot; ++i) h[i] = make_float2((float)vecs[2 * i], (float)vecs[2 * i + 1]);
+    float2 *dv = nullptr, *dout = nullptr;
+    float* dsv = nullptr;
+    SHLR_CUDA(cudaMalloc(&dv, std::max<size_t>(tot, 1) * sizeof(float2)));
+    SHLR_CUDA(cudaMalloc(&dout, std::max<size_t>(tot, 1) * sizeof(float2)));
+    if (sv_out) SHLR_CUDA(cudaMalloc(&dsv, std::max<size_t>((size_t)batch * d, 1) * sizeof(float)));
+    SHLR_CUDA(cudaMemcpy(dv, h.data(), tot * sizeof(float2), cudaMemcpyHostToDevice));
+    shlr_b200::hankel_svt_batched_device(dv, batch, nc, n, p, (float)tau, dout, dsv, nullptr);
+    SHLR_CUDA(cudaMemcpy(h.data(), dout, tot * sizeof(float2), cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < tot; ++i) {
+      out[2 * i] = h[i].x;
+      out[2 * i + 1] = h[i].y;
+    }
+    if (sv_out) {
+      std::vector<float> s((size_t)batch * d);
+      SHLR_CUDA(cudaMemcpy(s.data(), dsv, s.size() * sizeof(float), cudaMemcpyDeviceToHost));
+      for (size_t i = 0; i < s.size(); ++i) sv_out[i] = s[i];
+    }
+    cudaFree(dv);
+    cudaFree(dout);
+    if (dsv) cudaFree(dsv);
+    return SHLR_OK;
+  });
+}
+
+int shlr_cuda_lift_index_map(int n, int p, int coils, int vc, int32_t* map) {
+  return guarded([&] {
+    if (n < 1 || p < 1 || p > n || coils < 1 || !map)
+      throw shlr_b200::InvalidArg("lift_index_map: invalid arguments");
+    require_device();
+    shlr_b200::lift_index_map_device(n, p, coils, vc, map);
+    return SHLR_OK;
+  });
+}
+
+int shlr_cuda_fft_along_axis(double* data, const size_t* dims, int ndim, int axis, int inverse) {
+  return guarded([&] {
+    if (!data || !dims || ndim < 1) throw shlr_b200::InvalidArg("fft: invalid arguments");
+    for (int i = 0; i < ndim; ++i)
+      if (dims[i] == 0) throw shlr_b200::InvalidArg("fft: empty input");
+    require_device();
+    shlr_b200::fft_along_axis_host(data, dims, ndim, axis, inverse != 0);
+    return SHLR_OK;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,87 @@
+// Fused batched Hankel-SVT kernel: one CTA per lifted matrix.
+//
+// Per matrix (proj/src/solvers.cpp:172-181 for the ADMM mode, and the
+// lift_plain -> svt -> adjoint_lift_plain composition of solvers.cpp:264-282
+// for the plain mode):
+//   0. stage the J coil spectra of one k-space row/column in smem, weighted by
+//      the centred filter spectrum wc and, with virtual coils, conjugate-
+//      flipped (lift_weighted, operators.cpp:25-58);
+//   1. Gram  G = Ahat^H Ahat  (FP32 FMA), Ahat = L + D/beta streamed in row
+//      chunks of R (Ahat = A for tall A, A^H for wide A; d = min(m, n));
+//   2. cyclic parallel two-sided Jacobi on G (Brent-Luk ring ordering): G in
+//      smem (upper representation, stride d+1 so row and column walks are
+//      bank-conflict free), V in registers, 4 threads per row of V, one ring
+//      shift per round done with register moves and width-4 shuffles;
+//   3. f = (1 - tau/sigma)_+ and W = V diag(f) V^H (W replaces G in smem);
+//   4. Zhat = Ahat W per chunk, fused dual update D += tau_d (L - Z), and
+//      T = Z - D/beta (ADMM) or T = Z (plain);
+//   5. Hankel adjoint of T (deterministic anti-diagonal sums, no atomics) and
+//      the adjoint weighting conj(wc) (+ virtual-coil dagger)
+//      (adjoint_lift_weighted, operators.cpp:60-91).
+// Output is the k-space contribution of this row/column to the next RHS.
+#pragma once
+
+#include "common.cuh"
+
+namespace shlr_b200 {
+
+enum SvtMode : int { SVT_ADMM_WEIGHTED = 0, SVT_PLAIN = 1, SVT_ADMM_PLAIN = 2 };
+
+struct SvtFamily {
+  int count;           // matrices in this family
+  int len;             // vector length (N for rows, M for columns)
+  int P;               // pencil = rows of A
+  int q;               // len - P + 1
+  int J;               // coils
+  int B;               // blocks = J * (vc ? 2 : 1)
+  int vc;
+  int wide;            // 1: B*q > P, Ahat = A^H
+  int e, d;            // e = max(P, B*q), d = min(P, B*q)
+  // spectra in: element (mat, n, j) at spec[mat*s_mat + n*s_n + j*s_j]
+  const float2* spec;
+  long long s_mat, s_n, s_j;
+  // adjoint out, same addressing convention
+  float2* out;
+  long long o_mat, o_n, o_j;
+  const float2* wc;    // centred weights (len) for weighted modes
+  float2* D;           // duals, per matrix e*d row-major (Ahat orientation)
+  float* sv;           // optional: count x d singular values (descending)
+};
+
+struct SvtParams {
+  SvtFamily fam[2];
+  int nfam;
+  int mode;
+  float inv_beta;      // 1/beta
+  float tau_dual;      // ADMM multiplier step tau
+  float thresh;        // SVT threshold (1/beta or lambda2/beta or user tau)
+  int max_sweeps;
+  const int* skip;     // optional device flag: nonzero -> kernel is a no-op
+};
+
+// Index function shared by the kernel and shlr_cuda_lift_index_map: source
+// of element (i, c) of the p x (blocks*q) weighted lift (operators.cpp:36-56,
+// hankel.cpp:31-41): regular block b < J reads coil b at i + t; vc block
+// b >= J reads coil b - J at dagger_src(i + t) with conjugation.
+struct LiftSrc {
+  int coil, idx, conj;
+};
+__host__ __device__ __forceinline__ LiftSrc lift_source(int i, int c, int q, int J, int len) {
+  const int b = c / q, t = c - b * q;
+  LiftSrc s;
+  if (b < J) {
+    s.coil = b;
+    s.idx = i + t;
+    s.conj = 0;
+  } else {
+    s.coil = b - J;
+    s.idx = dagger_src(i + t, len);
+    s.conj = 1;
+  }
+  return s;
+}
+
+size_t svt_smem_bytes(int DP, int R, int maxB, int maxLen);
+void launch_hankel_svt(const SvtParams& prm, int total_matrices, cudaStream_t stream);
+
+}  // namespace shlr_b200

@@ -1,0 +1,1125 @@
+// Parallel-imaging ADMM on the device (see pi_solver.cuh).
+//
+// State lives in centred 2D k-space (X^ = F2D x, F2D unitary): without the
+// SPIRiT term the X-update normal operator of normal_apply
+// (proj/src/operators.cpp:213-248) is the diagonal
+//   lambda U(k0,k1) + beta a_N(k1) + beta a_M(k0),  a_n(k) = |wc[k]|^2 counts[k]
+// (+ the virtual-coil mirror term), so the capped, warm-started CG of
+// cg_solve (proj/src/solvers.cpp:23-67) is replayed exactly -- same
+// iteration count rule, same real pairing, same break and divergence tests --
+// on elementwise kernels with deterministic FP64 block reductions.  With
+// SPIRiT the operator adds lambda1 F2D P F2D^-1 with P = (G-I)^H (G-I) per
+// pixel (proj/src/spirit.cpp:151-165), applied as row iFFT -> fused column
+// (iFFT, J x J matvec, FFT) -> row FFT.
+#include "pi_solver.cuh"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+
+namespace shlr_b200 {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+// ------------------------------------------------------------ reductions
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Deterministic block sum (valid in thread 0).
+__device__ double block_sum(double v, double* sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  const int nw = (blockDim.x + 31) >> 5;
+  double t = 0.0;
+  if (warp == 0) {
+    t = lane < nw ? sh[lane] : 0.0;
+    t = warp_sum(t);
+  }
+  return t;
+}
+
+// Publishes `nv` per-block values and returns true in the last block to
+// arrive; that block then sums partials in a fixed order.
+__device__ bool publish_and_check_last(double* partials, int nblocks, const double* vals, int nv,
+                                       unsigned int* counter) {
+  __shared__ bool s_last;
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < nv; ++k) partials[k * nblocks + blockIdx.x] = vals[k];
+    __threadfence();
+    const unsigned int prev = atomicAdd(counter, 1u);
+    s_last = (prev == (unsigned int)(nblocks - 1));
+  }
+  __syncthreads();
+  return s_last;
+}
+
+__device__ double sum_partials(const double* partials, int nblocks, int slot, double* sh) {
+  double v = 0.0;
+  for (int b = threadIdx.x; b < nblocks; b += blockDim.x) v += __ldcg(partials + slot * nblocks + b);
+  return block_sum(v, sh);
+}
+
+__device__ __forceinline__ bool halted(const SolverCtl* c) { return c->stopped || c->error; }
+
+// ------------------------------------------------------------ setup kernels
+__global__ void k_init_data(const double* __restrict__ y, const uint8_t* __restrict__ mask,
+                            int mask_rows, int M, int N, int J, double lambda,
+                            float2* __restrict__ x0, float2* __restrict__ yk) {
+  const size_t nel = (size_t)M * N * J;
+  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < nel;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    const size_t pix = idx / J;
+    const int m = (int)(pix / N), n = (int)(pix % N);
+    const bool s = mask[(mask_rows == 1 ? 0 : m) * (size_t)N + n] != 0;
+    const double re = s ? y[2 * idx] : 0.0, im = s ? y[2 * idx + 1] : 0.0;
+    x0[idx] = make_float2((float)re, (float)im);
+    yk[idx] = make_float2((float)(lambda * re), (float)(lambda * im));
+  }
+}
+
+__global__ void k_fill(float2* __restrict__ p, size_t n, float2 v) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+__global__ void k_copy(float2* __restrict__ dst, const float2* __restrict__ src, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
+// H0 broadcast: hrow[r][n][j] = hN[n]; hcol[k0][c][j] = hM[k0].
+__global__ void k_init_h(float2* __restrict__ hrow, float2* __restrict__ hcol,
+                         const float2* __restrict__ hN, const float2* __restrict__ hM, int M, int N,
+                         int J) {
+  const size_t nel = (size_t)M * N * J;
+  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < nel;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    const size_t pix = idx / J;
+    const int m = (int)(pix / N), n = (int)(pix % N);
+    hrow[idx] = hN[n];
+    hcol[idx] = hM[m];
+  }
+}
+
+__global__ void k_reset_ctl(SolverCtl* c) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) memset(c, 0, sizeof(SolverCtl));
+}
+
+// SPIRiT: conv planes [M][N][J*J] in k-space (spirit.cpp:104-135 with
+// k1 = fft2c(ones) = sqrt(MN) delta at (floor(M/2), floor(N/2))).
+__global__ void k_spirit_conv(const double* __restrict__ w, int k, int M, int N, int J,
+                              float2* __restrict__ conv) {
+  const int JJ = J * J;
+  const size_t nel = (size_t)M * N * JJ;
+  const int h = k / 2;
+  const double s = sqrt((double)M * (double)N);
+  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < nel;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    const int pl = (int)(idx % JJ);
+    const size_t pix = idx / JJ;
+    const int r = (int)(pix / N), c = (int)(pix % N);
+    const int src = pl / J, dst = pl % J;
+    double re = 0, im = 0;
+    for (int di = -h; di <= h; ++di) {
+      if ((((r + di) % M) + M) % M != M / 2) continue;
+      for (int dj = -h; dj <= h; ++dj) {
+        if ((((c + dj) % N) + N) % N != N / 2) continue;
+        const size_t wi = ((((size_t)(di + h) * k + (dj + h)) * J + src) * J + dst);
+        re += w[2 * wi] * s;
+        im += w[2 * wi + 1] * s;
+      }
+    }
+    conv[idx] = make_float2((float)re, (float)im);
+  }
+}
+
+// P = (G - I)^H (G - I) per pixel, G[dst][src] = map[src*J + dst].
+__global__ void k_spirit_pmat(const float2* __restrict__ maps, int npix, int J,
+                              float2* __restrict__ pm) {
+  const int JJ = J * J;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < (size_t)npix * JJ;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const size_t pix = t / JJ;
+    const int a = (int)(t % JJ) / J, b = (int)(t % JJ) % J;
+    const float2* mp = maps + pix * JJ;
+    float2 acc = make_float2(0.f, 0.f);
+    for (int dst = 0; dst < J; ++dst) {
+      float2 ga = mp[a * J + dst];
+      float2 gb = mp[b * J + dst];
+      if (dst == a) ga.x -= 1.f;
+      if (dst == b) gb.x -= 1.f;
+      cfmac(acc, ga, gb);  // conj(Gm1[dst][a]) * Gm1[dst][b]
+    }
+    pm[t] = acc;
+  }
+}
+
+// ------------------------------------------------------------ FFT ops
+struct CopyOpCtl {
+  const float2* in;
+  float2* out;
+  long long so, sk, si;
+  const SolverCtl* ctl;
+  __device__ bool skip() const { return ctl && halted(ctl); }
+  __device__ float2 load(int o, int k, int i) const { return in[o * so + k * sk + i * si]; }
+  __device__ void store(int o, int k, int i, float2 v) const { out[o * so + k * sk + i * si] = v; }
+};
+
+// b^ = yk + beta (F0(hrow) + tmp), transform along axis 0 of [M][N*J].
+struct RhsOp {
+  const float2* hrow;
+  const float2* tmp;
+  const float2* yk;
+  float2* bk;
+  long long NJ;
+  float beta;
+  const SolverCtl* ctl;
+  __device__ bool skip() const { return halted(ctl); }
+  __device__ float2 load(int, int k, int i) const { return hrow[k * NJ + i]; }
+  __device__ void store(int, int k, int i, float2 v) const {
+    const long long idx = k * NJ + i;
+    const float2 t = tmp[idx], y = yk[idx];
+    bk[idx] = make_float2(fmaf(beta, v.x + t.x, y.x), fmaf(beta, v.y + t.y, y.y));
+  }
+};
+
+// First SPIRiT stage: p = r + gamma p (or x for the initial residual), then
+// the row iFFT of it into tmp.
+struct SpiritRowInvOp {
+  const float2* r;
+  float2* p;
+  const float2* x;   // non-null: apply to x instead of p
+  float2* tmp;
+  long long NJ, J;
+  const SolverCtl* ctl;
+  __device__ bool skip() const { return halted(ctl) || (x == nullptr && ctl->cg.done); }
+  __device__ float2 load(int o, int k, int i) const {
+    const long long idx = o * NJ + k * J + i;
+    if (x) return x[idx];
+    float2 v = r[idx];
+    if (ctl->cg.it > 0) {
+      const float g = (float)ctl->cg.gamma;
+      const float2 pv = p[idx];
+      v = make_float2(fmaf(g, pv.x, v.x), fmaf(g, pv.y, v.y));
+    }
+    p[idx] = v;
+    return v;
+  }
+  __device__ void store(int o, int k, int i, float2 v) const { tmp[o * NJ + k * J + i] = v; }
+};
+
+// ------------------------------------------------------------ CG kernels
+// Diagonal-operator variants (no SPIRiT).
+__global__ void k_cg_init_diag(const float2* __restrict__ bk, const float* __restrict__ dg,
+                               float2* __restrict__ x, float2* __restrict__ xold,
+                               float2* __restrict__ r, size_t nel, int J, SolverCtl* ctl,
+                               double* partials, double cg_tol) {
+  __shared__ double sh[32];
+  if (halted(ctl)) return;
+  double sb = 0.0, sr = 0.0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nel; i += (size_t)gridDim.x * blockDim.x) {
+    const float2 xv = x[i];
+    const float2 bv = bk[i];
+    const float dv = dg[i / J];
+    xold[i] = xv;
+    const float2 rv = make_float2(fmaf(-dv, xv.x, bv.x), fmaf(-dv, xv.y, bv.y));
+    r[i] = rv;
+    sb += (double)bv.x * bv.x + (double)bv.y * bv.y;
+    sr += (double)rv.x * rv.x + (double)rv.y * rv.y;
+  }
+  double vals[2];
+  vals[0] = block_sum(sb, sh);
+  vals[1] = block_sum(sr, sh);
+  if (!publish_and_check_last(partials, gridDim.x, vals, 2, &ctl->arrive[0])) return;
+  const double b2 = sum_partials(partials, gridDim.x, 0, sh);
+  const double r2 = sum_partials(partials, gridDim.x, 1, sh);
+  if (threadIdx.x == 0) {
+    CgState& c = ctl->cg;
+    c.it = 0;
+    c.zero_b = 0;
+    c.done = 0;
+    c.gamma = 0.0;
+    c.bnorm = sqrt(b2);
+    if (c.bnorm == 0.0) {  // solvers.cpp:30-33: zero right-hand side -> x = 0
+      c.zero_b = 1;
+      c.done = 1;
+      c.rel = 0.0;
+    } else {
+      c.rel = sqrt(r2) / c.bnorm;
+      if (!isfinite(c.rel)) {
+        ctl->error = 1;
+        c.done = 1;
+      } else if (!(c.rel > cg_tol)) {
+        c.done = 1;
+      } else {
+        c.rho = r2;
+      }
+    }
+    ctl->arrive[0] = 0;
+  }
+}
+
+// Zero x when b == 0 (cg_solve returns zeros, solvers.cpp:30-33).
+__global__ void k_cg_zero_x(float2* __restrict__ x, size_t nel, const SolverCtl* ctl) {
+  if (halted(ctl) || !ctl->cg.zero_b) return;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nel; i += (size_t)gridDim.x * blockDim.x)
+    x[i] = make_float2(0.f, 0.f);
+}
+
+__device__ void finalize_alpha(SolverCtl* ctl, double denom) {
+  CgState& c = ctl->cg;
+  c.denom = denom;
+  if (!isfinite(denom) || denom <= 0.0) {  // solvers.cpp:44-45
+    ctl->error = 2;
+    c.done = 1;
+  } else {
+    c.alpha = c.rho / denom;
+  }
+}
+
+// p = r + gamma p (p = r at it == 0); denom = Re<p, A p> with A = diag(dg).
+__global__ void k_cg_a_diag(const float2* __restrict__ r, float2* __restrict__ p,
+                            const float* __restrict__ dg, size_t nel, int J, SolverCtl* ctl,
+                            double* partials) {
+  __shared__ double sh[32];
+  if (halted(ctl) || ctl->cg.done) return;
+  const bool first = ctl->cg.it == 0;
+  const float g = (float)ctl->cg.gamma;
+  double s = 0.0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nel; i += (size_t)gridDim.x * blockDim.x) {
+    float2 pv = r[i];
+    if (!first) {
+      const float2 po = p[i];
+      pv = make_float2(fmaf(g, po.x, pv.x), fmaf(g, po.y, pv.y));
+    }
+    p[i] = pv;
+    const float dv = dg[i / J];
+    const float2 ap = make_float2(dv * pv.x, dv * pv.y);
+    s += (double)pv.x * ap.x + (double)pv.y * ap.y;
+  }
+  double v = block_sum(s, sh);
+  if (!publish_and_check_last(partials, gridDim.x, &v, 1, &ctl->arrive[1])) return;
+  const double denom = sum_partials(partials, gridDim.x, 0, sh);
+  if (threadIdx.x == 0) {
+    finalize_alpha(ctl, denom);
+    ctl->arrive[1] = 0;
+  }
+}
+
+__device__ void finalize_rho(SolverCtl* ctl, double rho_next, int cg_max, double cg_tol) {
+  CgState& c = ctl->cg;
+  if (!isfinite(rho_next)) {  // solvers.cpp:52-53
+    ctl->error = 1;
+    c.done = 1;
+    return;
+  }
+  c.rel = sqrt(rho_next) / c.bnorm;
+  c.it += 1;
+  if (c.rel <= cg_tol) {
+    c.done = 1;
+    return;
+  }
+  c.gamma = rho_next / c.rho;
+  c.rho = rho_next;
+  if (c.it >= cg_max) c.done = 1;
+}
+
+// x += alpha p ; r -= alpha A p ; rho' = <r, r>.  ap == nullptr: A = diag(dg).
+__global__ void k_cg_b(float2* __restrict__ x, float2* __restrict__ r, const float2* __restrict__ p,
+                       const float2* __restrict__ ap, const float* __restrict__ dg, size_t nel,
+                       int J, SolverCtl* ctl, double* partials, int cg_max, double cg_tol) {
+  __shared__ double sh[32];
+  if (halted(ctl) || ctl->cg.done) return;
+  const float a = (float)ctl->cg.alpha;
+  double s = 0.0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nel; i += (size_t)gridDim.x * blockDim.x) {
+    const float2 pv = p[i];
+    float2 apv;
+    if (ap) {
+      apv = ap[i];
+    } else {
+      const float dv = dg[i / J];
+      apv = make_float2(dv * pv.x, dv * pv.y);
+    }
+    float2 xv = x[i], rv = r[i];
+    xv = make_float2(fmaf(a, pv.x, xv.x), fmaf(a, pv.y, xv.y));
+    rv = make_float2(fmaf(-a, apv.x, rv.x), fmaf(-a, apv.y, rv.y));
+    x[i] = xv;
+    r[i] = rv;
+    s += (double)rv.x * rv.x + (double)rv.y * rv.y;
+  }
+  double v = block_sum(s, sh);
+  if (!publish_and_check_last(partials, gridDim.x, &v, 1, &ctl->arrive[2])) return;
+  const double rho_next = sum_partials(partials, gridDim.x, 0, sh);
+  if (threadIdx.x == 0) {
+    finalize_rho(ctl, rho_next, cg_max, cg_tol);
+    ctl->arrive[2] = 0;
+  }
+}
+
+// SPIRiT init finish: xold = x; r = b - ap; bnorm, rel, rho.
+__global__ void k_cg_init_from_ap(const float2* __restrict__ bk, const float2* __restrict__ ap,
+                                  const float2* __restrict__ x, float2* __restrict__ xold,
+                                  float2* __restrict__ r, size_t nel, SolverCtl* ctl,
+                                  double* partials, double cg_tol) {
+  __shared__ double sh[32];
+  if (halted(ctl)) return;
+  double sb = 0.0, sr = 0.0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nel; i += (size_t)gridDim.x * blockDim.x) {
+    const float2 bv = bk[i], av = ap[i];
+    xold[i] = x[i];
+    const float2 rv = csub(bv, av);
+    r[i] = rv;
+    sb += (double)bv.x * bv.x + (double)bv.y * bv.y;
+    sr += (double)rv.x * rv.x + (double)rv.y * rv.y;
+  }
+  double vals[2];
+  vals[0] = block_sum(sb, sh);
+  vals[1] = block_sum(sr, sh);
+  if (!publish_and_check_last(partials, gridDim.x, vals, 2, &ctl->arrive[0])) return;
+  const double b2 = sum_partials(partials, gridDim.x, 0, sh);
+  const double r2 = sum_partials(partials, gridDim.x, 1, sh);
+  if (threadIdx.x == 0) {
+    CgState& c = ctl->cg;
+    c.it = 0;
+    c.zero_b = 0;
+    c.done = 0;
+    c.gamma = 0.0;
+    c.bnorm = sqrt(b2);
+    if (c.bnorm == 0.0) {
+      c.zero_b = 1;
+      c.done = 1;
+      c.rel = 0.0;
+    } else {
+      c.rel = sqrt(r2) / c.bnorm;
+      if (!isfinite(c.rel)) {
+        ctl->error = 1;
+        c.done = 1;
+      } else if (!(c.rel > cg_tol)) {
+        c.done = 1;
+      } else {
+        c.rho = r2;
+      }
+    }
+    ctl->arrive[0] = 0;
+  }
+}
+
+// SPIRiT column stage on [M][N*J], tile of F = PPT*J fibres (PPT pixels):
+// v = iF0(tmp); w = P v per pixel; tmp2 = F0(w).
+__global__ void __launch_bounds__(256) k_spirit_cols(const float2* __restrict__ tmp,
+                                                     float2* __restrict__ tmp2,
+                                                     const float2* __restrict__ pm, FftTwiddles tw,
+                                                     int N, int J, int PPT, const SolverCtl* ctl,
+                                                     int for_x) {
+  extern __shared__ float2 sm[];
+  if (halted(ctl) || (!for_x && ctl->cg.done)) return;
+  const int M = tw.n;
+  const int F = PPT * J;
+  const long long NJ = (long long)N * J;
+  const int n0 = blockIdx.x * PPT;  // first pixel column of the tile
+  float2* a = sm;
+  float2* b = sm + (size_t)M * F;
+  for (int t = threadIdx.x; t < M * F; t += blockDim.x) {
+    const int f = t % F, k = t / F;
+    const int n = n0 + f / J;
+    a[t] = n < N ? tmp[k * NJ + (long long)n0 * J + f] : make_float2(0.f, 0.f);
+  }
+  __syncthreads();
+  float2* res = smem_centered_dft<true>(a, b, tw, F);
+  float2* oth = res == a ? b : a;
+  const float isn = rsqrtf((float)M);
+  // per-pixel matvec into the other buffer
+  for (int t = threadIdx.x; t < M * F; t += blockDim.x) {
+    const int f = t % F, k = t / F;
+    const int pl = f / J, ai = f % J;
+    const int n = n0 + pl;
+    float2 acc = make_float2(0.f, 0.f);
+    if (n < N) {
+      const float2* pp = pm + (((long long)k * N + n) * J + ai) * J;
+      const float2* vv = res + k * F + pl * J;
+      const float sc = centered_out_scale(k, M, tw.logn, isn);
+      for (int bi = 0; bi < J; ++bi) cfma(acc, __ldg(pp + bi), vv[bi]);
+      acc = cscale(acc, sc);
+    }
+    oth[t] = acc;
+  }
+  __syncthreads();
+  float2* res2 = smem_centered_dft<false>(oth, res, tw, F);
+  for (int t = threadIdx.x; t < M * F; t += blockDim.x) {
+    const int f = t % F, k = t / F;
+    const int n = n0 + f / J;
+    if (n < N) tmp2[k * NJ + (long long)n0 * J + f] = cscale(res2[t], centered_out_scale(k, M, tw.logn, isn));
+  }
+}
+
+// SPIRiT row forward stage, one CTA per row m: v = F1(tmp2 row);
+// ap = dg p + lambda1 v.  mode 0: CG iteration (reduce denom, finalize alpha);
+// mode 1: initial residual (apply to x, store ap only).
+__global__ void __launch_bounds__(256) k_spirit_rows_fwd(const float2* __restrict__ tmp2,
+                                                         const float2* __restrict__ vec,
+                                                         const float* __restrict__ dg,
+                                                         float2* __restrict__ ap, FftTwiddles tw,
+                                                         int J, float lambda1, SolverCtl* ctl,
+                                                         double* partials, int mode) {
+  extern __shared__ float2 sm[];
+  __shared__ double sh[32];
+  if (halted(ctl) || (mode == 0 && ctl->cg.done)) return;
+  const int N = tw.n;
+  const int F = J;
+  const long long NJ = (long long)N * J;
+  const int m = blockIdx.x;
+  float2* a = sm;
+  float2* b = sm + (size_t)N * F;
+  for (int t = threadIdx.x; t < N * F; t += blockDim.x) a[t] = tmp2[m * NJ + t];
+  __syncthreads();
+  float2* res = smem_centered_dft<false>(a, b, tw, F);
+  const float isn = rsqrtf((float)N);
+  double s = 0.0;
+  for (int t = threadIdx.x; t < N * F; t += blockDim.x) {
+    const int k = t / F;
+    const long long idx = m * NJ + t;
+    const float2 v = cscale(res[t], centered_out_scale(k, N, tw.logn, isn));
+    const float2 pv = vec[idx];
+    const float dv = dg[idx / J];
+    const float2 av = make_float2(fmaf(dv, pv.x, lambda1 * v.x), fmaf(dv, pv.y, lambda1 * v.y));
+    ap[idx] = av;
+    s += (double)pv.x * av.x + (double)pv.y * av.y;
+  }
+  if (mode != 0) return;
+  double v = block_sum(s, sh);
+  if (!publish_and_check_last(partials, gridDim.x, &v, 1, &ctl->arrive[1])) return;
+  const double denom = sum_partials(partials, gridDim.x, 0, sh);
+  if (threadIdx.x == 0) {
+    finalize_alpha(ctl, denom);
+    ctl->arrive[1] = 0;
+  }
+}
+
+// rel_change_sq (solvers.cpp:80-87) by Parseval in k-space, log record and
+// the stop rule (solvers.cpp:183-187).
+__global__ void k_relchange(const float2* __restrict__ x, const float2* __restrict__ xold,
+                            size_t nel, SolverCtl* ctl, double* partials, double* log, double tol,
+                            int max_outer) {
+  __shared__ double sh[32];
+  if (halted(ctl)) return;
+  double sn = 0.0, sd = 0.0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nel; i += (size_t)gridDim.x * blockDim.x) {
+    const float2 a = x[i], b = xold[i];
+    const double dx = (double)a.x - b.x, dy = (double)a.y - b.y;
+    sn += dx * dx + dy * dy;
+    sd += (double)b.x * b.x + (double)b.y * b.y;
+  }
+  double vals[2];
+  vals[0] = block_sum(sn, sh);
+  vals[1] = block_sum(sd, sh);
+  if (!publish_and_check_last(partials, gridDim.x, vals, 2, &ctl->arrive[3])) return;
+  const double num = sum_partials(partials, gridDim.x, 0, sh);
+  const double den = sum_partials(partials, gridDim.x, 1, sh);
+  if (threadIdx.x == 0) {
+    const double rc = den > 0.0 ? num / den : (num > 0.0 ? 1.0 : 0.0);
+    ctl->relchange = rc;
+    const int k = ctl->outer;
+    if (k < max_outer) {
+      log[3 * k + 0] = rc;
+      log[3 * k + 1] = (double)ctl->cg.it;
+      log[3 * k + 2] = ctl->cg.rel;
+    }
+    ctl->outer = k + 1;
+    if (rc < tol) ctl->stopped = 1;
+    ctl->arrive[3] = 0;
+  }
+}
+
+__global__ void k_to_double(const float2* __restrict__ src, double* __restrict__ dst, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    dst[2 * i] = src[i].x;
+    dst[2 * i + 1] = src[i].y;
+  }
+}
+
+__global__ void k_from_double(const double* __restrict__ src, float2* __restrict__ dst, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = make_float2((float)src[2 * i], (float)src[2 * i + 1]);
+}
+
+// ------------------------------------------------------------ host math (fp64)
+std::vector<double> hankel_counts_h(int n, int p) {
+  std::vector<double> c(n, 0.0);
+  const int q = n - p + 1;
+  for (int i = 0; i < p; ++i)
+    for (int j = 0; j < q; ++j) c[i + j] += 1.0;
+  return c;
+}
+
+// weights_centered (proj/src/hankel.cpp:75-97), as (re, im) pairs.
+std::vector<double> weights_centered_h(const double* taps, size_t ntaps, int n) {
+  std::vector<double> w(2 * n, 0.0), out(2 * n, 0.0);
+  for (int k = 0; k < n; ++k) {
+    double sr = 0, si = 0;
+    for (size_t t = 0; t < ntaps; ++t) {
+      const double ang = -2.0 * M_PI * (double)k * (double)t / (double)n;
+      const double c = std::cos(ang), s = std::sin(ang);
+      sr += taps[2 * t] * c - taps[2 * t + 1] * s;
+      si += taps[2 * t] * s + taps[2 * t + 1] * c;
+    }
+    w[2 * k] = sr;
+    w[2 * k + 1] = si;
+  }
+  const int c = n / 2;
+  for (int i = 0; i < n; ++i) {  // fftshift: out[(i + c) % n] = w[i]
+    out[2 * ((i + c) % n)] = w[2 * i];
+    out[2 * ((i + c) % n) + 1] = w[2 * i + 1];
+  }
+  return out;
+}
+
+int dagger_h(int i, int n) { return (2 * (n / 2) + n - i) % n; }
+
+template <class T>
+T* dalloc(size_t n) {
+  T* p = nullptr;
+  SHLR_CUDA(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
+  return p;
+}
+
+int grid_for(size_t n) {
+  const size_t blocks = (n + kThreads * 4 - 1) / (kThreads * 4);
+  return (int)std::max<size_t>(1, std::min<size_t>(blocks, (size_t)num_sms() * 4));
+}
+
+}  // namespace
+
+FftTwiddles make_twiddles(int n, float2** dev_storage, cudaStream_t stream) {
+  std::vector<float2> tw(n);
+  for (int k = 0; k < n; ++k) {
+    const double ang = -2.0 * M_PI * (double)k / (double)n;
+    tw[k] = make_float2((float)std::cos(ang), (float)std::sin(ang));
+  }
+  float2* d = dalloc<float2>(n);
+  SHLR_CUDA(cudaMemcpyAsync(d, tw.data(), n * sizeof(float2), cudaMemcpyHostToDevice, stream));
+  *dev_storage = d;
+  FftTwiddles t;
+  t.tw = d;
+  t.n = n;
+  int lg = -1;
+  if (n > 0 && (n & (n - 1)) == 0) {
+    lg = 0;
+    while ((1 << lg) < n) ++lg;
+  }
+  t.logn = lg;
+  return t;
+}
+
+// ------------------------------------------------------------ PiPlan
+PiPlan::PiPlan(const PiConfig& cfg, const double* y, const uint8_t* mask, size_t mask_rows,
+               const double* taps, size_t ntaps, const double* spirit_w, size_t spirit_k)
+    : cfg_(cfg) {
+  const int M = cfg.M, N = cfg.N, J = cfg.J;
+  SHLR_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  SHLR_CUDA(cudaEventCreate(&ev0_));
+  SHLR_CUDA(cudaEventCreate(&ev1_));
+  SHLR_CUDA(cudaEventCreate(&evA_));
+  SHLR_CUDA(cudaEventCreate(&evB_));
+  nel_ = (size_t)M * N * J;
+  qr_ = N - cfg.Pr + 1;
+  qc_ = M - cfg.Pc + 1;
+  B_ = J * (cfg.vc ? 2 : 1);
+  red_blocks_ = grid_for(nel_);
+
+  // ---- host-side constants (fp64, rounded once)
+  const auto wN = weights_centered_h(taps, ntaps, N);
+  const auto wM = weights_centered_h(taps, ntaps, M);
+  const auto cN = hankel_counts_h(N, cfg.Pr);
+  const auto cM = hankel_counts_h(M, cfg.Pc);
+  auto a_of = [&](const std::vector<double>& w, const std::vector<double>& cnt, int n) {
+    std::vector<double> a(n);
+    for (int k = 0; k < n; ++k) {
+      a[k] = (w[2 * k] * w[2 * k] + w[2 * k + 1] * w[2 * k + 1]) * cnt[k];
+      if (cfg.vc) {
+        const int f = dagger_h(k, n);
+        a[k] += (w[2 * f] * w[2 * f] + w[2 * f + 1] * w[2 * f + 1]) * cnt[f];
+      }
+    }
+    return a;
+  };
+  const auto aN = a_of(wN, cN, N), aM = a_of(wM, cM, M);
+  std::vector<float> dg((size_t)M * N);
+  for (int m = 0; m < M; ++m)
+    for (int n = 0; n < N; ++n) {
+      const bool s = mask[(mask_rows == 1 ? 0 : m) * (size_t)N + n] != 0;
+      dg[(size_t)m * N + n] = (float)((s ? cfg.lambda : 0.0) + cfg.beta * aN[n] + cfg.beta * aM[m]);
+    }
+  // initial RHS adjoint spectra for Z = 0, D = 1: T = -1/beta
+  auto h0_of = [&](const std::vector<double>& w, const std::vector<double>& cnt, int n) {
+    std::vector<float2> h(n);
+    for (int k = 0; k < n; ++k) {
+      double re = w[2 * k] * cnt[k], im = -w[2 * k + 1] * cnt[k];  // conj(wc) * counts
+      if (cfg.vc) {
+        const int f = dagger_h(k, n);
+        re += w[2 * f] * cnt[f];
+        im += w[2 * f + 1] * cnt[f];
+      }
+      h[k] = make_float2((float)(-re / cfg.beta), (float)(-im / cfg.beta));
+    }
+    return h;
+  };
+  const auto hN = h0_of(wN, cN, N), hM = h0_of(wM, cM, M);
+  std::vector<float2> wcNf(N), wcMf(M);
+  for (int k = 0; k < N; ++k) wcNf[k] = make_float2((float)wN[2 * k], (float)wN[2 * k + 1]);
+  for (int k = 0; k < M; ++k) wcMf[k] = make_float2((float)wM[2 * k], (float)wM[2 * k + 1]);
+
+  // ---- device buffers
+  yk_ = dalloc<float2>(nel_);
+  x_ = dalloc<float2>(nel_);
+  xold_ = dalloc<float2>(nel_);
+  r_ = dalloc<float2>(nel_);
+  p_ = dalloc<float2>(nel_);
+  bk_ = dalloc<float2>(nel_);
+  tmp_ = dalloc<float2>(nel_);
+  srow_ = dalloc<float2>(nel_);
+  scol_ = dalloc<float2>(nel_);
+  hrow_ = dalloc<float2>(nel_);
+  hcol_ = dalloc<float2>(nel_);
+  dg_ = dalloc<float>((size_t)M * N);
+  hrow0_ = dalloc<float2>(N);
+  hcol0_ = dalloc<float2>(M);
+  wcN_ = dalloc<float2>(N);
+  wcM_ = dalloc<float2>(M);
+  partials_ = dalloc<double>(4 * (size_t)std::max(red_blocks_, M));
+  ctl_ = dalloc<SolverCtl>(1);
+  log_ = dalloc<double>(3 * (size_t)std::max(cfg.max_outer, 1));
+  const int er = std::max(cfg.Pr, B_ * qr_), dr = std::min(cfg.Pr, B_ * qr_);
+  const int ec = std::max(cfg.Pc, B_ * qc_), dc = std::min(cfg.Pc, B_ * qc_);
+  d_row_elems_ = (size_t)M * er * dr;
+  d_col_elems_ = (size_t)N * ec * dc;
+  drow_ = dalloc<float2>(d_row_elems_);
+  dcol_ = dalloc<float2>(d_col_elems_);
+  if (cfg.debug_sv_iter > 0) {
+    if (dr != dc) throw InvalidArg("debug singular values need equal row/column d");
+    d_sv_ = dr;
+    sv_ = dalloc<float>((size_t)(M + N) * dr);
+  }
+  SHLR_CUDA(cudaMemcpyAsync(dg_, dg.data(), dg.size() * sizeof(float), cudaMemcpyHostToDevice, stream_));
+  SHLR_CUDA(cudaMemcpyAsync(hrow0_, hN.data(), N * sizeof(float2), cudaMemcpyHostToDevice, stream_));
+  SHLR_CUDA(cudaMemcpyAsync(hcol0_, hM.data(), M * sizeof(float2), cudaMemcpyHostToDevice, stream_));
+  SHLR_CUDA(cudaMemcpyAsync(wcN_, wcNf.data(), N * sizeof(float2), cudaMemcpyHostToDevice, stream_));
+  SHLR_CUDA(cudaMemcpyAsync(wcM_, wcMf.data(), M * sizeof(float2), cudaMemcpyHostToDevice, stream_));
+  tM_ = make_twiddles(M, &twM_, stream_);
+  tN_ = make_twiddles(N, &twN_, stream_);
+
+  // data: y (fp64) -> masked complex64 x0 and lambda*y
+  {
+    x0_ = dalloc<float2>(nel_);
+    double* y_d = dalloc<double>(2 * nel_);
+    uint8_t* m_d = dalloc<uint8_t>(mask_rows * (size_t)N);
+    SHLR_CUDA(cudaMemcpyAsync(y_d, y, 2 * nel_ * sizeof(double), cudaMemcpyHostToDevice, stream_));
+    SHLR_CUDA(cudaMemcpyAsync(m_d, mask, mask_rows * (size_t)N, cudaMemcpyHostToDevice, stream_));
+    k_init_data<<<grid_for(nel_), kThreads, 0, stream_>>>(y_d, m_d, (int)mask_rows, M, N, J,
+                                                          cfg.lambda, x0_, yk_);
+    SHLR_LAUNCH_CHECK();
+    SHLR_CUDA(cudaStreamSynchronize(stream_));
+    SHLR_CUDA(cudaFree(y_d));
+    SHLR_CUDA(cudaFree(m_d));
+  }
+
+  if (cfg.spirit) {
+    if (!spirit_w || spirit_k == 0) throw InvalidArg("spirit enabled without kernels");
+    const int JJ = J * J;
+    const size_t npl = (size_t)M * N * JJ;
+    double* w_d = dalloc<double>(2 * spirit_k * spirit_k * JJ);
+    SHLR_CUDA(cudaMemcpyAsync(w_d, spirit_w, 2 * spirit_k * spirit_k * JJ * sizeof(double),
+                              cudaMemcpyHostToDevice, stream_));
+    float2* conv = dalloc<float2>(npl);
+    float2* tmpc = dalloc<float2>(npl);
+    k_spirit_conv<<<grid_for(npl), kThreads, 0, stream_>>>(w_d, (int)spirit_k, M, N, J, conv);
+    SHLR_LAUNCH_CHECK();
+    // maps = ifft2c(conv) per plane: axis 1 then axis 0 over [M][N][JJ]
+    {
+      StridedCopyOp op1{conv, tmpc, (long long)N * JJ, JJ, 1};
+      launch_fft_axis<StridedCopyOp, true>(op1, tN_, M, JJ, std::min(JJ, 16), stream_);
+      StridedCopyOp op0{tmpc, conv, 0, (long long)N * JJ, 1};
+      launch_fft_axis<StridedCopyOp, true>(op0, tM_, 1, N * JJ, 16, stream_);
+    }
+    pmat_ = dalloc<float2>(npl);
+    k_spirit_pmat<<<grid_for(npl), kThreads, 0, stream_>>>(conv, M * N, J, pmat_);
+    SHLR_LAUNCH_CHECK();
+    SHLR_CUDA(cudaStreamSynchronize(stream_));
+    SHLR_CUDA(cudaFree(conv));
+    SHLR_CUDA(cudaFree(tmpc));
+    SHLR_CUDA(cudaFree(w_d));
+    ap_ = dalloc<float2>(nel_);
+    tmp2_ = dalloc<float2>(nel_);
+  }
+  SHLR_CUDA(cudaFuncSetAttribute(k_spirit_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+  SHLR_CUDA(cudaFuncSetAttribute(k_spirit_rows_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+  reset();
+  SHLR_CUDA(cudaStreamSynchronize(stream_));
+}
+
+PiPlan::~PiPlan() {
+  if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+  if (graph_) cudaGraphDestroy(graph_);
+  void* bufs[] = {yk_, x_, xold_, r_, p_, ap_, bk_, tmp_, tmp2_, dg_, srow_, scol_, hrow_, hcol_,
+                  hrow0_, hcol0_, drow_, dcol_, wcN_, wcM_, pmat_, twM_, twN_, sv_, partials_,
+                  ctl_, log_, x0_};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  if (ev0_) cudaEventDestroy(ev0_);
+  if (ev1_) cudaEventDestroy(ev1_);
+  if (evA_) cudaEventDestroy(evA_);
+  if (evB_) cudaEventDestroy(evB_);
+  if (stream_) cudaStreamDestroy(stream_);
+}
+
+void PiPlan::reset() {
+  const int M = cfg_.M, N = cfg_.N, J = cfg_.J;
+  k_copy<<<grid_for(nel_), kThreads, 0, stream_>>>(x_, x0_, nel_);
+  k_fill<<<grid_for(d_row_elems_), kThreads, 0, stream_>>>(drow_, d_row_elems_, make_float2(1.f, 0.f));
+  k_fill<<<grid_for(d_col_elems_), kThreads, 0, stream_>>>(dcol_, d_col_elems_, make_float2(1.f, 0.f));
+  k_init_h<<<grid_for(nel_), kThreads, 0, stream_>>>(hrow_, hcol_, hrow0_, hcol0_, M, N, J);
+  k_reset_ctl<<<1, 1, 0, stream_>>>(ctl_);
+  SHLR_CUDA(cudaMemsetAsync(log_, 0, 3 * sizeof(double) * std::max(cfg_.max_outer, 1), stream_));
+  SHLR_LAUNCH_CHECK();
+  iter_ = 0;
+}
+
+void PiPlan::cg_apply_spirit(float2* in_vec, float2* out_ap, bool init) {
+  const int M = cfg_.M, N = cfg_.N, J = cfg_.J;
+  const long long NJ = (long long)N * J;
+  // stage 1: row iFFT (with p update)
+  SpiritRowInvOp op1{r_, p_, init ? in_vec : nullptr, tmp_, NJ, J, ctl_};
+  launch_fft_axis<SpiritRowInvOp, true>(op1, tN_, M, J, J, stream_);
+  ++launch_count_;
+  // stage 2: columns
+  const int ppt = std::max(1, 16 / J);
+  const size_t smem2 = 2 * (size_t)M * ppt * J * sizeof(float2);
+  k_spirit_cols<<<(N + ppt - 1) / ppt, kThreads, smem2, stream_>>>(tmp_, tmp2_, pmat_, tM_, N, J, ppt,
+                                                                   ctl_, init ? 1 : 0);
+  SHLR_LAUNCH_CHECK();
+  ++launch_count_;
+  // stage 3: row FFT + combine (+ alpha)
+  const size_t smem3 = 2 * (size_t)N * J * sizeof(float2);
+  k_spirit_rows_fwd<<<M, kThreads, smem3, stream_>>>(tmp2_, init ? in_vec : p_, dg_, out_ap, tN_, J,
+                                                     (float)cfg_.lambda1, ctl_, partials_, init ? 1 : 0);
+  SHLR_LAUNCH_CHECK();
+  ++launch_count_;
+}
+
+void PiPlan::enqueue_iteration(int k, bool record_events) {
+  const int M = cfg_.M, N = cfg_.N, J = cfg_.J;
+  const long long NJ = (long long)N * J;
+  const int g = red_blocks_;
+  // ---- RHS: b^ = lambda y + beta (F0 hrow + F1 hcol)
+  {
+    CopyOpCtl op1{hcol_, tmp_, NJ, J, 1, ctl_};
+    launch_fft_axis<CopyOpCtl, false>(op1, tN_, M, J, J, stream_);
+    RhsOp op0{hrow_, tmp_, yk_, bk_, NJ, (float)cfg_.beta, ctl_};
+    launch_fft_axis<RhsOp, false>(op0, tM_, 1, N * J, 16, stream_);
+    launch_count_ += 2;
+  }
+  // ---- CG (solvers.cpp:23-67)
+  if (!cfg_.spirit) {
+    k_cg_init_diag<<<g, kThreads, 0, stream_>>>(bk_, dg_, x_, xold_, r_, nel_, J, ctl_, partials_,
+                                                cfg_.cg_tol);
+    k_cg_zero_x<<<g, kThreads, 0, stream_>>>(x_, nel_, ctl_);
+    launch_count_ += 2;
+    for (int it = 0; it < cfg_.cg_max; ++it) {
+      k_cg_a_diag<<<g, kThreads, 0, stream_>>>(r_, p_, dg_, nel_, J, ctl_, partials_);
+      k_cg_b<<<g, kThreads, 0, stream_>>>(x_, r_, p_, nullptr, dg_, nel_, J, ctl_, partials_,
+                                         cfg_.cg_max, cfg_.cg_tol);
+      launch_count_ += 2;
+    }
+  } else {
+    cg_apply_spirit(x_, ap_, true);
+    k_cg_init_from_ap<<<g, kThreads, 0, stream_>>>(bk_, ap_, x_, xold_, r_, nel_, ctl_, partials_,
+                                                   cfg_.cg_tol);
+    k_cg_zero_x<<<g, kThreads, 0, stream_>>>(x_, nel_, ctl_);
+    launch_count_ += 2;
+    for (int it = 0; it < cfg_.cg_max; ++it) {
+      cg_apply_spirit(p_, ap_, false);
+      k_cg_b<<<g, kThreads, 0, stream_>>>(x_, r_, p_, ap_, dg_, nel_, J, ctl_, partials_, cfg_.cg_max,
+                                         cfg_.cg_tol);
+      launch_count_ += 1;
+    }
+  }
+  SHLR_LAUNCH_CHECK();
+  // ---- lifted spectra of x_new: rows = iF0(X), columns = iF1(X)
+  {
+    CopyOpCtl op0{x_, srow_, 0, NJ, 1, ctl_};
+    launch_fft_axis<CopyOpCtl, true>(op0, tM_, 1, N * J, 16, stream_);
+    CopyOpCtl op1{x_, scol_, NJ, J, 1, ctl_};
+    launch_fft_axis<CopyOpCtl, true>(op1, tN_, M, J, J, stream_);
+    launch_count_ += 2;
+  }
+  // ---- Hankel SVT + dual update + adjoint, rows and columns in one launch
+  {
+    SvtParams sp{};
+    sp.nfam = 2;
+    sp.mode = SVT_ADMM_WEIGHTED;
+    sp.inv_beta = (float)(1.0 / cfg_.beta);
+    sp.tau_dual = (float)cfg_.tau;
+    sp.thresh = (float)(1.0 / cfg_.beta);
+    sp.max_sweeps = 20;
+    sp.skip = &ctl_->stopped;
+    for (int f = 0; f < 2; ++f) {
+      SvtFamily& F = sp.fam[f];
+      const bool rows = f == 0;
+      F.count = rows ? M : N;
+      F.len = rows ? N : M;
+      F.P = rows ? cfg_.Pr : cfg_.Pc;
+      F.q = F.len - F.P + 1;
+      F.J = J;
+      F.B = B_;
+      F.vc = cfg_.vc ? 1 : 0;
+      F.wide = (B_ * F.q > F.P) ? 1 : 0;
+      F.e = std::max(F.P, B_ * F.q);
+      F.d = std::min(F.P, B_ * F.q);
+      F.spec = rows ? srow_ : scol_;
+      F.s_mat = rows ? NJ : J;
+      F.s_n = rows ? J : NJ;
+      F.s_j = 1;
+      F.out = rows ? hrow_ : hcol_;
+      F.o_mat = F.s_mat;
+      F.o_n = F.s_n;
+      F.o_j = 1;
+      F.wc = rows ? wcN_ : wcM_;
+      F.D = rows ? drow_ : dcol_;
+      F.sv = (sv_ && k + 1 == cfg_.debug_sv_iter) ? (rows ? sv_ : sv_ + (size_t)M * d_sv_) : nullptr;
+    }
+    if (record_events) SHLR_CUDA(cudaEventRecord(evA_, stream_));
+    launch_hankel_svt(sp, M + N, stream_);
+    if (record_events) SHLR_CUDA(cudaEventRecord(evB_, stream_));
+    launch_count_ += 1;
+  }
+  // ---- stop rule + log
+  k_relchange<<<g, kThreads, 0, stream_>>>(x_, xold_, nel_, ctl_, partials_, log_, cfg_.tol,
+                                           cfg_.max_outer);
+  SHLR_LAUNCH_CHECK();
+  launch_count_ += 1;
+}
+
+void PiPlan::build_graph() {
+  launch_count_ = 0;
+  SHLR_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+  enqueue_iteration(/*k=*/-1, false);
+  SHLR_CUDA(cudaStreamEndCapture(stream_, &graph_));
+  SHLR_CUDA(cudaGraphInstantiate(&graph_exec_, graph_, 0));
+  launches_per_iter_ = launch_count_;
+}
+
+void PiPlan::run(size_t iters) {
+  const size_t todo = std::min(iters, (size_t)std::max(0, cfg_.max_outer - iter_));
+  svt_ms_ = 0;
+  const bool use_graph = !timing_ && cfg_.debug_sv_iter <= 0 && !std::getenv("SHLR_NO_GRAPH");
+  if (use_graph && !graph_exec_) build_graph();
+  SHLR_CUDA(cudaEventRecord(ev0_, stream_));
+  for (size_t i = 0; i < todo; ++i) {
+    if (use_graph) {
+      SHLR_CUDA(cudaGraphLaunch(graph_exec_, stream_));
+    } else {
+      launch_count_ = 0;
+      enqueue_iteration(iter_, timing_);
+      launches_per_iter_ = launch_count_;
+      if (timing_) {
+        SHLR_CUDA(cudaEventSynchronize(evB_));
+        float ms = 0;
+        SHLR_CUDA(cudaEventElapsedTime(&ms, evA_, evB_));
+        svt_ms_ += ms;
+      }
+    }
+    ++iter_;
+  }
+  SHLR_CUDA(cudaEventRecord(ev1_, stream_));
+}
+
+void PiPlan::sync() {
+  SHLR_CUDA(cudaStreamSynchronize(stream_));
+  float ms = 0;
+  if (cudaEventElapsedTime(&ms, ev0_, ev1_) == cudaSuccess) total_ms_ = ms;
+}
+
+void PiPlan::download(double* x_out, size_t* outer_iters, double* final_rel,
+                      std::vector<std::string>* log_lines, int* error) {
+  const int M = cfg_.M, N = cfg_.N, J = cfg_.J;
+  const long long NJ = (long long)N * J;
+  // x = iF2D(X): axis 1 then axis 0
+  StridedCopyOp op1{x_, tmp_, NJ, J, 1};
+  launch_fft_axis<StridedCopyOp, true>(op1, tN_, M, J, J, stream_);
+  StridedCopyOp op0{tmp_, bk_, 0, NJ, 1};
+  launch_fft_axis<StridedCopyOp, true>(op0, tM_, 1, N * J, 16, stream_);
+  double* xd = dalloc<double>(2 * nel_);
+  k_to_double<<<grid_for(nel_), kThreads, 0, stream_>>>(bk_, xd, nel_);
+  SHLR_LAUNCH_CHECK();
+  SolverCtl hc;
+  std::vector<double> lg(3 * (size_t)std::max(cfg_.max_outer, 1));
+  SHLR_CUDA(cudaMemcpyAsync(x_out, xd, 2 * nel_ * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+  SHLR_CUDA(cudaMemcpyAsync(&hc, ctl_, sizeof(SolverCtl), cudaMemcpyDeviceToHost, stream_));
+  SHLR_CUDA(cudaMemcpyAsync(lg.data(), log_, lg.size() * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+  SHLR_CUDA(cudaStreamSynchronize(stream_));
+  SHLR_CUDA(cudaFree(xd));
+  *outer_iters = (size_t)hc.outer;
+  *final_rel = hc.outer > 0 ? hc.relchange : 1.0;
+  *error = hc.error;
+  if (log_lines) {
+    log_lines->clear();
+    for (int k = 0; k < hc.outer && k < cfg_.max_outer; ++k) {
+      char buf[160];
+      std::snprintf(buf, sizeof buf, "iter=%d relchange=%.3e cg_iters=%d cg_res=%.3e", k + 1,
+                    lg[3 * k], (int)lg[3 * k + 1], lg[3 * k + 2]);
+      log_lines->push_back(buf);
+    }
+  }
+}
+
+void PiPlan::download_sv(double* sv_out) {
+  if (!sv_) return;
+  const size_t n = (size_t)(cfg_.M + cfg_.N) * d_sv_;
+  std::vector<float> h(n);
+  SHLR_CUDA(cudaMemcpyAsync(h.data(), sv_, n * sizeof(float), cudaMemcpyDeviceToHost, stream_));
+  SHLR_CUDA(cudaStreamSynchronize(stream_));
+  for (size_t i = 0; i < n; ++i) sv_out[i] = h[i];
+}
+
+// ------------------------------------------------------------ standalone units
+void hankel_svt_batched_device(const float2* vecs, int batch, int nc, int n, int p, float tau,
+                               float2* out, float* sv, cudaStream_t stream) {
+  SvtParams sp{};
+  sp.nfam = 1;
+  sp.mode = SVT_PLAIN;
+  sp.inv_beta = 1.f;
+  sp.tau_dual = 0.f;
+  sp.thresh = tau;
+  sp.max_sweeps = 20;
+  SvtFamily& F = sp.fam[0];
+  F.count = batch;
+  F.len = n;
+  F.P = p;
+  F.q = n - p + 1;
+  F.J = nc;
+  F.B = nc;
+  F.vc = 0;
+  F.wide = (nc * F.q > p) ? 1 : 0;
+  F.e = std::max(p, nc * F.q);
+  F.d = std::min(p, nc * F.q);
+  F.spec = vecs;
+  F.s_mat = (long long)nc * n;
+  F.s_n = 1;
+  F.s_j = n;
+  F.out = out;
+  F.o_mat = F.s_mat;
+  F.o_n = 1;
+  F.o_j = n;
+  F.sv = sv;
+  launch_hankel_svt(sp, batch, stream);
+}
+
+void fft_along_axis_host(double* data, const size_t* dims, int ndim, int axis, bool inverse) {
+  if (axis < 0 || axis >= ndim) throw InvalidArg("fft_along_axis: axis out of range");
+  size_t outer = 1, inner = 1, total = 1;
+  for (int i = 0; i < ndim; ++i) total *= dims[i];
+  for (int i = 0; i < axis; ++i) outer *= dims[i];
+  for (int i = axis + 1; i < ndim; ++i) inner *= dims[i];
+  const int n = (int)dims[axis];
+  cudaStream_t st;
+  SHLR_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  float2* tw_storage = nullptr;
+  FftTwiddles tw = make_twiddles(n, &tw_storage, st);
+  double* dd = dalloc<double>(2 * total);
+  float2* a = dalloc<float2>(total);
+  float2* b = dalloc<float2>(total);
+  SHLR_CUDA(cudaMemcpyAsync(dd, data, 2 * total * sizeof(double), cudaMemcpyHostToDevice, st));
+  k_from_double<<<grid_for(total), kThreads, 0, st>>>(dd, a, total);
+  const int F = (int)std::min<size_t>(16, inner);
+  StridedCopyOp op{a, b, (long long)(n * inner), (long long)inner, 1};
+  if (inverse)
+    launch_fft_axis<StridedCopyOp, true>(op, tw, (int)outer, (int)inner, F, st);
+  else
+    launch_fft_axis<StridedCopyOp, false>(op, tw, (int)outer, (int)inner, F, st);
+  k_to_double<<<grid_for(total), kThreads, 0, st>>>(b, dd, total);
+  SHLR_LAUNCH_CHECK();
+  SHLR_CUDA(cudaMemcpyAsync(data, dd, 2 * total * sizeof(double), cudaMemcpyDeviceToHost, st));
+  SHLR_CUDA(cudaStreamSynchronize(st));
+  cudaFree(dd);
+  cudaFree(a);
+  cudaFree(b);
+  cudaFree(tw_storage);
+  cudaStreamDestroy(st);
+}
+
+namespace {
+__global__ void k_lift_map(int n, int p, int coils, int vc, int32_t* map) {
+  const int q = n - p + 1;
+  const int blocks = coils * (vc ? 2 : 1);
+  const int total = p * blocks * q;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const int i = t / (blocks * q), c = t % (blocks * q);
+    const LiftSrc s = lift_source(i, c, q, coils, n);
+    map[3 * t] = s.coil;
+    map[3 * t + 1] = s.idx;
+    map[3 * t + 2] = s.conj;
+  }
+}
+}  // namespace
+
+void lift_index_map_device(int n, int p, int coils, int vc, int32_t* map_host) {
+  const int q = n - p + 1;
+  const size_t total = (size_t)p * coils * (vc ? 2 : 1) * q;
+  int32_t* d = dalloc<int32_t>(3 * total);
+  k_lift_map<<<grid_for(total), kThreads>>>(n, p, coils, vc, d);
+  SHLR_LAUNCH_CHECK();
+  SHLR_CUDA(cudaMemcpy(map_host, d, 3 * total * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  cudaFree(d);
+}
+
+namespace {
+// 8 independent FMA chains per thread, unrolled; FLOPs = 2 per FMA.
+__global__ void __launch_bounds__(256) k_fma_probe(float* out, int iters, float a, float b) {
+  float x0 = threadIdx.x * 1e-3f, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5,
+        x6 = x0 + 6, x7 = x0 + 7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      x0 = fmaf(x0, a, b); x1 = fmaf(x1, a, b); x2 = fmaf(x2, a, b); x3 = fmaf(x3, a, b);
+      x4 = fmaf(x4, a, b); x5 = fmaf(x5, a, b); x6 = fmaf(x6, a, b); x7 = fmaf(x7, a, b);
+    }
+  }
+  const float s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+  if (s == 12345.678f) out[0] = s;  // keep the chains alive
+}
+}  // namespace
+
+double fp32_peak_probe() {
+  float* out = dalloc<float>(1);
+  const int blocks = num_sms() * 8, iters = 4096;
+  cudaEvent_t e0, e1;
+  SHLR_CUDA(cudaEventCreate(&e0));
+  SHLR_CUDA(cudaEventCreate(&e1));
+  k_fma_probe<<<blocks, 256>>>(out, 64, 0.999f, 1e-3f);  // warm-up
+  double best = 0;
+  for (int rep = 0; rep < 5; ++rep) {
+    SHLR_CUDA(cudaEventRecord(e0));
+    k_fma_probe<<<blocks, 256>>>(out, iters, 0.999f, 1e-3f);
+    SHLR_CUDA(cudaEventRecord(e1));
+    SHLR_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    SHLR_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    const double flops = 2.0 * 8 * 16 * (double)iters * 256.0 * blocks;
+    best = std::max(best, flops / (ms * 1e-3) / 1e12);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  return best;
+}
+
+}  // namespace shlr_b200
