@@ -121,6 +121,12 @@ int shlr_cuda_hankel_svt_batched(const void* vecs, int batch, int nc, int n, int
 int shlr_cuda_hankel_svt_batched_host(const double* vecs, int batch, int nc, int n, int p,
                                       double tau, double* out, double* sv_out);
 
+/* Diagnostics: the device-pointer batched SVT that also writes, per matrix,
+ * the number of Jacobi sweeps the eigen-solver used (sweeps_dev: device int
+ * array of batch entries). */
+int shlr_cuda_debug_svt_sweeps(const void* vecs, int batch, int nc, int n, int p, float tau,
+                               void* out, int* sweeps_dev);
+
 /* Hankel lift index map used by the device kernels, for bit-exact parity of
  * the lift (operators.cpp:25-58, hankel.cpp:31-41,99-113).  For a p x
  * (blocks*q) matrix built from `coils` vectors of length n (blocks = coils *

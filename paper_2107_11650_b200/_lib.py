@@ -68,6 +68,8 @@ PROTOTYPES = {
     "shlr_cuda_hankel_svt_batched_host": (C.c_int, [C.POINTER(C.c_double), C.c_int, C.c_int,
                                                     C.c_int, C.c_int, C.c_double,
                                                     C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "shlr_cuda_debug_svt_sweeps": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
+                                             C.c_float, C.c_void_p, C.c_void_p]),
     "shlr_cuda_lift_index_map": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int,
                                            C.POINTER(C.c_int32)]),
     "shlr_cuda_fft_along_axis": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_size_t), C.c_int,

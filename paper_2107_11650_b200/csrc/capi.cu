@@ -269,6 +269,18 @@ int shlr_cuda_hankel_svt_batched_host(const double* vecs, int batch, int nc, int
   });
 }
 
+int shlr_cuda_debug_svt_sweeps(const void* vecs, int batch, int nc, int n, int p, float tau,
+                               void* out, int* sweeps_dev) {
+  return guarded([&] {
+    if (batch < 0 || nc < 1 || n < 1 || p < 1 || p > n || tau < 0 || !vecs || !out || !sweeps_dev)
+      throw shlr_b200::InvalidArg("debug_svt_sweeps: invalid arguments");
+    require_device();
+    shlr_b200::hankel_svt_batched_device(static_cast<const float2*>(vecs), batch, nc, n, p, tau,
+                                         static_cast<float2*>(out), nullptr, nullptr, sweeps_dev);
+    return SHLR_OK;
+  });
+}
+
 int shlr_cuda_lift_index_map(int n, int p, int coils, int vc, int32_t* map) {
   return guarded([&] {
     if (n < 1 || p < 1 || p > n || coils < 1 || !map)

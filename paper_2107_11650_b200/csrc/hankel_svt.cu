@@ -300,6 +300,7 @@ __global__ void __launch_bounds__(4 * DP, 1) hankel_svt_kernel(const SvtParams p
     const int any = *rot_flag;
     if (tid == 0) flags[(sweep + 1) & 1] = 0;
     __syncthreads();
+    if (prm.sweeps_out && tid == 0) prm.sweeps_out[blockIdx.x] = sweep + 1;
     if (!any) break;
   }
 

@@ -57,6 +57,7 @@ struct SvtParams {
   float thresh;        // SVT threshold (1/beta or lambda2/beta or user tau)
   int max_sweeps;
   const int* skip;     // optional device flag: nonzero -> kernel is a no-op
+  int* sweeps_out;     // optional diagnostics: Jacobi sweeps used per matrix
 };
 
 // Index function shared by the kernel and shlr_cuda_lift_index_map: source

@@ -992,8 +992,9 @@ void PiPlan::download_sv(double* sv_out) {
 
 // ------------------------------------------------------------ standalone units
 void hankel_svt_batched_device(const float2* vecs, int batch, int nc, int n, int p, float tau,
-                               float2* out, float* sv, cudaStream_t stream) {
+                               float2* out, float* sv, cudaStream_t stream, int* sweeps_out) {
   SvtParams sp{};
+  sp.sweeps_out = sweeps_out;
   sp.nfam = 1;
   sp.mode = SVT_PLAIN;
   sp.inv_beta = 1.f;

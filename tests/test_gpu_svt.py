@@ -1,0 +1,86 @@
+"""GPU parity of the batched Hankel-SVT unit (BASELINE config 5) against the
+oracle on the sweep's synthetic inputs, over the shapes this build supports
+(d = min(p, Nc K) <= 128), plus size-independent properties at full batch."""
+import numpy as np
+import pytest
+
+import shlr_oracle as O
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+SWEEP = [(n, nc, k) for n in (128, 256, 512) for nc in (1, 8, 32) for k in (7, 15, 31)
+         if min(n - k + 1, nc * k) <= 128]
+
+
+@pytest.mark.parametrize("n,nc,k", SWEEP)
+def test_sweep_point_parity(gpu, n, nc, k):
+    from paper_2107_11650_b200 import synth
+    b = 6
+    v = synth.sweep_vectors(n, nc, k, b)
+    tau = synth.sweep_tau(n, nc, k)
+    p = n - k + 1
+    adj, sv = gpu.hankel_svt_batched(v, p, tau)
+    adj_o, sv_o = O.hankel_svt_unit(v, p, tau)
+    assert rel(sv, sv_o) < TOL
+    assert rel(adj, adj_o) < TOL
+
+
+def test_threshold_extremes(gpu):
+    rng = np.random.default_rng(0)
+    v = rng.normal(size=(4, 3, 40)) + 1j * rng.normal(size=(4, 3, 40))
+    # tau = 0: identity on the lifted matrix -> adjoint of the lift = counts * v
+    adj, _ = gpu.hankel_svt_batched(v, 31, 0.0)
+    assert rel(adj, O.hankel_counts(40, 31) * v) < 1e-5
+    # tau above sigma_max: annihilation
+    adj, sv = gpu.hankel_svt_batched(v, 31, 1e6)
+    assert np.max(np.abs(adj)) == 0.0
+    assert sv.shape == (4, 30)
+
+
+def test_rank_one_analytic(gpu):
+    """Rank-1 Hankel: v = a e^{jwt} lifts to a rank-1 matrix with sigma =
+    |a| sqrt(p q); SVT scales it by (1 - tau/sigma) (test_solvers.cpp:47)."""
+    n, p = 64, 40
+    q = n - p + 1
+    t = np.arange(n)
+    v = (2.0 * np.exp(1j * 0.3 * t)).reshape(1, 1, n)
+    sigma = 2.0 * np.sqrt(p * q)
+    tau = 0.25 * sigma
+    adj, sv = gpu.hankel_svt_batched(v, p, tau)
+    assert abs(sv[0, 0] - sigma) < 1e-5 * sigma
+    assert np.max(sv[0, 1:]) < 1e-3 * sigma
+    assert rel(adj, 0.75 * O.hankel_counts(n, p) * v) < 1e-5
+
+
+def test_full_batch_properties(gpu):
+    """BASELINE config-2 geometry at full batch (512 x 242 x 120): singular
+    values match the oracle on a sample and the SVT is non-expansive."""
+    from paper_2107_11650_b200 import synth
+    n, nc, k, b = 256, 8, 15, 512
+    v = synth.sweep_vectors(n, nc, k, b)
+    tau = synth.sweep_tau(n, nc, k)
+    adj, sv = gpu.hankel_svt_batched(v, n - k + 1, tau)
+    idx = [0, 17, 255, 511]
+    adj_o, sv_o = O.hankel_svt_unit(v[idx], n - k + 1, tau)
+    assert rel(sv[idx], sv_o) < TOL
+    assert rel(adj[idx], adj_o) < TOL
+    assert np.all(np.diff(sv, axis=1) <= 0)
+    w = v + 0.01 * np.random.default_rng(1).normal(size=v.shape)
+    adj2, _ = gpu.hankel_svt_batched(w, n - k + 1, tau)
+    # non-expansive in the lifted domain -> adjoint differences bounded by counts * input diff
+    lhs = np.linalg.norm(adj2 - adj)
+    rhs = np.linalg.norm(O.hankel_counts(n, n - k + 1) * (w - v))
+    assert lhs <= rhs * (1 + 1e-4)
+
+
+def test_unsupported_large_d_fails_loudly(gpu):
+    from paper_2107_11650_b200 import synth
+    v = synth.sweep_vectors(256, 32, 15, 2)
+    with pytest.raises(NotImplementedError):
+        gpu.hankel_svt_batched(v, 242, 10.0)
