@@ -105,6 +105,14 @@ int shlr_cuda_pi_plan_timing(shlr_pi_plan* plan, double* svt_ms, double* total_m
 /* Timing mode: plan_run launches kernels directly (no CUDA graph) and times
  * the Hankel-SVT launch of every iteration with CUDA events. */
 int shlr_cuda_pi_plan_set_timing(shlr_pi_plan* plan, int on);
+/* Eigen-solver warm start across outer iterations (default on): each row /
+ * column matrix starts its Jacobi refinement from the eigenvectors it had in
+ * the previous iteration.  The result is the same spectral function either
+ * way; only the sweep count changes. */
+int shlr_cuda_pi_plan_set_warm_start(shlr_pi_plan* plan, int on);
+/* Diagnostics: Jacobi sweeps (stage1 * 100 + stage2) per matrix of the last
+ * Hankel-SVT launch, rows first then columns; n = m + n entries. */
+int shlr_cuda_pi_plan_debug_sweeps(shlr_pi_plan* plan, int* out, int n);
 int shlr_cuda_pi_plan_download(shlr_pi_plan* plan, double* x_out, shlr_stats* stats,
                                shlr_log_fn log_cb, void* log_ctx);
 void shlr_cuda_pi_plan_destroy(shlr_pi_plan* plan);

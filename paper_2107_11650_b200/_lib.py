@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libshlr_b200.so")
+LIB_PATH = os.environ.get("SHLR_LIB_PATH") or os.path.join(_HERE, "lib", "libshlr_b200.so")
 
 SHLR_OK = 0
 SHLR_EINVAL = 1
@@ -62,6 +62,8 @@ PROTOTYPES = {
                                              C.POINTER(ShlrStats), LOG_FN, C.c_void_p]),
     "shlr_cuda_pi_plan_destroy": (None, [C.c_void_p]),
     "shlr_cuda_pi_plan_set_timing": (C.c_int, [C.c_void_p, C.c_int]),
+    "shlr_cuda_pi_plan_set_warm_start": (C.c_int, [C.c_void_p, C.c_int]),
+    "shlr_cuda_pi_plan_debug_sweeps": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.c_int]),
     "shlr_cuda_fp32_peak_tflops": (C.c_int, [C.POINTER(C.c_double)]),
     "shlr_cuda_hankel_svt_batched": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
                                                C.c_float, C.c_void_p, C.c_void_p, C.c_void_p]),

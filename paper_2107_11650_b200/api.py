@@ -252,6 +252,16 @@ class PiPlan:
     def set_timing(self, on: bool):
         _check(lib.shlr_cuda_pi_plan_set_timing(self._h, int(on)), "plan_set_timing")
 
+    def set_warm_start(self, on: bool):
+        _check(lib.shlr_cuda_pi_plan_set_warm_start(self._h, int(on)), "plan_set_warm_start")
+
+    def debug_sweeps(self) -> np.ndarray:
+        n = self.shape[0] + self.shape[1]
+        out = np.zeros(n, np.int32)
+        _check(lib.shlr_cuda_pi_plan_debug_sweeps(self._h, out.ctypes.data_as(C.POINTER(C.c_int)), n),
+               "plan_debug_sweeps")
+        return out
+
     def timing(self):
         s, t, n = C.c_double(), C.c_double(), C.c_int()
         _check(lib.shlr_cuda_pi_plan_timing(self._h, C.byref(s), C.byref(t), C.byref(n)), "timing")

@@ -177,6 +177,22 @@ int shlr_cuda_pi_plan_download(shlr_pi_plan* plan, double* x_out, shlr_stats* st
   });
 }
 
+int shlr_cuda_pi_plan_set_warm_start(shlr_pi_plan* plan, int on) {
+  return guarded([&] {
+    if (!plan) throw shlr_b200::InvalidArg("null plan");
+    plan->impl->set_warm_start(on != 0);
+    return SHLR_OK;
+  });
+}
+
+int shlr_cuda_pi_plan_debug_sweeps(shlr_pi_plan* plan, int* out, int n) {
+  return guarded([&] {
+    if (!plan || !out) throw shlr_b200::InvalidArg("null plan/output");
+    plan->impl->debug_sweeps(out, n);
+    return SHLR_OK;
+  });
+}
+
 int shlr_cuda_pi_plan_set_timing(shlr_pi_plan* plan, int on) {
   return guarded([&] {
     if (!plan) throw shlr_b200::InvalidArg("null plan");

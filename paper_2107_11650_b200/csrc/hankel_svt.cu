@@ -1,46 +1,49 @@
 // Fused batched Hankel-SVT kernel (see hankel_svt.cuh for the algorithm).
+//
+// Eigen-solver: cyclic parallel two-sided Jacobi on the d x d Gram in smem
+// (Brent-Luk ring ordering), in two stages:
+//   stage 1 (cold start only)  G  = Ahat^H Ahat               -> V1
+//   stage 2 (always)           G2 = (Ahat V1)^H (Ahat V1)      -> V = V1 V2
+// Stage 2 recovers the accuracy the FP32 Gram loses on small singular values
+// (G2's entries are accurate relative to sigma_i sigma_j) and is also the
+// ADMM warm start: V1 = the eigenvectors this matrix had in the previous
+// outer iteration (kept in HBM), so a warm launch skips the Gram and stage 1.
+// The Gram diagonal is carried in FP64 (it is updated once per round).
+#include <algorithm>
+#include <string>
+
 #include "hankel_svt.cuh"
 
 namespace shlr_b200 {
 
 namespace {
 
-constexpr float kTolRel = 3.0e-7f;   // rotate iff |g_ab| > kTolRel sqrt(g_aa g_bb)
-constexpr float kTolAbs = 1.0e-7f;   //        and |g_ab| > kTolAbs max_u g_uu
+// Stage 1 (loose: stage 2 refines) and stage 2 (tight) rotation thresholds:
+// rotate iff |g_ab| > tol_rel sqrt(g_aa g_bb) and |g_ab| > tol_abs max_u g_uu.
+constexpr float kTolRel1 = 1.0e-5f;
+constexpr float kTolAbs1 = 1.0e-7f;
+constexpr float kTolRel2 = 2.0e-6f;
 
-struct __align__(16) RotParam {
-  float c, sn;       // cos, sin
-  float2 cw, sw;     // c * conj(phase), s * conj(phase)
-  float na, nb;      // new diagonal entries
-  int flag;          // 1 = non-identity rotation
-  int pad;
+struct __align__(16) SlotRec {
+  int a, b, flag, pad;  // storage indices of the pair, 1 = non-identity rotation
+  float c, sn;          // cos, sin
+  float2 cw;            // c * conj(phase)
+  float2 sw;            // s * conj(phase)
+  float pad2[2];
+  double na, nb;        // diagonal entries a, b after this rotation
 };
 
-// Ring (round-robin / circle method) pairing at round r for DP indices.
-// Position k < DP-1 on the ring holds storage index (k - r) mod (DP-1);
-// top[0] is fixed at DP-1.  top[s] = ring position s-1 (s >= 1),
-// bot[s] = ring position DP-2-s.
 __device__ __forceinline__ int ring_idx(int k, int r, int DP) {
-  int v = k - r;
-  v %= (DP - 1);
+  const int v = k - r;
   return v < 0 ? v + DP - 1 : v;
 }
 __device__ __forceinline__ int top_of(int s, int r, int DP) {
   return s == 0 ? DP - 1 : ring_idx(s - 1, r, DP);
 }
 __device__ __forceinline__ int bot_of(int s, int r, int DP) { return ring_idx(DP - 2 - s, r, DP); }
-
-template <int DP>
-__device__ __forceinline__ float2 gget(const float2* G, int x, int y) {
-  return x <= y ? G[x * (DP + 1) + y] : cconj(G[y * (DP + 1) + x]);
-}
-template <int DP>
-__device__ __forceinline__ void gput(float2* G, int x, int y, float2 v) {
-  if (x <= y)
-    G[x * (DP + 1) + y] = v;
-  else
-    G[y * (DP + 1) + x] = cconj(v);
-}
+// storage column held by slot s at round 0 (the arrangement after a sweep)
+__device__ __forceinline__ int top0(int s, int DP) { return s == 0 ? DP - 1 : s - 1; }
+__device__ __forceinline__ int bot0(int s, int DP) { return DP - 2 - s; }
 
 __device__ __forceinline__ const SvtFamily& family_of(const SvtParams& p, int blk, int& local) {
   if (p.nfam > 1 && blk >= p.fam[0].count) {
@@ -51,8 +54,8 @@ __device__ __forceinline__ const SvtFamily& family_of(const SvtParams& p, int bl
   return p.fam[0];
 }
 
-// Lifted element L at (row i of Ahat, storage column u) from staged weighted
-// spectra wl[b * len + n].
+// Lifted element L at (row i of Ahat, storage column u) from the staged
+// weighted spectra wl[b * len + n].
 __device__ __forceinline__ float2 lift_elem(const float2* wl, const SvtFamily& F, int i, int u) {
   if (!F.wide) {
     const int b = u / F.q, t = u - b * F.q;
@@ -63,205 +66,278 @@ __device__ __forceinline__ float2 lift_elem(const float2* wl, const SvtFamily& F
   }
 }
 
-}  // namespace
+// Shared state of one CTA.
+template <int DP>
+struct Smem {
+  float2* G;     // DP x (DP+1): Gram / V1 / G2 / W (off-diagonal upper repr. in Jacobi)
+  double* dg;    // DP: diagonal of G (fp64)
+  float2* wl;    // B x len weighted spectra
+  float2* acc;   // B x len adjoint accumulators
+  float2* A;     // R x DP chunk of Ahat (also V panel staging)
+  float2* X;     // R x DP chunk of D / B = Ahat V1 / T
+  SlotRec* rec;  // 2 x S (current / next round)
+  float* f;      // DP shrink factors
+  int* flags;    // 4
+  float* scal;   // 4
+};
 
+// Ahat chunk rows [i0, i0 + rows) into S.A (zero padded to R x DP); with
+// want_d the raw D rows go to S.X.
 template <int DP, int R>
-__global__ void __launch_bounds__(4 * DP, 1) hankel_svt_kernel(const SvtParams prm) {
-  constexpr int NT = 4 * DP;
-  constexpr int S = DP / 2;         // slots
-  constexpr int W = DP / 8;         // slots per V thread (4 groups)
-  constexpr int HALF = DP / 2;      // GEMM column pairs
-  constexpr int GS = DP + 1;        // G / W row stride
-  static_assert(DP % 8 == 0 && DP >= 8 && DP <= 128, "DP must be a multiple of 8 in [8,128]");
-  static_assert(R % 8 == 0, "R must be a multiple of 8");
-
-  if (prm.skip && *prm.skip) return;
-  int mat;
-  const SvtFamily& F = family_of(prm, blockIdx.x, mat);
-  const int tid = threadIdx.x;
-  const int d = F.d, e = F.e, len = F.len, B = F.B, J = F.J;
-  const bool admm = prm.mode != SVT_PLAIN;
-  const bool weighted = prm.mode == SVT_ADMM_WEIGHTED;
-
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  float2* Gs = reinterpret_cast<float2*>(smem_raw);            // DP x GS
-  float2* wl = Gs + DP * GS;                                   // B x len
-  float2* acc = wl + B * len;                                  // B x len
-  float2* Abuf = acc + B * len;                                // R x DP
-  float2* Dbuf = Abuf + R * DP;                                // R x DP
-  RotParam* prmS = reinterpret_cast<RotParam*>(Dbuf + R * DP); // S
-  float* fbuf = reinterpret_cast<float*>(prmS + S);            // DP
-  int* flags = reinterpret_cast<int*>(fbuf + DP);              // 4
-  float* scal = reinterpret_cast<float*>(flags + 4);           // 4
-
-  float2* Dg = admm ? F.D + (long long)mat * e * d : nullptr;
-
-  // ---------------------------------------------------------- phase 0
-  {
-    const float2* sp = F.spec + (long long)mat * F.s_mat;
-    for (int t = tid; t < J * len; t += NT) {
-      const int j = t / len, n = t - j * len;
-      float2 s = sp[n * F.s_n + j * F.s_j];
-      if (weighted) {
-        wl[j * len + n] = cmul(F.wc[n], s);
-        if (F.vc) {
-          const int fl = dagger_src(n, len);
-          const float2 sf = sp[fl * F.s_n + j * F.s_j];
-          wl[(J + j) * len + n] = cmul(F.wc[n], cconj(sf));
-        }
-      } else {
-        wl[j * len + n] = s;
+__device__ __forceinline__ void load_chunk(const Smem<DP>& S, const SvtFamily& F, const float2* Dg,
+                                           int i0, int rows, float inv_beta, bool want_d) {
+  const int d = F.d;
+  for (int t = threadIdx.x; t < R * DP; t += blockDim.x) {
+    const int r = t / DP, u = t - r * DP;
+    float2 v = make_float2(0.f, 0.f), dd = make_float2(0.f, 0.f);
+    if (r < rows && u < d) {
+      v = lift_elem(S.wl, F, i0 + r, u);
+      if (Dg) {
+        dd = Dg[(long long)(i0 + r) * d + u];
+        v.x = fmaf(dd.x, inv_beta, v.x);
+        v.y = fmaf(dd.y, inv_beta, v.y);
       }
     }
-    for (int t = tid; t < B * len; t += NT) acc[t] = make_float2(0.f, 0.f);
-    if (tid < 4) flags[tid] = 0;
+    S.A[t] = v;
+    if (want_d) S.X[t] = dd;
   }
-  __syncthreads();
+}
 
-  // GEMM tile coordinates
-  const int lp = tid % HALF;          // column pair -> columns 2lp, 2lp+1
-  const int kq = tid / HALF;          // 0..7
-  const int l0 = 2 * lp;
-
-  // ---------------------------------------------------------- phase 1: Gram
-  {
-    float2 g0[W], g1[W];
-#pragma unroll
-    for (int m = 0; m < W; ++m) g0[m] = g1[m] = make_float2(0.f, 0.f);
-    for (int i0 = 0; i0 < e; i0 += R) {
-      const int rows = min(R, e - i0);
-      for (int t = tid; t < R * DP; t += NT) {
-        const int r = t / DP, u = t - r * DP;
-        float2 v = make_float2(0.f, 0.f);
-        if (r < rows && u < d) {
-          v = lift_elem(wl, F, i0 + r, u);
-          if (admm) {
-            const float2 dd = Dg[(long long)(i0 + r) * d + u];
-            v.x = fmaf(dd.x, prm.inv_beta, v.x);
-            v.y = fmaf(dd.y, prm.inv_beta, v.y);
-          }
-        }
-        Abuf[t] = v;
-      }
-      __syncthreads();
-      for (int r = 0; r < rows; ++r) {
-        const float2* row = Abuf + r * DP;
-        const float2 b0 = row[l0], b1 = row[l0 + 1];
-#pragma unroll
-        for (int m = 0; m < W; ++m) {
-          const float2 a = row[kq + 8 * m];
-          cfmac(g0[m], a, b0);
-          cfmac(g1[m], a, b1);
-        }
-      }
-      __syncthreads();
-    }
+// Gram-type accumulation acc[m][c] += sum_r conj(src[r][kq+8m]) src[r][l0+c].
+template <int DP, int W>
+__device__ __forceinline__ void gram_accumulate(const float2* src, int rows, int kq, int l0,
+                                                float2 (&g0)[W], float2 (&g1)[W]) {
+  for (int r = 0; r < rows; ++r) {
+    const float2* row = src + r * DP;
+    const float2 b0 = row[l0], b1 = row[l0 + 1];
 #pragma unroll
     for (int m = 0; m < W; ++m) {
-      const int k = kq + 8 * m;
-      Gs[k * GS + l0] = g0[m];
-      Gs[k * GS + l0 + 1] = g1[m];
+      const float2 a = row[kq + 8 * m];
+      cfmac(g0[m], a, b0);
+      cfmac(g1[m], a, b1);
     }
   }
-  __syncthreads();
+}
 
-  // ---------------------------------------------------------- phase 2: Jacobi
-  const int vrow = tid >> 2, vg = tid & 3;
-  float2 vt[W], vb[W];
-#pragma unroll
-  for (int w = 0; w < W; ++w) {
-    const int s = vg * W + w;
-    const int t0 = s == 0 ? DP - 1 : s - 1;
-    const int b0 = DP - 2 - s;
-    vt[w] = make_float2(vrow == t0 ? 1.f : 0.f, 0.f);
-    vb[w] = make_float2(vrow == b0 ? 1.f : 0.f, 0.f);
+// Gram tile entries (k, l0) and (k, l0+1) into the full Hermitian storage:
+// the upper-triangle value is written to both (k, l) and conj to (l, k), the
+// real diagonal to S.dg.
+template <int DP>
+__device__ __forceinline__ void store_gram_pair(const Smem<DP>& S, int k, int l0, float2 g0, float2 g1) {
+  constexpr int GS = DP + 1;
+  if (k < l0) {
+    S.G[k * GS + l0] = g0;
+    S.G[l0 * GS + k] = cconj(g0);
   }
-  if (tid < 32) {
-    float mx = 0.f;
-    for (int u = tid; u < DP; u += 32) mx = fmaxf(mx, Gs[u * GS + u].x);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if (tid == 0) scal[0] = kTolAbs * mx;
+  if (k < l0 + 1) {
+    S.G[k * GS + l0 + 1] = g1;
+    S.G[(l0 + 1) * GS + k] = cconj(g1);
   }
-  __syncthreads();
-  const float tol_abs = scal[0];
-  constexpr int NBLK = S * (S + 1) / 2;
+  if (k == l0) S.dg[k] = g0.x;
+  if (k == l0 + 1) S.dg[k] = g1.x;
+}
 
-  for (int sweep = 0; sweep < prm.max_sweeps; ++sweep) {
-    int* rot_flag = &flags[sweep & 1];
-    for (int r = 0; r < DP - 1; ++r) {
-      if (tid < S) {
-        const int s = tid;
-        const int a = top_of(s, r, DP), b = bot_of(s, r, DP);
-        const float al = Gs[a * GS + a].x, be = Gs[b * GS + b].x;
-        const float2 gm = gget<DP>(Gs, a, b);
-        const float g = hypotf(gm.x, gm.y);
-        RotParam rp;
-        rp.flag = 0;
-        if (g > 0.f && g > tol_abs && g > kTolRel * sqrtf(fmaxf(al * be, 0.f))) {
-          const float zeta = (be - al) / (2.f * g);
-          const float az = fabsf(zeta);
-          float t = (az > 1e18f) ? 0.5f / az : 1.f / (az + sqrtf(1.f + az * az));
-          t = zeta < 0.f ? -t : t;
-          const float c = rsqrtf(1.f + t * t);
-          const float sn = c * t;
-          const float2 ph = make_float2(gm.x / g, -gm.y / g);  // conj(g)/|g|
-          rp.c = c;
-          rp.sn = sn;
-          rp.cw = cscale(ph, c);
-          rp.sw = cscale(ph, sn);
-          rp.na = al - t * g;
-          rp.nb = be + t * g;
-          rp.flag = 1;
-          *rot_flag = 1;
-        }
-        prmS[s] = rp;
+// out[kq+8m][l0..l0+1] = sum_k A[kq+8m][k] * Bm[k][l0..l0+1], k < kmax.
+template <int DP, int RM>
+__device__ __forceinline__ void chunk_gemm(const float2* A, const float2* Bm, int kmax, int kq, int l0,
+                                           float2 (&z0)[RM], float2 (&z1)[RM]) {
+  constexpr int GS = DP + 1;
+#pragma unroll
+  for (int m = 0; m < RM; ++m) z0[m] = z1[m] = make_float2(0.f, 0.f);
+  for (int k = 0; k < kmax; ++k) {
+    const float2 w0 = Bm[k * GS + l0], w1 = Bm[k * GS + l0 + 1];
+#pragma unroll
+    for (int m = 0; m < RM; ++m) {
+      const float2 a = A[(kq + 8 * m) * DP + k];
+      cfma(z0[m], a, w0);
+      cfma(z1[m], a, w1);
+    }
+  }
+}
+
+// Rotation that annihilates g = G[a][b] given the current diagonal entries
+// (al, be): rotate iff |g| > tol_rel sqrt(al be) and |g| > tol_abs.
+__device__ __forceinline__ bool make_rotation(SlotRec& rc, int a, int b, double al, double be,
+                                              float2 gm, float tol_rel, float tol_abs) {
+  rc.a = a;
+  rc.b = b;
+  rc.flag = 0;
+  rc.c = 1.f;
+  rc.sn = 0.f;
+  rc.cw = make_float2(1.f, 0.f);
+  rc.sw = make_float2(0.f, 0.f);
+  rc.na = al;
+  rc.nb = be;
+  const float g = hypotf(gm.x, gm.y);
+  const float alf = (float)al, bef = (float)be;
+  if (!(g > 0.f && g > tol_abs && g > tol_rel * sqrtf(fmaxf(alf * bef, 0.f)))) return false;
+#ifdef SHLR_ROT_FP64
+  {
+    const double zeta = (be - al) / (2.0 * (double)g);
+    const double az = fabs(zeta);
+    double t = 1.0 / (az + sqrt(1.0 + az * az));
+    t = zeta < 0.0 ? -t : t;
+    const double ci = 1.0 / sqrt(1.0 + t * t);
+    const float2 ph = make_float2(gm.x / g, -gm.y / g);
+    rc.c = (float)ci;
+    rc.sn = (float)(t * ci);
+    rc.cw = cscale(ph, rc.c);
+    rc.sw = cscale(ph, rc.sn);
+    rc.na = al - t * (double)g;
+    rc.nb = be + t * (double)g;
+    rc.flag = 1;
+    return true;
+  }
+#endif
+  // the difference of the diagonal entries in fp64 (they may be close), the
+  // angle in fp32, the diagonal update in fp64
+  const float ig = __frcp_rn(g);
+  const float zeta = (float)(be - al) * (0.5f * ig);
+  const float az = fabsf(zeta);
+  float t = az > 1e18f ? 0.5f / az : __frcp_rn(az + sqrtf(fmaf(az, az, 1.f)));
+  t = zeta < 0.f ? -t : t;
+  const float c = 1.0f / sqrtf(fmaf(t, t, 1.f));  // IEEE sqrt/div: c^2 + s^2 = 1 to 1 ulp
+  const float sn = t * c;
+  const float2 ph = make_float2(gm.x * ig, -gm.y * ig);  // conj(g)/|g|
+  rc.c = c;
+  rc.sn = sn;
+  rc.cw = cscale(ph, c);
+  rc.sw = cscale(ph, sn);
+  const double tg = (double)t * (double)g;
+  rc.na = al - tg;
+  rc.nb = be + tg;
+  rc.flag = 1;
+  return true;
+}
+
+// Parallel cyclic Jacobi on S.G (off-diagonal, upper representation) and
+// S.dg (diagonal, fp64) with V held in registers (vt/vb, 4 threads per row).
+//
+// One barrier per round: the rotation of slot s for round r+1 pairs
+// (top_r(s-1), bot_r(s+1)) -- an element of block (s-1, s+1) of round r --
+// so the thread that updates that block computes the next rotation on the
+// spot (diagonal entries come from the round-r rotation records).  Special
+// cases: slot 0 <- block (0,1) element (top0, bot1); slot 1 <- block (0,2)
+// element (bot0, bot2); slot S-1 <- block (S-2,S-1) element (top, top).
+// Returns the number of sweeps; the final diagonal is written to S.dg.
+template <int DP, int W>
+__device__ int jacobi(const Smem<DP>& S, float2 (&vt)[W], float2 (&vb)[W], float tol_rel,
+                      float tol_abs, int max_sweeps) {
+  constexpr int NT = 4 * DP;
+  constexpr int S_ = DP / 2;
+  constexpr int GS = DP + 1;
+  const int tid = threadIdx.x;
+  const int vg = tid & 3;
+  // Work items q = tid + k*NT: items 0..S-1 are the S rotation-carrying
+  // blocks (threads 0..S-1, i.e. the first warps only, so the rotation math
+  // does not diverge every warp); the remaining off-diagonal blocks follow in
+  // row-major order (consecutive lanes -> consecutive s2 -> conflict-free).
+  constexpr int NOFF = S_ * (S_ - 1) / 2;
+  constexpr int NBT = (NOFF + NT - 1) / NT;
+  int blk_code[NBT];  // s1 | s2 << 8 | (carrier + 1) << 16, or -1
+#pragma unroll
+  for (int k = 0; k < NBT; ++k) {
+    const int q = tid + k * NT;
+    int s1 = -1, s2 = -1, cr = -1;
+    if (q < S_) {
+      const int s = q;
+      if (s == 0) {
+        s1 = 0; s2 = 1; cr = 0;
+      } else if (s == 1) {
+        s1 = 0; s2 = 2; cr = (1 << 2) | 1;
+      } else if (s == S_ - 1) {
+        s1 = S_ - 2; s2 = S_ - 1; cr = ((S_ - 1) << 2) | 2;
+      } else {
+        s1 = s - 1; s2 = s + 1; cr = s << 2;
       }
-      __syncthreads();
-      // G <- J^H G J on slot-pair blocks (s1 <= s2)
-      for (int blk = tid; blk < NBLK; blk += NT) {
-        // triangular decode: row s1 holds S - s1 entries
-        int s1 = (int)((2.f * S + 1.f - sqrtf((2.f * S + 1.f) * (2.f * S + 1.f) - 8.f * blk)) * 0.5f);
-        int base = s1 * S - (s1 * (s1 - 1)) / 2;
-        while (s1 > 0 && base > blk) { --s1; base = s1 * S - (s1 * (s1 - 1)) / 2; }
-        while (blk >= base + (S - s1)) { base += S - s1; ++s1; }
-        const int s2 = s1 + (blk - base);
-        const RotParam& p1 = prmS[s1];
-        const RotParam& p2 = prmS[s2];
-        if (!p1.flag && !p2.flag) continue;
-        const int x0 = top_of(s1, r, DP), x1 = bot_of(s1, r, DP);
-        if (s1 == s2) {
-          Gs[x0 * GS + x0] = make_float2(p1.na, 0.f);
-          Gs[x1 * GS + x1] = make_float2(p1.nb, 0.f);
-          gput<DP>(Gs, x0, x1, make_float2(0.f, 0.f));
-          continue;
+    } else if (q < NOFF) {
+      // j-th non-carrying block in row-major order
+      int j = q - S_;
+      for (int row = 0; row < S_ - 2; ++row) {
+        const int first = row == 0 ? 3 : row + 1;             // row 0 skips (0,1),(0,2)
+        const int cnt = row == 0 ? S_ - 3 : S_ - 2 - row;      // rows >= 1 skip (row,row+2)
+        if (j < cnt) {
+          s1 = row;
+          s2 = first + j;
+          if (row >= 1 && s2 >= row + 2) ++s2;
+          break;
         }
-        const int y0 = top_of(s2, r, DP), y1 = bot_of(s2, r, DP);
-        float2 a00 = gget<DP>(Gs, x0, y0), a01 = gget<DP>(Gs, x0, y1);
-        float2 a10 = gget<DP>(Gs, x1, y0), a11 = gget<DP>(Gs, x1, y1);
-        if (p2.flag) {  // X J2 on columns
+        j -= cnt;
+      }
+    }
+    blk_code[k] = s1 < 0 ? -1 : (s1 | (s2 << 8) | ((cr + 1) << 16));
+  }
+  // rotations of round 0 of the first sweep
+  if (tid < S_) {
+    const int a = top_of(tid, 0, DP), b = bot_of(tid, 0, DP);
+    SlotRec rc;
+    if (make_rotation(rc, a, b, S.dg[a], S.dg[b], S.G[a * GS + b], tol_rel, tol_abs)) {
+      S.G[a * GS + b] = make_float2(0.f, 0.f);
+      S.G[b * GS + a] = make_float2(0.f, 0.f);
+      S.flags[0] = 1;
+    }
+    S.rec[tid] = rc;
+  }
+  __syncthreads();
+  int cur = 0;
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    for (int r = 0; r < DP - 1; ++r) {
+      const SlotRec* rc = S.rec + cur * S_;
+      SlotRec* rn = S.rec + (cur ^ 1) * S_;
+      int* next_flag = &S.flags[(r == DP - 2) ? ((sweep + 1) & 1) : (sweep & 1)];
+#pragma unroll
+      for (int k = 0; k < NBT; ++k) {
+        const int code = blk_code[k];
+        if (code < 0) continue;
+        const int s1 = code & 0xff, s2 = (code >> 8) & 0xff, cr = (code >> 16) - 1;
+        const SlotRec& p1 = rc[s1];
+        const SlotRec& p2 = rc[s2];
+        if (cr < 0 && !(p1.flag | p2.flag)) continue;
+        const int x0 = p1.a, x1 = p1.b, y0 = p2.a, y1 = p2.b;
+        // full Hermitian storage: read the (x, y) orientation, write both
+        float2 a00 = S.G[x0 * GS + y0], a01 = S.G[x0 * GS + y1];
+        float2 a10 = S.G[x1 * GS + y0], a11 = S.G[x1 * GS + y1];
+        {  // X J2 (columns); identity parameters are exact
           const float2 n00 = csub(cscale(a00, p2.c), cmul(p2.sw, a01));
           const float2 n01 = cadd(cscale(a00, p2.sn), cmul(p2.cw, a01));
           const float2 n10 = csub(cscale(a10, p2.c), cmul(p2.sw, a11));
           const float2 n11 = cadd(cscale(a10, p2.sn), cmul(p2.cw, a11));
           a00 = n00; a01 = n01; a10 = n10; a11 = n11;
         }
-        if (p1.flag) {  // J1^H X on rows
+        {  // J1^H X (rows)
           const float2 n00 = csub(cscale(a00, p1.c), cmulc(p1.sw, a10));
           const float2 n10 = cadd(cscale(a00, p1.sn), cmulc(p1.cw, a10));
           const float2 n01 = csub(cscale(a01, p1.c), cmulc(p1.sw, a11));
           const float2 n11 = cadd(cscale(a01, p1.sn), cmulc(p1.cw, a11));
           a00 = n00; a01 = n01; a10 = n10; a11 = n11;
         }
-        gput<DP>(Gs, x0, y0, a00);
-        gput<DP>(Gs, x0, y1, a01);
-        gput<DP>(Gs, x1, y0, a10);
-        gput<DP>(Gs, x1, y1, a11);
+        if (cr >= 0) {  // next-round rotation carried by this block
+          const int kind = cr & 3, slot = cr >> 2;
+          const int ra = kind == 1 ? x1 : x0;
+          const int rb = kind == 2 ? y0 : y1;
+          const double al = kind == 1 ? p1.nb : p1.na;
+          const double be = kind == 2 ? p2.na : p2.nb;
+          const float2 gm = kind == 0 ? a01 : (kind == 1 ? a11 : a00);
+          SlotRec nr;
+          if (make_rotation(nr, ra, rb, al, be, gm, tol_rel, tol_abs)) {
+            const float2 z = make_float2(0.f, 0.f);
+            if (kind == 0) a01 = z;
+            if (kind == 1) a11 = z;
+            if (kind == 2) a00 = z;
+            *next_flag = 1;
+          }
+          rn[slot] = nr;
+        }
+        S.G[x0 * GS + y0] = a00; S.G[x0 * GS + y1] = a01;
+        S.G[x1 * GS + y0] = a10; S.G[x1 * GS + y1] = a11;
+        S.G[y0 * GS + x0] = cconj(a00); S.G[y1 * GS + x0] = cconj(a01);
+        S.G[y0 * GS + x1] = cconj(a10); S.G[y1 * GS + x1] = cconj(a11);
       }
       // V <- V J on this thread's slots
 #pragma unroll
       for (int w = 0; w < W; ++w) {
-        const RotParam& p = prmS[vg * W + w];
+        const SlotRec& p = rc[vg * W + w];
         if (p.flag) {
           const float2 a = vt[w], b = vb[w];
           vt[w] = csub(cscale(a, p.c), cmul(p.sw, b));
@@ -269,7 +345,8 @@ __global__ void __launch_bounds__(4 * DP, 1) hankel_svt_kernel(const SvtParams p
         }
       }
       __syncthreads();
-      // ring shift of V columns: top moves right, bottom moves left
+      cur ^= 1;
+      // ring shift of the V columns: tops move right, bottoms move left
       {
         const float2 up_t = make_float2(__shfl_up_sync(0xffffffffu, vt[W - 1].x, 1, 4),
                                         __shfl_up_sync(0xffffffffu, vt[W - 1].y, 1, 4));
@@ -278,7 +355,7 @@ __global__ void __launch_bounds__(4 * DP, 1) hankel_svt_kernel(const SvtParams p
         const float2 dn_b = make_float2(__shfl_down_sync(0xffffffffu, vb[0].x, 1, 4),
                                         __shfl_down_sync(0xffffffffu, vb[0].y, 1, 4));
         float2 nt[W], nb[W];
-        if (W == 1) {
+        if constexpr (W == 1) {
           nt[0] = vg == 0 ? vt[0] : (vg == 1 ? up_b : up_t);
         } else {
           nt[0] = vg == 0 ? vt[0] : up_t;
@@ -296,50 +373,235 @@ __global__ void __launch_bounds__(4 * DP, 1) hankel_svt_kernel(const SvtParams p
         }
       }
     }
+    // every rotation of this sweep has been decided (the last round decided
+    // round 0 of the next sweep into the other flag)
+    const int any = S.flags[sweep & 1];
     __syncthreads();
-    const int any = *rot_flag;
-    if (tid == 0) flags[(sweep + 1) & 1] = 0;
-    __syncthreads();
-    if (prm.sweeps_out && tid == 0) prm.sweeps_out[blockIdx.x] = sweep + 1;
-    if (!any) break;
+    if (tid == 0) S.flags[sweep & 1] = 0;
+    if (!any) {
+      ++sweep;
+      break;
+    }
   }
+  // final diagonal: the pending (identity after convergence) records hold it
+  if (tid < S_) {
+    const SlotRec& p = S.rec[cur * S_ + tid];
+    S.dg[p.a] = p.na;
+    S.dg[p.b] = p.nb;
+  }
+  if (tid < 2) S.flags[tid] = 0;
+  __syncthreads();
+  return sweep;
+}
 
-  // ---------------------------------------------------------- phase 3: f, W
+// V (registers, round-0 arrangement) <-> row-major DP x DP storage.
+template <int DP, int W>
+__device__ __forceinline__ void store_v(float2* dst, int stride, const float2 (&vt)[W],
+                                        const float2 (&vb)[W]) {
+  const int vrow = threadIdx.x >> 2, vg = threadIdx.x & 3;
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    const int s = vg * W + w;
+    dst[vrow * stride + top0(s, DP)] = vt[w];
+    dst[vrow * stride + bot0(s, DP)] = vb[w];
+  }
+}
+template <int DP, int W>
+__device__ __forceinline__ void load_v(const float2* src, int stride, float2 (&vt)[W], float2 (&vb)[W]) {
+  const int vrow = threadIdx.x >> 2, vg = threadIdx.x & 3;
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    const int s = vg * W + w;
+    vt[w] = src[vrow * stride + top0(s, DP)];
+    vb[w] = src[vrow * stride + bot0(s, DP)];
+  }
+}
+
+}  // namespace
+
+// Registers per thread when one CTA of 4*DP threads (DP/8 warps) owns the
+// SM: each of the 4 sub-partitions holds ceil(warps/4) warps in its 16K-entry
+// register file.
+constexpr int svt_max_regs(int DP) {
+  return (512 / ((DP / 8 + 3) / 4)) / 8 * 8 > 255 ? 255 : (512 / ((DP / 8 + 3) / 4)) / 8 * 8;
+}
+
+template <int DP, int R>
+__global__ void __maxnreg__(svt_max_regs(DP)) hankel_svt_kernel(const SvtParams prm) {
+  // (one CTA per SM: the whole register file is available to its 4*DP threads)
+  constexpr int NT = 4 * DP;
+  constexpr int S_ = DP / 2;
+  constexpr int W = DP / 8;
+  constexpr int HALF = DP / 2;
+  constexpr int GS = DP + 1;
+  constexpr int RM = R / 8;
+  static_assert(DP % 8 == 0 && DP >= 8 && DP <= 128, "DP must be a multiple of 8 in [8,128]");
+  static_assert(R % 8 == 0, "R must be a multiple of 8");
+
+  if (prm.skip && *prm.skip) return;
+  int mat;
+  const SvtFamily& F = family_of(prm, blockIdx.x, mat);
+  const int tid = threadIdx.x;
+  const int d = F.d, e = F.e, len = F.len, B = F.B, J = F.J;
+  const bool admm = prm.mode != SVT_PLAIN;
+  const bool weighted = prm.mode == SVT_ADMM_WEIGHTED;
+
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem<DP> S;
+  S.G = reinterpret_cast<float2*>(smem_raw);
+  S.wl = S.G + DP * GS;
+  S.acc = S.wl + B * len;
+  S.A = S.acc + B * len;
+  S.X = S.A + R * DP;
+  S.rec = reinterpret_cast<SlotRec*>(S.X + R * DP);
+  S.dg = reinterpret_cast<double*>(S.rec + 2 * S_);
+  S.f = reinterpret_cast<float*>(S.dg + DP);
+  S.flags = reinterpret_cast<int*>(S.f + DP);
+  S.scal = reinterpret_cast<float*>(S.flags + 4);
+
+  float2* Dg = admm ? F.D + (long long)mat * e * d : nullptr;
+  float2* Vg = F.V + (long long)mat * DP * DP;
+  const bool warm = prm.warm && *prm.warm;
+  const bool exact_sv = F.sv != nullptr;
+
+  // ---------------------------------------------------------- phase 0
   {
-    for (int u = tid; u < DP; u += NT) {
-      const float lam = Gs[u * GS + u].x;
-      float f = 0.f;
-      if (lam > prm.thresh * prm.thresh && lam > 0.f) f = 1.f - prm.thresh / sqrtf(lam);
-      fbuf[u] = f;
+    const float2* sp = F.spec + (long long)mat * F.s_mat;
+    for (int t = tid; t < J * len; t += NT) {
+      const int j = t / len, n = t - j * len;
+      const float2 s = sp[n * F.s_n + j * F.s_j];
+      if (weighted) {
+        S.wl[j * len + n] = cmul(F.wc[n], s);
+        if (F.vc) {
+          const int fl = dagger_src(n, len);
+          const float2 sf = sp[fl * F.s_n + j * F.s_j];
+          S.wl[(J + j) * len + n] = cmul(F.wc[n], cconj(sf));
+        }
+      } else {
+        S.wl[j * len + n] = s;
+      }
+    }
+    for (int t = tid; t < B * len; t += NT) S.acc[t] = make_float2(0.f, 0.f);
+    if (tid < 4) S.flags[tid] = 0;
+  }
+  __syncthreads();
+
+  const int lp = tid % HALF;   // GEMM column pair -> columns 2lp, 2lp+1
+  const int kq = tid / HALF;   // 0..7
+  const int l0 = 2 * lp;
+  float2 vt[W], vb[W];
+  int sweeps1 = 0;
+
+  // ---------------------------------------------------------- stage 1 (cold)
+  if (!warm) {
+    {
+      float2 g0[W], g1[W];
+#pragma unroll
+      for (int m = 0; m < W; ++m) g0[m] = g1[m] = make_float2(0.f, 0.f);
+      for (int i0 = 0; i0 < e; i0 += R) {
+        const int rows = min(R, e - i0);
+        load_chunk<DP, R>(S, F, Dg, i0, rows, prm.inv_beta, false);
+        __syncthreads();
+        gram_accumulate<DP, W>(S.A, rows, kq, l0, g0, g1);
+        __syncthreads();
+      }
+#pragma unroll
+      for (int m = 0; m < W; ++m) store_gram_pair<DP>(S, kq + 8 * m, l0, g0[m], g1[m]);
     }
     __syncthreads();
-    if (F.sv) {
-      float* sv = F.sv + (long long)mat * d;
-      for (int u = tid; u < d; u += NT) {
-        const float su = sqrtf(fmaxf(Gs[u * GS + u].x, 0.f));
-        int rank = 0;
-        for (int v = 0; v < d; ++v) {
-          const float s2 = sqrtf(fmaxf(Gs[v * GS + v].x, 0.f));
-          rank += (s2 > su) || (s2 == su && v < u);
-        }
-        sv[rank] = su;
+    if (tid < 32) {
+      double mx = 0.0;
+      for (int u = tid; u < DP; u += 32) mx = fmax(mx, S.dg[u]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      if (tid == 0) S.scal[0] = (float)(kTolAbs1 * mx);
+    }
+    {
+      const int vrow = tid >> 2, vg = tid & 3;
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        const int s = vg * W + w;
+        vt[w] = make_float2(vrow == top0(s, DP) ? 1.f : 0.f, 0.f);
+        vb[w] = make_float2(vrow == bot0(s, DP) ? 1.f : 0.f, 0.f);
       }
     }
     __syncthreads();
-    for (int t = tid; t < DP * GS; t += NT) Gs[t] = make_float2(0.f, 0.f);
-    // panel staging area: DP x 2W in Abuf/Dbuf (R*DP*2 >= DP*2W)
-    float2* panel = Abuf;
+    sweeps1 = jacobi<DP, W>(S, vt, vb, kTolRel1, S.scal[0], prm.max_sweeps);
+    // V1 -> smem (refinement GEMM operand) and HBM (reloaded for stage 2)
+    store_v<DP, W>(S.G, GS, vt, vb);
+    store_v<DP, W>(Vg, DP, vt, vb);
+  } else {
+    for (int t = tid; t < DP * DP; t += NT) {
+      const int k = t / DP, l = t - k * DP;
+      S.G[k * GS + l] = Vg[t];
+    }
+  }
+  __syncthreads();
+
+  // ---------------------------------------------------------- refinement: G2 = (Ahat V1)^H (Ahat V1)
+  {
+    float2 g0[W], g1[W];
+#pragma unroll
+    for (int m = 0; m < W; ++m) g0[m] = g1[m] = make_float2(0.f, 0.f);
+    for (int i0 = 0; i0 < e; i0 += R) {
+      const int rows = min(R, e - i0);
+      load_chunk<DP, R>(S, F, Dg, i0, rows, prm.inv_beta, false);
+      __syncthreads();
+      float2 z0[RM], z1[RM];
+      chunk_gemm<DP, RM>(S.A, S.G, d, kq, l0, z0, z1);
+#pragma unroll
+      for (int m = 0; m < RM; ++m) {
+        S.X[(kq + 8 * m) * DP + l0] = z0[m];
+        S.X[(kq + 8 * m) * DP + l0 + 1] = z1[m];
+      }
+      __syncthreads();
+      gram_accumulate<DP, W>(S.X, rows, kq, l0, g0, g1);
+      __syncthreads();
+    }
+    // V1 is no longer needed in smem: G2 takes its place
+#pragma unroll
+    for (int m = 0; m < W; ++m) store_gram_pair<DP>(S, kq + 8 * m, l0, g0[m], g1[m]);
+  }
+  load_v<DP, W>(Vg, DP, vt, vb);  // this thread's own stage-1 / previous-iteration values
+  __syncthreads();
+  // stage 2: relative criterion only (G2 is accurate relative to its entries)
+  const int sweeps2 = jacobi<DP, W>(S, vt, vb, kTolRel2, 0.f, prm.max_sweeps);
+  if (prm.sweeps_out && tid == 0) prm.sweeps_out[blockIdx.x] = sweeps1 * 100 + sweeps2;
+  store_v<DP, W>(Vg, DP, vt, vb);
+
+  // ---------------------------------------------------------- phase 3: f, W = V f V^H
+  {
+    for (int u = tid; u < DP; u += NT) {
+      const double lam = S.dg[u];
+      float f = 0.f;
+      if (lam > (double)prm.thresh * prm.thresh && lam > 0.0) f = (float)(1.0 - prm.thresh / sqrt(lam));
+      S.f[u] = f;
+    }
+    __syncthreads();
+    if (exact_sv) {
+      float* sv = F.sv + (long long)mat * d;
+      for (int u = tid; u < d; u += NT) {
+        const double su = sqrt(fmax(S.dg[u], 0.0));
+        int rank = 0;
+        for (int v = 0; v < d; ++v) {
+          const double s2 = sqrt(fmax(S.dg[v], 0.0));
+          rank += (s2 > su) || (s2 == su && v < u);
+        }
+        sv[rank] = (float)su;
+      }
+    }
+    for (int t = tid; t < DP * GS; t += NT) S.G[t] = make_float2(0.f, 0.f);
+    float2* panel = S.A;  // DP x 2W staging in the chunk buffers
     constexpr int PW = 2 * W;
+    const int vrow = tid >> 2, vg = tid & 3;
     for (int g = 0; g < 4; ++g) {
       __syncthreads();
       if (vg == g) {
 #pragma unroll
         for (int w = 0; w < W; ++w) {
           const int s = g * W + w;
-          const int ct = s == 0 ? DP - 1 : s - 1;
-          const int cb = DP - 2 - s;
-          panel[vrow * PW + 2 * w] = cscale(vt[w], sqrtf(fbuf[ct]));
-          panel[vrow * PW + 2 * w + 1] = cscale(vb[w], sqrtf(fbuf[cb]));
+          panel[vrow * PW + 2 * w] = cscale(vt[w], sqrtf(S.f[top0(s, DP)]));
+          panel[vrow * PW + 2 * w + 1] = cscale(vb[w], sqrtf(S.f[bot0(s, DP)]));
         }
       }
       __syncthreads();
@@ -349,99 +611,67 @@ __global__ void __launch_bounds__(4 * DP, 1) hankel_svt_kernel(const SvtParams p
         const float2* pk = panel + k * PW;
         const float2* pl0 = panel + l0 * PW;
         const float2* pl1 = panel + (l0 + 1) * PW;
-        float2 s0 = Gs[k * GS + l0], s1 = Gs[k * GS + l0 + 1];
+        float2 s0 = S.G[k * GS + l0], s1 = S.G[k * GS + l0 + 1];
 #pragma unroll
         for (int mm = 0; mm < PW; ++mm) {
           const float2 a = pk[mm];
-          // W[k][l] += U[k][m] conj(U[l][m])
-          cfmac(s0, pl0[mm], a);
+          cfmac(s0, pl0[mm], a);  // W[k][l] += U[k][m] conj(U[l][m])
           cfmac(s1, pl1[mm], a);
         }
-        Gs[k * GS + l0] = s0;
-        Gs[k * GS + l0 + 1] = s1;
+        S.G[k * GS + l0] = s0;
+        S.G[k * GS + l0 + 1] = s1;
       }
     }
     __syncthreads();
   }
 
   // ---------------------------------------------------------- phase 4: Z, D, T, adjoint
-  {
-    constexpr int RM = R / 8;
-    for (int i0 = 0; i0 < e; i0 += R) {
-      const int rows = min(R, e - i0);
-      for (int t = tid; t < R * DP; t += NT) {
-        const int r = t / DP, u = t - r * DP;
-        float2 v = make_float2(0.f, 0.f), dd = make_float2(0.f, 0.f);
-        if (r < rows && u < d) {
-          v = lift_elem(wl, F, i0 + r, u);
-          if (admm) {
-            dd = Dg[(long long)(i0 + r) * d + u];
-            v.x = fmaf(dd.x, prm.inv_beta, v.x);
-            v.y = fmaf(dd.y, prm.inv_beta, v.y);
-          }
-        }
-        Abuf[t] = v;
-        Dbuf[t] = dd;
-      }
-      __syncthreads();
-      float2 z0[RM], z1[RM];
+  for (int i0 = 0; i0 < e; i0 += R) {
+    const int rows = min(R, e - i0);
+    load_chunk<DP, R>(S, F, Dg, i0, rows, prm.inv_beta, true);
+    __syncthreads();
+    float2 z0[RM], z1[RM];
+    chunk_gemm<DP, RM>(S.A, S.G, d, kq, l0, z0, z1);
+    __syncthreads();
 #pragma unroll
-      for (int m = 0; m < RM; ++m) z0[m] = z1[m] = make_float2(0.f, 0.f);
-      for (int k = 0; k < d; ++k) {
-        const float2 w0 = Gs[k * GS + l0], w1 = Gs[k * GS + l0 + 1];
-#pragma unroll
-        for (int m = 0; m < RM; ++m) {
-          const float2 a = Abuf[(kq + 8 * m) * DP + k];
-          cfma(z0[m], a, w0);
-          cfma(z1[m], a, w1);
-        }
-      }
-      __syncthreads();
-#pragma unroll
-      for (int m = 0; m < RM; ++m) {
-        Abuf[(kq + 8 * m) * DP + l0] = z0[m];
-        Abuf[(kq + 8 * m) * DP + l0 + 1] = z1[m];
-      }
-      __syncthreads();
-      for (int t = tid; t < R * DP; t += NT) {
-        const int r = t / DP, u = t - r * DP;
-        if (r < rows && u < d) {
-          const float2 z = Abuf[t];
-          float2 tv = z;
-          if (admm) {
-            const float2 L = lift_elem(wl, F, i0 + r, u);
-            float2 dn = Dbuf[t];
-            dn.x = fmaf(prm.tau_dual, L.x - z.x, dn.x);
-            dn.y = fmaf(prm.tau_dual, L.y - z.y, dn.y);
-            Dg[(long long)(i0 + r) * d + u] = dn;
-            tv.x = fmaf(-dn.x, prm.inv_beta, z.x);
-            tv.y = fmaf(-dn.y, prm.inv_beta, z.y);
-          }
-          Dbuf[t] = tv;
-        }
-      }
-      __syncthreads();
-      // anti-diagonal sums (Hankel adjoint), fixed summation order
-      for (int o = tid; o < B * len; o += NT) {
-        const int b = o / len, n = o - b * len;
-        float2 s = acc[o];
-        if (!F.wide) {
-          // T[i][b*q + t], i + t = n, i in chunk, 0 <= t < q
-          const int ilo = max(i0, n - F.q + 1), ihi = min(i0 + rows - 1, n);
-          for (int i = ilo; i <= ihi; ++i) s = cadd(s, Dbuf[(i - i0) * DP + b * F.q + (n - i)]);
-        } else {
-          // rows i = b*q + t of That, T[k][b*q+t] = conj(That[i][k]), k + t = n
-          const int tlo = max(max(0, i0 - b * F.q), n - F.P + 1);
-          const int thi = min(min(F.q - 1, i0 + rows - 1 - b * F.q), n);
-          for (int t = tlo; t <= thi; ++t) {
-            const int i = b * F.q + t;
-            s = cadd(s, cconj(Dbuf[(i - i0) * DP + (n - t)]));
-          }
-        }
-        acc[o] = s;
-      }
-      __syncthreads();
+    for (int m = 0; m < RM; ++m) {
+      S.A[(kq + 8 * m) * DP + l0] = z0[m];
+      S.A[(kq + 8 * m) * DP + l0 + 1] = z1[m];
     }
+    __syncthreads();
+    for (int t = tid; t < R * DP; t += NT) {
+      const int r = t / DP, u = t - r * DP;
+      if (r < rows && u < d) {
+        const float2 z = S.A[t];
+        float2 tv = z;
+        if (admm) {
+          const float2 L = lift_elem(S.wl, F, i0 + r, u);
+          float2 dn = S.X[t];
+          dn.x = fmaf(prm.tau_dual, L.x - z.x, dn.x);
+          dn.y = fmaf(prm.tau_dual, L.y - z.y, dn.y);
+          Dg[(long long)(i0 + r) * d + u] = dn;
+          tv.x = fmaf(-dn.x, prm.inv_beta, z.x);
+          tv.y = fmaf(-dn.y, prm.inv_beta, z.y);
+        }
+        S.X[t] = tv;
+      }
+    }
+    __syncthreads();
+    // anti-diagonal sums (Hankel adjoint), fixed summation order
+    for (int o = tid; o < B * len; o += NT) {
+      const int b = o / len, n = o - b * len;
+      float2 s = S.acc[o];
+      if (!F.wide) {
+        const int ilo = max(i0, n - F.q + 1), ihi = min(i0 + rows - 1, n);
+        for (int i = ilo; i <= ihi; ++i) s = cadd(s, S.X[(i - i0) * DP + b * F.q + (n - i)]);
+      } else {
+        const int tlo = max(max(0, i0 - b * F.q), n - F.P + 1);
+        const int thi = min(min(F.q - 1, i0 + rows - 1 - b * F.q), n);
+        for (int t = tlo; t <= thi; ++t) s = cadd(s, cconj(S.X[(b * F.q + t - i0) * DP + (n - t)]));
+      }
+      S.acc[o] = s;
+    }
+    __syncthreads();
   }
 
   // ---------------------------------------------------------- phase 5: weighting + store
@@ -449,12 +679,12 @@ __global__ void __launch_bounds__(4 * DP, 1) hankel_svt_kernel(const SvtParams p
     float2* op = F.out + (long long)mat * F.o_mat;
     for (int t = tid; t < J * len; t += NT) {
       const int j = t / len, n = t - j * len;
-      float2 v = acc[j * len + n];
+      float2 v = S.acc[j * len + n];
       if (weighted) {
         v = cmulc(F.wc[n], v);  // conj(wc) * v
         if (F.vc) {
           const int fl = dagger_src(n, len);
-          v = cadd(v, cmul(F.wc[fl], cconj(acc[(J + j) * len + fl])));
+          v = cadd(v, cmul(F.wc[fl], cconj(S.acc[(J + j) * len + fl])));
         }
       }
       op[n * F.o_n + j * F.o_j] = v;
@@ -463,10 +693,12 @@ __global__ void __launch_bounds__(4 * DP, 1) hankel_svt_kernel(const SvtParams p
 }
 
 size_t svt_smem_bytes(int DP, int R, int maxB, int maxLen) {
-  const int S = DP / 2;
+  const int S_ = DP / 2;
   return sizeof(float2) * ((size_t)DP * (DP + 1) + 2ull * maxB * maxLen + 2ull * R * DP) +
-         sizeof(RotParam) * S + sizeof(float) * DP + 8 * sizeof(int) + 64;
+         sizeof(SlotRec) * 2 * S_ + sizeof(double) * DP + sizeof(float) * DP + 8 * sizeof(int) + 64;
 }
+
+int svt_padded_dim(int d) { return std::max(8, ((d + 7) / 8) * 8); }
 
 namespace {
 
@@ -485,9 +717,10 @@ void launch_one(const SvtParams& prm, int total, size_t smem, cudaStream_t strea
 template <int DP>
 void dispatch_r(const SvtParams& prm, int total, int maxB, int maxLen, cudaStream_t stream) {
   const size_t lim = 227 * 1024;
-  size_t s32 = svt_smem_bytes(DP, 32, maxB, maxLen);
+  const size_t s32 = svt_smem_bytes(DP, 32, maxB, maxLen);
+  // the W-panel staging needs 2 R DP >= DP * DP / 4 complex: true for R >= 16, DP <= 128
   if (s32 <= lim) return launch_one<DP, 32>(prm, total, s32, stream);
-  size_t s16 = svt_smem_bytes(DP, 16, maxB, maxLen);
+  const size_t s16 = svt_smem_bytes(DP, 16, maxB, maxLen);
   if (s16 <= lim) return launch_one<DP, 16>(prm, total, s16, stream);
   throw Unsupported("hankel_svt: shared-memory footprint exceeds 227 KB for this geometry");
 }
@@ -503,18 +736,25 @@ void launch_hankel_svt(const SvtParams& prm, int total, cudaStream_t stream) {
     maxLen = std::max(maxLen, prm.fam[f].len);
     if (prm.fam[f].J * prm.fam[f].len < 1) throw InvalidArg("hankel_svt: empty family");
   }
-  const int dp = ((dmax + 7) / 8) * 8;
+  const int dp = svt_padded_dim(dmax);
+  for (int f = 0; f < prm.nfam; ++f)
+    if (!prm.fam[f].V) throw InvalidArg("hankel_svt: missing eigenvector store");
   switch (dp) {
     case 8: return dispatch_r<8>(prm, total, maxB, maxLen, stream);
     case 16: return dispatch_r<16>(prm, total, maxB, maxLen, stream);
     case 24: return dispatch_r<24>(prm, total, maxB, maxLen, stream);
     case 32: return dispatch_r<32>(prm, total, maxB, maxLen, stream);
-    case 40: case 48: return dispatch_r<48>(prm, total, maxB, maxLen, stream);
-    case 56: case 64: return dispatch_r<64>(prm, total, maxB, maxLen, stream);
+    case 40: return dispatch_r<40>(prm, total, maxB, maxLen, stream);
+    case 48: return dispatch_r<48>(prm, total, maxB, maxLen, stream);
+    case 56: return dispatch_r<56>(prm, total, maxB, maxLen, stream);
+    case 64: return dispatch_r<64>(prm, total, maxB, maxLen, stream);
     case 72: return dispatch_r<72>(prm, total, maxB, maxLen, stream);
-    case 80: case 88: case 96: return dispatch_r<96>(prm, total, maxB, maxLen, stream);
+    case 80: return dispatch_r<80>(prm, total, maxB, maxLen, stream);
+    case 88: return dispatch_r<88>(prm, total, maxB, maxLen, stream);
+    case 96: return dispatch_r<96>(prm, total, maxB, maxLen, stream);
     case 104: return dispatch_r<104>(prm, total, maxB, maxLen, stream);
-    case 112: case 120: return dispatch_r<120>(prm, total, maxB, maxLen, stream);
+    case 112: return dispatch_r<112>(prm, total, maxB, maxLen, stream);
+    case 120: return dispatch_r<120>(prm, total, maxB, maxLen, stream);
     case 128: return dispatch_r<128>(prm, total, maxB, maxLen, stream);
     default:
       throw Unsupported("hankel_svt: min(m, n) = " + std::to_string(dmax) +

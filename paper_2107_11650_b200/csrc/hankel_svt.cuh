@@ -46,6 +46,8 @@ struct SvtFamily {
   const float2* wc;    // centred weights (len) for weighted modes
   float2* D;           // duals, per matrix e*d row-major (Ahat orientation)
   float* sv;           // optional: count x d singular values (descending)
+  float2* V;           // required: count x DP x DP eigenvector store (V1 spill and the
+                       // ADMM warm start; DP = svt_padded_dim of the launch)
 };
 
 struct SvtParams {
@@ -57,6 +59,7 @@ struct SvtParams {
   float thresh;        // SVT threshold (1/beta or lambda2/beta or user tau)
   int max_sweeps;
   const int* skip;     // optional device flag: nonzero -> kernel is a no-op
+  const int* warm;     // optional device flag: nonzero -> V holds a warm start
   int* sweeps_out;     // optional diagnostics: Jacobi sweeps used per matrix
 };
 
@@ -83,6 +86,7 @@ __host__ __device__ __forceinline__ LiftSrc lift_source(int i, int c, int q, int
 }
 
 size_t svt_smem_bytes(int DP, int R, int maxB, int maxLen);
+int svt_padded_dim(int d);
 void launch_hankel_svt(const SvtParams& prm, int total_matrices, cudaStream_t stream);
 
 }  // namespace shlr_b200

@@ -509,7 +509,7 @@ __global__ void __launch_bounds__(256) k_spirit_rows_fwd(const float2* __restric
 // the stop rule (solvers.cpp:183-187).
 __global__ void k_relchange(const float2* __restrict__ x, const float2* __restrict__ xold,
                             size_t nel, SolverCtl* ctl, double* partials, double* log, double tol,
-                            int max_outer) {
+                            int max_outer, int warm_enable) {
   __shared__ double sh[32];
   if (halted(ctl)) return;
   double sn = 0.0, sd = 0.0;
@@ -536,6 +536,7 @@ __global__ void k_relchange(const float2* __restrict__ x, const float2* __restri
     }
     ctl->outer = k + 1;
     if (rc < tol) ctl->stopped = 1;
+    ctl->have_v = warm_enable;  // the SVT of this iteration left its eigenvectors in HBM
     ctl->arrive[3] = 0;
   }
 }
@@ -704,6 +705,10 @@ PiPlan::PiPlan(const PiConfig& cfg, const double* y, const uint8_t* mask, size_t
   d_col_elems_ = (size_t)N * ec * dc;
   drow_ = dalloc<float2>(d_row_elems_);
   dcol_ = dalloc<float2>(d_col_elems_);
+  svt_dp_ = svt_padded_dim(std::max(dr, dc));
+  vrow_ = dalloc<float2>((size_t)M * svt_dp_ * svt_dp_);
+  vcol_ = dalloc<float2>((size_t)N * svt_dp_ * svt_dp_);
+  sweeps_ = dalloc<int>((size_t)(M + N));
   if (cfg.debug_sv_iter > 0) {
     if (dr != dc) throw InvalidArg("debug singular values need equal row/column d");
     d_sv_ = dr;
@@ -771,7 +776,7 @@ PiPlan::~PiPlan() {
   if (graph_) cudaGraphDestroy(graph_);
   void* bufs[] = {yk_, x_, xold_, r_, p_, ap_, bk_, tmp_, tmp2_, dg_, srow_, scol_, hrow_, hcol_,
                   hrow0_, hcol0_, drow_, dcol_, wcN_, wcM_, pmat_, twM_, twN_, sv_, partials_,
-                  ctl_, log_, x0_};
+                  ctl_, log_, x0_, vrow_, vcol_, sweeps_};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (ev0_) cudaEventDestroy(ev0_);
@@ -871,6 +876,8 @@ void PiPlan::enqueue_iteration(int k, bool record_events) {
     sp.thresh = (float)(1.0 / cfg_.beta);
     sp.max_sweeps = 20;
     sp.skip = &ctl_->stopped;
+    sp.warm = &ctl_->have_v;
+    sp.sweeps_out = sweeps_;
     for (int f = 0; f < 2; ++f) {
       SvtFamily& F = sp.fam[f];
       const bool rows = f == 0;
@@ -894,6 +901,7 @@ void PiPlan::enqueue_iteration(int k, bool record_events) {
       F.o_j = 1;
       F.wc = rows ? wcN_ : wcM_;
       F.D = rows ? drow_ : dcol_;
+      F.V = rows ? vrow_ : vcol_;
       F.sv = (sv_ && k + 1 == cfg_.debug_sv_iter) ? (rows ? sv_ : sv_ + (size_t)M * d_sv_) : nullptr;
     }
     if (record_events) SHLR_CUDA(cudaEventRecord(evA_, stream_));
@@ -903,7 +911,7 @@ void PiPlan::enqueue_iteration(int k, bool record_events) {
   }
   // ---- stop rule + log
   k_relchange<<<g, kThreads, 0, stream_>>>(x_, xold_, nel_, ctl_, partials_, log_, cfg_.tol,
-                                           cfg_.max_outer);
+                                           cfg_.max_outer, warm_start_ ? 1 : 0);
   SHLR_LAUNCH_CHECK();
   launch_count_ += 1;
 }
@@ -1020,8 +1028,34 @@ void hankel_svt_batched_device(const float2* vecs, int batch, int nc, int n, int
   F.o_mat = F.s_mat;
   F.o_n = 1;
   F.o_j = n;
-  F.sv = sv;
-  launch_hankel_svt(sp, batch, stream);
+  // cold solves need a V1 spill area: process the batch in chunks so the
+  // stream-ordered scratch stays <= 256 MB
+  const int dp = svt_padded_dim(F.d);
+  const size_t per = (size_t)dp * dp * sizeof(float2);
+  const int chunk = (int)std::max<size_t>(1, std::min<size_t>((size_t)batch, (256ull << 20) / per));
+  float2* vscr = nullptr;
+  SHLR_CUDA(cudaMallocAsync(&vscr, (size_t)chunk * per, stream));
+  for (int b0 = 0; b0 < batch; b0 += chunk) {
+    const int nb = std::min(chunk, batch - b0);
+    SvtParams spc = sp;
+    SvtFamily& Fc = spc.fam[0];
+    Fc.count = nb;
+    Fc.spec = vecs + (long long)b0 * F.s_mat;
+    Fc.out = out + (long long)b0 * F.o_mat;
+    Fc.sv = sv ? sv + (long long)b0 * F.d : nullptr;
+    Fc.V = vscr;
+    spc.sweeps_out = sweeps_out ? sweeps_out + b0 : nullptr;
+    launch_hankel_svt(spc, nb, stream);
+  }
+  SHLR_CUDA(cudaFreeAsync(vscr, stream));
+}
+
+void PiPlan::debug_sweeps(int* out, int n) {
+  const int total = cfg_.M + cfg_.N;
+  std::vector<int> h(total);
+  SHLR_CUDA(cudaMemcpyAsync(h.data(), sweeps_, total * sizeof(int), cudaMemcpyDeviceToHost, stream_));
+  SHLR_CUDA(cudaStreamSynchronize(stream_));
+  for (int i = 0; i < std::min(n, total); ++i) out[i] = h[i];
 }
 
 void fft_along_axis_host(double* data, const size_t* dims, int ndim, int axis, bool inverse) {

@@ -22,7 +22,7 @@ struct SolverCtl {
   int stopped;   // ADMM stop rule fired (solvers.cpp:187)
   int error;     // 1: non-finite residual, 2: operator not positive definite
   int outer;     // completed outer iterations
-  int pad;
+  int have_v;    // the SVT eigenvector store holds a warm start
   unsigned int arrive[8];
 };
 
@@ -53,6 +53,9 @@ class PiPlan {
   double total_ms() const { return total_ms_; }
   int launches_per_iter() const { return launches_per_iter_; }
   void set_timing(bool on) { timing_ = on; }
+  void set_warm_start(bool on) { warm_start_ = on; }
+  // per-matrix Jacobi sweeps (stage1 * 100 + stage2) of the last SVT launch
+  void debug_sweeps(int* out, int n);
   cudaStream_t stream() const { return stream_; }
   const PiConfig& config() const { return cfg_; }
 
@@ -75,6 +78,10 @@ class PiPlan {
   float2 *srow_ = nullptr, *scol_ = nullptr, *hrow_ = nullptr, *hcol_ = nullptr;
   float2 *hrow0_ = nullptr, *hcol0_ = nullptr;
   float2 *drow_ = nullptr, *dcol_ = nullptr;
+  float2 *vrow_ = nullptr, *vcol_ = nullptr;  // SVT eigenvector stores (warm start)
+  int* sweeps_ = nullptr;                     // diagnostics
+  bool warm_start_ = true;
+  int svt_dp_ = 0;
   float2 *wcN_ = nullptr, *wcM_ = nullptr;
   float2* pmat_ = nullptr;  // SPIRiT (G-I)^H(G-I) per pixel, [M][N][J][J]
   float2 *twM_ = nullptr, *twN_ = nullptr;

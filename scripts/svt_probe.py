@@ -12,7 +12,9 @@ vd = torch.from_numpy(v.astype(np.complex64)).cuda()
 out = torch.empty_like(vd)
 sw = torch.zeros(b, dtype=torch.int32, device="cuda")
 rc = lib.shlr_cuda_debug_svt_sweeps(C.c_void_p(vd.data_ptr()), b, nc, n, p, tau, C.c_void_p(out.data_ptr()), C.c_void_p(sw.data_ptr()))
-torch.cuda.synchronize(); print("rc", rc, "sweeps: min", int(sw.min()), "max", int(sw.max()), "mean", float(sw.float().mean()))
+torch.cuda.synchronize()
+s1, s2 = (sw // 100).float(), (sw % 100).float()
+print("rc", rc, "stage1 sweeps mean %.2f max %d | stage2 mean %.2f max %d" % (s1.mean(), s1.max(), s2.mean(), s2.max()))
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 for rep in range(int(os.environ.get("REPS", 3))):
     e0.record()
