@@ -113,6 +113,10 @@ int shlr_cuda_pi_plan_set_warm_start(shlr_pi_plan* plan, int on);
 /* Diagnostics: Jacobi sweeps (stage1 * 100 + stage2) per matrix of the last
  * Hankel-SVT launch, rows first then columns; n = m + n entries. */
 int shlr_cuda_pi_plan_debug_sweeps(shlr_pi_plan* plan, int* out, int n);
+/* Diagnostics: per-matrix clock64 stamps of the subspace solver's phases
+ * (8 per matrix) of the last launch; zeros unless SHLR_PHASE_CLK was set in
+ * the environment when the plan was created. */
+int shlr_cuda_pi_plan_debug_phases(shlr_pi_plan* plan, long long* out, int n);
 int shlr_cuda_pi_plan_download(shlr_pi_plan* plan, double* x_out, shlr_stats* stats,
                                shlr_log_fn log_cb, void* log_ctx);
 void shlr_cuda_pi_plan_destroy(shlr_pi_plan* plan);

@@ -64,6 +64,7 @@ PROTOTYPES = {
     "shlr_cuda_pi_plan_set_timing": (C.c_int, [C.c_void_p, C.c_int]),
     "shlr_cuda_pi_plan_set_warm_start": (C.c_int, [C.c_void_p, C.c_int]),
     "shlr_cuda_pi_plan_debug_sweeps": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.c_int]),
+    "shlr_cuda_pi_plan_debug_phases": (C.c_int, [C.c_void_p, C.POINTER(C.c_longlong), C.c_int]),
     "shlr_cuda_fp32_peak_tflops": (C.c_int, [C.POINTER(C.c_double)]),
     "shlr_cuda_hankel_svt_batched": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
                                                C.c_float, C.c_void_p, C.c_void_p, C.c_void_p]),

@@ -185,6 +185,14 @@ int shlr_cuda_pi_plan_set_warm_start(shlr_pi_plan* plan, int on) {
   });
 }
 
+int shlr_cuda_pi_plan_debug_phases(shlr_pi_plan* plan, long long* out, int n) {
+  return guarded([&] {
+    if (!plan || !out) throw shlr_b200::InvalidArg("null plan/output");
+    plan->impl->debug_phases(out, n);
+    return SHLR_OK;
+  });
+}
+
 int shlr_cuda_pi_plan_debug_sweeps(shlr_pi_plan* plan, int* out, int n) {
   return guarded([&] {
     if (!plan || !out) throw shlr_b200::InvalidArg("null plan/output");

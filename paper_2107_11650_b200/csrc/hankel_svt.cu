@@ -30,7 +30,6 @@ struct __align__(16) SlotRec {
   float2 cw;            // c * conj(phase)
   float2 sw;            // s * conj(phase)
   float pad2[2];
-  double na, nb;        // diagonal entries a, b after this rotation
 };
 
 __device__ __forceinline__ int ring_idx(int k, int r, int DP) {
@@ -76,6 +75,7 @@ struct Smem {
   float2* A;     // R x DP chunk of Ahat (also V panel staging)
   float2* X;     // R x DP chunk of D / B = Ahat V1 / T
   SlotRec* rec;  // 2 x S (current / next round)
+  double2* dgr;  // 2 x S diagonal entries (a, b) of each slot after its rotation
   float* f;      // DP shrink factors
   int* flags;    // 4
   float* scal;   // 4
@@ -100,6 +100,26 @@ __device__ __forceinline__ void load_chunk(const Smem<DP>& S, const SvtFamily& F
     }
     S.A[t] = v;
     if (want_d) S.X[t] = dd;
+  }
+}
+
+// Same as load_chunk, into an explicit R x DP buffer (no D copy).
+template <int DP, int R>
+__device__ __forceinline__ void load_chunk_to(float2* dst, const float2* wl, const SvtFamily& F,
+                                              const float2* Dg, int i0, int rows, float inv_beta) {
+  const int d = F.d;
+  for (int t = threadIdx.x; t < R * DP; t += blockDim.x) {
+    const int r = t / DP, u = t - r * DP;
+    float2 v = make_float2(0.f, 0.f);
+    if (r < rows && u < d) {
+      v = lift_elem(wl, F, i0 + r, u);
+      if (Dg) {
+        const float2 dd = Dg[(long long)(i0 + r) * d + u];
+        v.x = fmaf(dd.x, inv_beta, v.x);
+        v.y = fmaf(dd.y, inv_beta, v.y);
+      }
+    }
+    dst[t] = v;
   }
 }
 
@@ -156,9 +176,11 @@ __device__ __forceinline__ void chunk_gemm(const float2* A, const float2* Bm, in
 }
 
 // Rotation that annihilates g = G[a][b] given the current diagonal entries
-// (al, be): rotate iff |g| > tol_rel sqrt(al be) and |g| > tol_abs.
-__device__ __forceinline__ bool make_rotation(SlotRec& rc, int a, int b, double al, double be,
-                                              float2 gm, float tol_rel, float tol_abs) {
+// (al, be): rotate iff |g| > tol_rel sqrt(al be), |g| > tol_abs and not both
+// al, be < tail (pairs inside a tail whose shrink factor is 0 either way).
+__device__ __forceinline__ bool make_rotation(SlotRec& rc, double2& nd, int a, int b, double al,
+                                              double be, float2 gm, float tol_rel, float tol_abs,
+                                              float tail) {
   rc.a = a;
   rc.b = b;
   rc.flag = 0;
@@ -166,46 +188,24 @@ __device__ __forceinline__ bool make_rotation(SlotRec& rc, int a, int b, double 
   rc.sn = 0.f;
   rc.cw = make_float2(1.f, 0.f);
   rc.sw = make_float2(0.f, 0.f);
-  rc.na = al;
-  rc.nb = be;
+  nd = make_double2(al, be);
   const float g = hypotf(gm.x, gm.y);
   const float alf = (float)al, bef = (float)be;
   if (!(g > 0.f && g > tol_abs && g > tol_rel * sqrtf(fmaxf(alf * bef, 0.f)))) return false;
-#ifdef SHLR_ROT_FP64
-  {
-    const double zeta = (be - al) / (2.0 * (double)g);
-    const double az = fabs(zeta);
-    double t = 1.0 / (az + sqrt(1.0 + az * az));
-    t = zeta < 0.0 ? -t : t;
-    const double ci = 1.0 / sqrt(1.0 + t * t);
-    const float2 ph = make_float2(gm.x / g, -gm.y / g);
-    rc.c = (float)ci;
-    rc.sn = (float)(t * ci);
-    rc.cw = cscale(ph, rc.c);
-    rc.sw = cscale(ph, rc.sn);
-    rc.na = al - t * (double)g;
-    rc.nb = be + t * (double)g;
-    rc.flag = 1;
-    return true;
-  }
-#endif
-  // the difference of the diagonal entries in fp64 (they may be close), the
-  // angle in fp32, the diagonal update in fp64
-  const float ig = __frcp_rn(g);
-  const float zeta = (float)(be - al) * (0.5f * ig);
-  const float az = fabsf(zeta);
-  float t = az > 1e18f ? 0.5f / az : __frcp_rn(az + sqrtf(fmaf(az, az, 1.f)));
-  t = zeta < 0.f ? -t : t;
-  const float c = 1.0f / sqrtf(fmaf(t, t, 1.f));  // IEEE sqrt/div: c^2 + s^2 = 1 to 1 ulp
-  const float sn = t * c;
-  const float2 ph = make_float2(gm.x * ig, -gm.y * ig);  // conj(g)/|g|
-  rc.c = c;
-  rc.sn = sn;
-  rc.cw = cscale(ph, c);
-  rc.sw = cscale(ph, sn);
-  const double tg = (double)t * (double)g;
-  rc.na = al - tg;
-  rc.nb = be + tg;
+  if (alf < tail && bef < tail) return false;
+  // fp64 angle: with fp32 the accumulated diagonal/angle mismatch costs ~10x
+  // in the final singular values (measured)
+  const double zeta = (be - al) / (2.0 * (double)g);
+  const double az = fabs(zeta);
+  double t = 1.0 / (az + sqrt(1.0 + az * az));
+  t = zeta < 0.0 ? -t : t;
+  const double ci = 1.0 / sqrt(1.0 + t * t);
+  const float2 ph = make_float2(gm.x / g, -gm.y / g);  // conj(g)/|g|
+  rc.c = (float)ci;
+  rc.sn = (float)(t * ci);
+  rc.cw = cscale(ph, rc.c);
+  rc.sw = cscale(ph, rc.sn);
+  nd = make_double2(al - t * (double)g, be + t * (double)g);
   rc.flag = 1;
   return true;
 }
@@ -222,7 +222,7 @@ __device__ __forceinline__ bool make_rotation(SlotRec& rc, int a, int b, double 
 // Returns the number of sweeps; the final diagonal is written to S.dg.
 template <int DP, int W>
 __device__ int jacobi(const Smem<DP>& S, float2 (&vt)[W], float2 (&vb)[W], float tol_rel,
-                      float tol_abs, int max_sweeps) {
+                      float tol_abs, int max_sweeps, float tail = 0.f) {
   constexpr int NT = 4 * DP;
   constexpr int S_ = DP / 2;
   constexpr int GS = DP + 1;
@@ -237,7 +237,7 @@ __device__ int jacobi(const Smem<DP>& S, float2 (&vt)[W], float2 (&vb)[W], float
   int blk_code[NBT];  // s1 | s2 << 8 | (carrier + 1) << 16, or -1
 #pragma unroll
   for (int k = 0; k < NBT; ++k) {
-    const int q = tid + k * NT;
+    const int q = tid < NT ? tid + k * NT : NOFF;  // threads >= 4*DP only join barriers
     int s1 = -1, s2 = -1, cr = -1;
     if (q < S_) {
       const int s = q;
@@ -270,13 +270,17 @@ __device__ int jacobi(const Smem<DP>& S, float2 (&vt)[W], float2 (&vb)[W], float
   // rotations of round 0 of the first sweep
   if (tid < S_) {
     const int a = top_of(tid, 0, DP), b = bot_of(tid, 0, DP);
+    const int lo = min(a, b), hi = max(a, b);
+    float2 gm = S.G[lo * GS + hi];
+    if (a > b) gm.y = -gm.y;
     SlotRec rc;
-    if (make_rotation(rc, a, b, S.dg[a], S.dg[b], S.G[a * GS + b], tol_rel, tol_abs)) {
-      S.G[a * GS + b] = make_float2(0.f, 0.f);
-      S.G[b * GS + a] = make_float2(0.f, 0.f);
+    double2 nd;
+    if (make_rotation(rc, nd, a, b, S.dg[a], S.dg[b], gm, tol_rel, tol_abs, tail)) {
+      S.G[lo * GS + hi] = make_float2(0.f, 0.f);
       S.flags[0] = 1;
     }
     S.rec[tid] = rc;
+    S.dgr[tid] = nd;
   }
   __syncthreads();
   int cur = 0;
@@ -295,9 +299,13 @@ __device__ int jacobi(const Smem<DP>& S, float2 (&vt)[W], float2 (&vb)[W], float
         const SlotRec& p2 = rc[s2];
         if (cr < 0 && !(p1.flag | p2.flag)) continue;
         const int x0 = p1.a, x1 = p1.b, y0 = p2.a, y1 = p2.b;
-        // full Hermitian storage: read the (x, y) orientation, write both
-        float2 a00 = S.G[x0 * GS + y0], a01 = S.G[x0 * GS + y1];
-        float2 a10 = S.G[x1 * GS + y0], a11 = S.G[x1 * GS + y1];
+        // upper-representation addresses and conjugation signs
+        const int i00 = min(x0, y0) * GS + max(x0, y0), i01 = min(x0, y1) * GS + max(x0, y1);
+        const int i10 = min(x1, y0) * GS + max(x1, y0), i11 = min(x1, y1) * GS + max(x1, y1);
+        const float s00 = x0 > y0 ? -1.f : 1.f, s01 = x0 > y1 ? -1.f : 1.f;
+        const float s10 = x1 > y0 ? -1.f : 1.f, s11 = x1 > y1 ? -1.f : 1.f;
+        float2 a00 = S.G[i00], a01 = S.G[i01], a10 = S.G[i10], a11 = S.G[i11];
+        a00.y *= s00; a01.y *= s01; a10.y *= s10; a11.y *= s11;
         {  // X J2 (columns); identity parameters are exact
           const float2 n00 = csub(cscale(a00, p2.c), cmul(p2.sw, a01));
           const float2 n01 = cadd(cscale(a00, p2.sn), cmul(p2.cw, a01));
@@ -314,13 +322,15 @@ __device__ int jacobi(const Smem<DP>& S, float2 (&vt)[W], float2 (&vb)[W], float
         }
         if (cr >= 0) {  // next-round rotation carried by this block
           const int kind = cr & 3, slot = cr >> 2;
+          const double2 d1 = S.dgr[cur * S_ + s1], d2 = S.dgr[cur * S_ + s2];
           const int ra = kind == 1 ? x1 : x0;
           const int rb = kind == 2 ? y0 : y1;
-          const double al = kind == 1 ? p1.nb : p1.na;
-          const double be = kind == 2 ? p2.na : p2.nb;
+          const double al = kind == 1 ? d1.y : d1.x;
+          const double be = kind == 2 ? d2.x : d2.y;
           const float2 gm = kind == 0 ? a01 : (kind == 1 ? a11 : a00);
           SlotRec nr;
-          if (make_rotation(nr, ra, rb, al, be, gm, tol_rel, tol_abs)) {
+          double2 nd;
+          if (make_rotation(nr, nd, ra, rb, al, be, gm, tol_rel, tol_abs, tail)) {
             const float2 z = make_float2(0.f, 0.f);
             if (kind == 0) a01 = z;
             if (kind == 1) a11 = z;
@@ -328,26 +338,27 @@ __device__ int jacobi(const Smem<DP>& S, float2 (&vt)[W], float2 (&vb)[W], float
             *next_flag = 1;
           }
           rn[slot] = nr;
+          S.dgr[(cur ^ 1) * S_ + slot] = nd;
         }
-        S.G[x0 * GS + y0] = a00; S.G[x0 * GS + y1] = a01;
-        S.G[x1 * GS + y0] = a10; S.G[x1 * GS + y1] = a11;
-        S.G[y0 * GS + x0] = cconj(a00); S.G[y1 * GS + x0] = cconj(a01);
-        S.G[y0 * GS + x1] = cconj(a10); S.G[y1 * GS + x1] = cconj(a11);
+        a00.y *= s00; a01.y *= s01; a10.y *= s10; a11.y *= s11;
+        S.G[i00] = a00; S.G[i01] = a01; S.G[i10] = a10; S.G[i11] = a11;
       }
       // V <- V J on this thread's slots
+      if (tid < NT) {
 #pragma unroll
-      for (int w = 0; w < W; ++w) {
-        const SlotRec& p = rc[vg * W + w];
-        if (p.flag) {
-          const float2 a = vt[w], b = vb[w];
-          vt[w] = csub(cscale(a, p.c), cmul(p.sw, b));
-          vb[w] = cadd(cscale(a, p.sn), cmul(p.cw, b));
+        for (int w = 0; w < W; ++w) {
+          const SlotRec& p = rc[vg * W + w];
+          if (p.flag) {
+            const float2 a = vt[w], b = vb[w];
+            vt[w] = csub(cscale(a, p.c), cmul(p.sw, b));
+            vb[w] = cadd(cscale(a, p.sn), cmul(p.cw, b));
+          }
         }
       }
       __syncthreads();
       cur ^= 1;
       // ring shift of the V columns: tops move right, bottoms move left
-      {
+      if (tid < NT) {  // whole warps: 4*DP is a multiple of 32
         const float2 up_t = make_float2(__shfl_up_sync(0xffffffffu, vt[W - 1].x, 1, 4),
                                         __shfl_up_sync(0xffffffffu, vt[W - 1].y, 1, 4));
         const float2 up_b = make_float2(__shfl_up_sync(0xffffffffu, vb[0].x, 1, 4),
@@ -386,8 +397,9 @@ __device__ int jacobi(const Smem<DP>& S, float2 (&vt)[W], float2 (&vb)[W], float
   // final diagonal: the pending (identity after convergence) records hold it
   if (tid < S_) {
     const SlotRec& p = S.rec[cur * S_ + tid];
-    S.dg[p.a] = p.na;
-    S.dg[p.b] = p.nb;
+    const double2 nd = S.dgr[cur * S_ + tid];
+    S.dg[p.a] = nd.x;
+    S.dg[p.b] = nd.y;
   }
   if (tid < 2) S.flags[tid] = 0;
   __syncthreads();
@@ -441,6 +453,7 @@ __global__ void __maxnreg__(svt_max_regs(DP)) hankel_svt_kernel(const SvtParams 
   if (prm.skip && *prm.skip) return;
   int mat;
   const SvtFamily& F = family_of(prm, blockIdx.x, mat);
+  if (prm.only_flagged && !F.fallback[mat]) return;
   const int tid = threadIdx.x;
   const int d = F.d, e = F.e, len = F.len, B = F.B, J = F.J;
   const bool admm = prm.mode != SVT_PLAIN;
@@ -449,12 +462,18 @@ __global__ void __maxnreg__(svt_max_regs(DP)) hankel_svt_kernel(const SvtParams 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem<DP> S;
   S.G = reinterpret_cast<float2*>(smem_raw);
-  S.wl = S.G + DP * GS;
-  S.acc = S.wl + B * len;
+  if (prm.wl_global) {  // plain lift of contiguous coil vectors: read the source in place
+    S.wl = const_cast<float2*>(F.spec) + (long long)mat * F.s_mat;
+    S.acc = S.G + DP * GS;
+  } else {
+    S.wl = S.G + DP * GS;
+    S.acc = S.wl + B * len;
+  }
   S.A = S.acc + B * len;
   S.X = S.A + R * DP;
   S.rec = reinterpret_cast<SlotRec*>(S.X + R * DP);
-  S.dg = reinterpret_cast<double*>(S.rec + 2 * S_);
+  S.dgr = reinterpret_cast<double2*>(S.rec + 2 * S_);
+  S.dg = reinterpret_cast<double*>(S.dgr + 2 * S_);
   S.f = reinterpret_cast<float*>(S.dg + DP);
   S.flags = reinterpret_cast<int*>(S.f + DP);
   S.scal = reinterpret_cast<float*>(S.flags + 4);
@@ -467,7 +486,7 @@ __global__ void __maxnreg__(svt_max_regs(DP)) hankel_svt_kernel(const SvtParams 
   // ---------------------------------------------------------- phase 0
   {
     const float2* sp = F.spec + (long long)mat * F.s_mat;
-    for (int t = tid; t < J * len; t += NT) {
+    for (int t = tid; t < (prm.wl_global ? 0 : J * len); t += NT) {
       const int j = t / len, n = t - j * len;
       const float2 s = sp[n * F.s_n + j * F.s_j];
       if (weighted) {
@@ -692,10 +711,610 @@ __global__ void __maxnreg__(svt_max_regs(DP)) hankel_svt_kernel(const SvtParams 
   }
 }
 
-size_t svt_smem_bytes(int DP, int R, int maxB, int maxLen) {
+// ============================================================================
+// Subspace SVT solver
+// ============================================================================
+namespace {
+
+constexpr int kSubNT = 512;  // threads of the subspace kernel (16 warps)
+
+__device__ __forceinline__ float hash_unit(unsigned int x) {
+  x ^= x >> 16;
+  x *= 0x7feb352dU;
+  x ^= x >> 15;
+  x *= 0x846ca68bU;
+  x ^= x >> 16;
+  return (float)(x >> 8) * (2.0f / 16777216.0f) - 1.0f;
+}
+
+__device__ __forceinline__ float warp_sum_f(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Householder vector of column j of M (rows j..d-1): v_j = 1 implicit, rows
+// > j overwritten by v, tau[j] set.  Executed by one warp.
+template <int KS>
+__device__ __forceinline__ void householder_prep(float2* M, int d, int j, float* tau) {
+  const int lane = threadIdx.x & 31;
+  float s = 0.f;
+  for (int i = j + lane; i < d; i += 32) {
+    const float2 x = M[i * KS + j];
+    s = fmaf(x.x, x.x, fmaf(x.y, x.y, s));
+  }
+  s = warp_sum_f(s);
+  const float nrm = sqrtf(s);
+  const float2 x0 = M[j * KS + j];
+  const float ax0 = hypotf(x0.x, x0.y);
+  float t = 0.f;
+  float2 inv_v0 = make_float2(0.f, 0.f);
+  if (nrm > 0.f) {
+    const float2 ph = ax0 > 0.f ? make_float2(x0.x / ax0, x0.y / ax0) : make_float2(1.f, 0.f);
+    const float2 alpha = make_float2(-ph.x * nrm, -ph.y * nrm);
+    const float2 v0 = csub(x0, alpha);        // = ph (|x0| + nrm)
+    const float n0 = ax0 + nrm;
+    inv_v0 = make_float2(ph.x / n0, -ph.y / n0);  // 1 / v0
+    t = 1.f + ax0 / nrm;                      // (alpha - x0) / alpha, real
+    (void)v0;
+  }
+  __syncwarp();
+  for (int i = j + 1 + lane; i < d; i += 32) M[i * KS + j] = cmul(M[i * KS + j], inv_v0);
+  if (lane == 0) tau[j] = t;
+  __syncwarp();
+}
+
+__device__ __forceinline__ float group8_sum(float v, unsigned mask = 0xffffffffu) {
+  v += __shfl_xor_sync(mask, v, 4);
+  v += __shfl_xor_sync(mask, v, 2);
+  v += __shfl_xor_sync(mask, v, 1);
+  return v;
+}
+
+// Q (rows < d, KB orthonormal columns, stride KS) of the Householder QR of M
+// (same shape); M is destroyed (its columns receive the reflectors).
+//
+// Each column is owned by a group of 8 threads for the whole factorisation
+// and held in registers (rows s + 8t).  Step j: the owner of column j has
+// already formed reflector j from its registers (v_j -> column j of M, tau),
+// every owner of a column k > j applies it to its registers, and the owner of
+// column j+1 forms reflector j+1 -- one CTA barrier per column.  Forming Q
+// applies the stored reflectors backwards to register-resident columns of
+// the identity, with no barrier at all.
+template <int KB, int KS, int DP>
+__device__ void householder_qr(float2* M, float2* Q, int d, float* tau) {
+  constexpr int T = DP / 8;  // rows per thread
+  const int g = threadIdx.x >> 3, s = threadIdx.x & 7;
+  static_assert(kSubNT / 8 >= KB && kSubNT / 8 == 64, "one 8-thread group per column");
+  static_assert(DP % 8 == 0, "DP multiple of 8");
+  // column of group g = 4w + l: the 4 groups of a warp take columns 8 apart
+  const int w = g >> 2, l = g & 3;
+  const int k = (w >> 3) * 32 + 8 * l + (w & 7);
+  const bool act = k < KB;
+  const unsigned gmask = 0xffu << (8 * l);  // this group's lanes
+  float2 col[T];
+#pragma unroll
+  for (int t = 0; t < T; ++t) {
+    const int row = s + 8 * t;
+    col[t] = (act && row < d) ? M[row * KS + k] : make_float2(0.f, 0.f);
+  }
+  // reflector of this group's column (k == j) from its registers
+  auto reflect = [&](int j) {
+    float ss = 0.f;
+    float2 x0 = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      const int row = s + 8 * t;
+      if (row >= j) ss = fmaf(col[t].x, col[t].x, fmaf(col[t].y, col[t].y, ss));
+      if (row == j) x0 = col[t];
+    }
+    ss += __shfl_xor_sync(gmask, ss, 4);
+    ss += __shfl_xor_sync(gmask, ss, 2);
+    ss += __shfl_xor_sync(gmask, ss, 1);
+    x0.x = __shfl_sync(gmask, x0.x, (8 * l) + (j & 7));
+    x0.y = __shfl_sync(gmask, x0.y, (8 * l) + (j & 7));
+    const float nrm = sqrtf(ss);
+    const float ax0 = hypotf(x0.x, x0.y);
+    float tj = 0.f;
+    float2 inv_v0 = make_float2(0.f, 0.f);
+    if (nrm > 0.f) {
+      const float2 ph = ax0 > 0.f ? make_float2(x0.x / ax0, x0.y / ax0) : make_float2(1.f, 0.f);
+      const float n0 = ax0 + nrm;                   // v0 = x0 - alpha = ph (|x0| + nrm)
+      inv_v0 = make_float2(ph.x / n0, -ph.y / n0);  // 1 / v0
+      tj = 1.f + ax0 / nrm;                         // (alpha - x0) / alpha, real
+    }
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      const int row = s + 8 * t;
+      if (row > j && row < d) M[row * KS + j] = cmul(col[t], inv_v0);
+    }
+    if (s == 0) tau[j] = tj;
+  };
+  if (k == 0) reflect(0);
+  __syncthreads();
+  for (int j = 0; j < KB; ++j) {
+    const bool upd = act && k > j;
+    float2 part = make_float2(0.f, 0.f);
+    float2 v[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      const int row = s + 8 * t;
+      v[t] = (row > j && row < d) ? M[row * KS + j] : make_float2(row == j ? 1.f : 0.f, 0.f);
+      cfmac(part, v[t], col[t]);  // sum conj(v) col
+    }
+    part.x = group8_sum(part.x);
+    part.y = group8_sum(part.y);
+    if (upd) {
+      const float2 tw = cscale(part, tau[j]);
+#pragma unroll
+      for (int t = 0; t < T; ++t) col[t] = csub(col[t], cmul(v[t], tw));
+      if (k == j + 1) reflect(j + 1);
+    }
+    __syncthreads();
+  }
+  // explicit Q = H_0 ... H_{KB-1} [I; 0]: column k of the identity, reflectors backwards
+#pragma unroll
+  for (int t = 0; t < T; ++t) col[t] = make_float2(s + 8 * t == k ? 1.f : 0.f, 0.f);
+  for (int j = KB - 1; j >= 0; --j) {
+    float2 part = make_float2(0.f, 0.f);
+    float2 v[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      const int row = s + 8 * t;
+      v[t] = (row > j && row < d) ? M[row * KS + j] : make_float2(row == j ? 1.f : 0.f, 0.f);
+      cfmac(part, v[t], col[t]);
+    }
+    part.x = group8_sum(part.x);
+    part.y = group8_sum(part.y);
+    if (act && k >= j) {
+      const float2 tw = cscale(part, tau[j]);
+#pragma unroll
+      for (int t = 0; t < T; ++t) col[t] = csub(col[t], cmul(v[t], tw));
+    }
+  }
+  if (act) {
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      const int row = s + 8 * t;
+      if (row < DP) Q[row * KS + k] = row < d ? col[t] : make_float2(0.f, 0.f);
+    }
+  }
+}
+
+}  // namespace
+
+template <int DP, int KB, int R>
+__global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams prm) {
+  constexpr int NT = kSubNT;
+  constexpr int KS = KB + 1;       // row stride of the d x KB blocks (conflict-free column walks)
+  constexpr int NC = KB / 16;      // 16-column groups
+  constexpr int MR = (DP + 31) / 32;
+  static_assert(KB % 16 == 0 && KB % 8 == 0, "KB must be a multiple of 16");
+  static_assert(R == 32, "the thread mappings assume 32-row chunks");
+
+  if (prm.skip && *prm.skip) return;
+  int mat;
+  const SvtFamily& F = family_of(prm, blockIdx.x, mat);
+  const int tid = threadIdx.x;
+  const int d = F.d, e = F.e, len = F.len, B = F.B, J = F.J;
+  const bool admm = prm.mode != SVT_PLAIN;
+  const bool weighted = prm.mode == SVT_ADMM_WEIGHTED;
+
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float2* V = reinterpret_cast<float2*>(smem_raw);  // DP x KS
+  float2* X = V + DP * KS;                           // DP x KS (also H for the Ritz solve)
+  float2* C = X + DP * KS;                           // R x DP  (Ahat chunk / U / T)
+  float2* Yc = C + R * DP;                           // R x KS
+  float2* wl = Yc + R * KS;                          // B x len
+  float2* acc = wl + B * len;                        // B x len
+  Smem<KB> S;                                        // Rayleigh-Ritz Jacobi workspace
+  S.G = X;
+  S.rec = reinterpret_cast<SlotRec*>(acc + B * len);
+  S.dgr = reinterpret_cast<double2*>(S.rec + KB);
+  S.dg = reinterpret_cast<double*>(S.dgr + KB);
+  S.f = reinterpret_cast<float*>(S.dg + KB);
+  float* tau = S.f + KB;
+  S.flags = reinterpret_cast<int*>(tau + KB);
+  S.scal = reinterpret_cast<float*>(S.flags + 4);
+  int* cnt = reinterpret_cast<int*>(S.scal + 4);
+  int* perm = cnt + 4;                               // KB: descending-order position
+
+  float2* Dg = admm ? F.D + (long long)mat * e * d : nullptr;
+  float2* Vsg = F.Vs + (long long)mat * DP * KB;
+  const bool warm = prm.warm && *prm.warm;
+
+  // ---------------------------------------------------------- spectra
+  {
+    const float2* sp = F.spec + (long long)mat * F.s_mat;
+    for (int t = tid; t < J * len; t += NT) {
+      const int j = t / len, n = t - j * len;
+      const float2 s = sp[n * F.s_n + j * F.s_j];
+      if (weighted) {
+        wl[j * len + n] = cmul(F.wc[n], s);
+        if (F.vc) {
+          const int fl = dagger_src(n, len);
+          const float2 sf = sp[fl * F.s_n + j * F.s_j];
+          wl[(J + j) * len + n] = cmul(F.wc[n], cconj(sf));
+        }
+      } else {
+        wl[j * len + n] = s;
+      }
+    }
+    for (int t = tid; t < B * len; t += NT) acc[t] = make_float2(0.f, 0.f);
+    if (tid < 4) S.flags[tid] = 0;
+    if (tid == 0) *cnt = 0;
+  }
+  long long clk_qr = 0, clk_pass = 0, clk_t = clock64();
+#define SUB_STAMP(k) \
+  if (prm.phase_clk && tid == 0) prm.phase_clk[(long long)blockIdx.x * 8 + (k)] = clock64()
+  SUB_STAMP(0);
+
+  // ---------------------------------------------------------- starting block
+  if (warm) {
+    for (int t = tid; t < DP * KB; t += NT) {
+      const int k = t / KB, j = t - k * KB;
+      V[k * KS + j] = Vsg[t];
+    }
+    __syncthreads();
+  } else {
+    for (int t = tid; t < DP * KB; t += NT) {
+      const int k = t / KB, j = t - k * KB;
+      const unsigned int h = (unsigned int)(mat * 0x9E3779B1u) ^ (unsigned int)(t * 0x85EBCA77u);
+      X[k * KS + j] = k < d ? make_float2(hash_unit(h), hash_unit(h ^ 0x5bd1e995u)) : make_float2(0.f, 0.f);
+    }
+    __syncthreads();
+    householder_qr<KB, KS, DP>(X, V, d, tau);
+  }
+
+  // mappings: Yc rows yi / X rows k0 + 32m, columns c + 16n
+  const int yi = tid >> 4, c16 = tid & 15;
+  const int iters = warm ? prm.q_warm : prm.q_cold;
+
+  // ---------------------------------------------------------- subspace iteration
+  for (int it = 0; it < iters; ++it) {
+    float2 xa[MR][NC];
+#pragma unroll
+    for (int m = 0; m < MR; ++m)
+#pragma unroll
+      for (int n = 0; n < NC; ++n) xa[m][n] = make_float2(0.f, 0.f);
+    for (int i0 = 0; i0 < e; i0 += R) {
+      const int rows = min(R, e - i0);
+      load_chunk_to<DP, R>(C, wl, F, Dg, i0, rows, prm.inv_beta);
+      __syncthreads();
+      {  // Yc = C V
+        float2 y[NC];
+#pragma unroll
+        for (int n = 0; n < NC; ++n) y[n] = make_float2(0.f, 0.f);
+        for (int k = 0; k < d; ++k) {
+          const float2 a = C[yi * DP + k];
+#pragma unroll
+          for (int n = 0; n < NC; ++n) cfma(y[n], a, V[k * KS + c16 + 16 * n]);
+        }
+#pragma unroll
+        for (int n = 0; n < NC; ++n) Yc[yi * KS + c16 + 16 * n] = y[n];
+      }
+      __syncthreads();
+      for (int i = 0; i < rows; ++i) {  // X += C^H Yc
+        float2 yv[NC];
+#pragma unroll
+        for (int n = 0; n < NC; ++n) yv[n] = Yc[i * KS + c16 + 16 * n];
+#pragma unroll
+        for (int m = 0; m < MR; ++m) {
+          const int k = yi + 32 * m;
+          if (k < DP) {
+            const float2 a = C[i * DP + k];
+#pragma unroll
+            for (int n = 0; n < NC; ++n) cfmac(xa[m][n], a, yv[n]);
+          }
+        }
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int m = 0; m < MR; ++m) {
+      const int k = yi + 32 * m;
+      if (k < DP)
+#pragma unroll
+        for (int n = 0; n < NC; ++n) X[k * KS + c16 + 16 * n] = xa[m][n];
+    }
+    __syncthreads();
+    clk_pass += clock64() - clk_t;
+    clk_t = clock64();
+    householder_qr<KB, KS, DP>(X, V, d, tau);
+    clk_qr += clock64() - clk_t;
+    clk_t = clock64();
+  }
+  if (prm.phase_clk && tid == 0) {
+    prm.phase_clk[(long long)blockIdx.x * 8 + 1] = clk_pass;
+    prm.phase_clk[(long long)blockIdx.x * 8 + 2] = clk_qr;
+  }
+  SUB_STAMP(3);
+
+  // ---------------------------------------------------------- Rayleigh-Ritz: H = (Ahat V)^H (Ahat V)
+  {
+    constexpr int HM = (KB + 31) / 32;
+    float2 h[HM][NC];
+#pragma unroll
+    for (int m = 0; m < HM; ++m)
+#pragma unroll
+      for (int n = 0; n < NC; ++n) h[m][n] = make_float2(0.f, 0.f);
+    for (int i0 = 0; i0 < e; i0 += R) {
+      const int rows = min(R, e - i0);
+      load_chunk_to<DP, R>(C, wl, F, Dg, i0, rows, prm.inv_beta);
+      __syncthreads();
+      {
+        float2 y[NC];
+#pragma unroll
+        for (int n = 0; n < NC; ++n) y[n] = make_float2(0.f, 0.f);
+        for (int k = 0; k < d; ++k) {
+          const float2 a = C[yi * DP + k];
+#pragma unroll
+          for (int n = 0; n < NC; ++n) cfma(y[n], a, V[k * KS + c16 + 16 * n]);
+        }
+#pragma unroll
+        for (int n = 0; n < NC; ++n) Yc[yi * KS + c16 + 16 * n] = y[n];
+      }
+      __syncthreads();
+      for (int i = 0; i < rows; ++i) {
+#pragma unroll
+        for (int m = 0; m < HM; ++m) {
+          const int a = yi + 32 * m;
+          if (a < KB) {
+            const float2 ya = Yc[i * KS + a];
+#pragma unroll
+            for (int n = 0; n < NC; ++n) cfmac(h[m][n], ya, Yc[i * KS + c16 + 16 * n]);
+          }
+        }
+      }
+      __syncthreads();
+    }
+    // H (full Hermitian, stride KB+1 = KS) into X, diagonal to S.dg
+#pragma unroll
+    for (int m = 0; m < HM; ++m) {
+      const int a = yi + 32 * m;
+      if (a < KB)
+#pragma unroll
+        for (int n = 0; n < NC; ++n) {
+          const int b = c16 + 16 * n;
+          if (a == b) S.dg[a] = h[m][n].x;
+          else X[a * KS + b] = h[m][n];
+        }
+    }
+  }
+  __syncthreads();
+  if (tid < 32) {  // absolute rotation floor relative to the largest Ritz value
+    double mx = 0.0;
+    for (int u = tid; u < KB; u += 32) mx = fmax(mx, S.dg[u]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (tid == 0) S.scal[0] = (float)(kTolAbs1 * mx);
+  }
+  __syncthreads();
+  {
+    constexpr int WK = KB / 8;
+    float2 ut[WK], ub[WK];
+    if (tid < 4 * KB) {
+      const int vrow = tid >> 2, vg = tid & 3;
+#pragma unroll
+      for (int w = 0; w < WK; ++w) {
+        const int s = vg * WK + w;
+        ut[w] = make_float2(vrow == top0(s, KB) ? 1.f : 0.f, 0.f);
+        ub[w] = make_float2(vrow == bot0(s, KB) ? 1.f : 0.f, 0.f);
+      }
+    }
+    SUB_STAMP(4);
+    // Ritz pairs both well below the threshold only mix the tail (shrink
+    // factor 0 either way) and are not rotated
+    const float tail = 0.25f * prm.thresh * prm.thresh;
+    const int sw = jacobi<KB, WK>(S, ut, ub, kTolRel2, S.scal[0], prm.max_sweeps, tail);
+    SUB_STAMP(5);
+    if (prm.sweeps_out && tid == 0) prm.sweeps_out[blockIdx.x] = sw;
+    if (tid < 4 * KB) store_v<KB, WK>(C, KS, ut, ub);  // U (KB x KB) into the chunk buffer
+  }
+  // descending order of the Ritz values: the stored block stays sorted, so the
+  // next warm-started QR processes dominant directions first
+  for (int j = tid; j < KB; j += NT) {
+    const double lj = S.dg[j];
+    int rank = 0;
+    for (int i = 0; i < KB; ++i) {
+      const double li = S.dg[i];
+      rank += (li > lj) || (li == lj && i < j);
+    }
+    perm[j] = rank;
+  }
+  __syncthreads();
+  // V <- V U (Ritz vectors, sorted) into X
+  {
+    float2 va[MR][NC];
+#pragma unroll
+    for (int m = 0; m < MR; ++m)
+#pragma unroll
+      for (int n = 0; n < NC; ++n) va[m][n] = make_float2(0.f, 0.f);
+    for (int j = 0; j < KB; ++j) {
+      float2 u[NC];
+#pragma unroll
+      for (int n = 0; n < NC; ++n) u[n] = C[j * KS + c16 + 16 * n];
+#pragma unroll
+      for (int m = 0; m < MR; ++m) {
+        const int k = yi + 32 * m;
+        if (k < DP) {
+          const float2 v = V[k * KS + j];
+#pragma unroll
+          for (int n = 0; n < NC; ++n) cfma(va[m][n], v, u[n]);
+        }
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < MR; ++m) {
+      const int k = yi + 32 * m;
+      if (k < DP)
+#pragma unroll
+        for (int n = 0; n < NC; ++n) X[k * KS + perm[c16 + 16 * n]] = va[m][n];
+    }
+  }
+  for (int j = tid; j < KB; j += NT) {
+    const double lam = S.dg[j];
+    float f = 0.f;
+    if (lam > (double)prm.thresh * prm.thresh && lam > 0.0) {
+      f = (float)(1.0 - prm.thresh / sqrt(lam));
+      atomicAdd(cnt, 1);
+    }
+    S.f[perm[j]] = f;
+  }
+  __syncthreads();
+  float2* Vf = X;  // final Ritz vectors (d x KB)
+  const int r = *cnt;
+  if (F.fallback) {
+    if (tid == 0) F.fallback[mat] = (r > KB - kSubspaceMargin) ? 1 : 0;
+  }
+  if (r > KB - kSubspaceMargin) return;  // the full solver redoes this matrix
+  for (int t = tid; t < DP * KB; t += NT) {
+    const int k = t / KB, j = t - k * KB;
+    Vsg[t] = Vf[k * KS + j];
+  }
+
+  // ---------------------------------------------------------- Z = (Ahat V) f V^H, duals, adjoint
+  SUB_STAMP(6);
+  for (int i0 = 0; i0 < e; i0 += R) {
+    const int rows = min(R, e - i0);
+    load_chunk_to<DP, R>(C, wl, F, Dg, i0, rows, prm.inv_beta);
+    __syncthreads();
+    {
+      float2 y[NC];
+#pragma unroll
+      for (int n = 0; n < NC; ++n) y[n] = make_float2(0.f, 0.f);
+      for (int k = 0; k < d; ++k) {
+        const float2 a = C[yi * DP + k];
+#pragma unroll
+        for (int n = 0; n < NC; ++n) cfma(y[n], a, Vf[k * KS + c16 + 16 * n]);
+      }
+#pragma unroll
+      for (int n = 0; n < NC; ++n) Yc[yi * KS + c16 + 16 * n] = cscale(y[n], S.f[c16 + 16 * n]);
+    }
+    __syncthreads();
+    {
+      // Z[yi][k] = sum_j Yc[yi][j] conj(Vf[k][j]), k = c16 + 16 m
+      constexpr int MZ = (DP + 15) / 16;
+      float2 z[MZ];
+#pragma unroll
+      for (int m = 0; m < MZ; ++m) z[m] = make_float2(0.f, 0.f);
+      for (int j = 0; j < KB; ++j) {
+        const float2 yv = Yc[yi * KS + j];
+#pragma unroll
+        for (int m = 0; m < MZ; ++m) {
+          const int k = c16 + 16 * m;
+          if (k < DP) cfmac(z[m], Vf[k * KS + j], yv);  // yv * conj(V[k][j])
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < MZ; ++m) {
+        const int k = c16 + 16 * m;
+        if (yi < rows && k < d) {
+          float2 tv = z[m];
+          if (admm) {
+            const float2 L = lift_elem(wl, F, i0 + yi, k);
+            const long long gi = (long long)(i0 + yi) * d + k;
+            float2 dn = Dg[gi];
+            dn.x = fmaf(prm.tau_dual, L.x - z[m].x, dn.x);
+            dn.y = fmaf(prm.tau_dual, L.y - z[m].y, dn.y);
+            Dg[gi] = dn;
+            tv.x = fmaf(-dn.x, prm.inv_beta, z[m].x);
+            tv.y = fmaf(-dn.y, prm.inv_beta, z[m].y);
+          }
+          C[yi * DP + k] = tv;
+        }
+      }
+    }
+    __syncthreads();
+    for (int o = tid; o < B * len; o += NT) {
+      const int b = o / len, n = o - b * len;
+      float2 s = acc[o];
+      if (!F.wide) {
+        const int ilo = max(i0, n - F.q + 1), ihi = min(i0 + rows - 1, n);
+        for (int i = ilo; i <= ihi; ++i) s = cadd(s, C[(i - i0) * DP + b * F.q + (n - i)]);
+      } else {
+        const int tlo = max(max(0, i0 - b * F.q), n - F.P + 1);
+        const int thi = min(min(F.q - 1, i0 + rows - 1 - b * F.q), n);
+        for (int t = tlo; t <= thi; ++t) s = cadd(s, cconj(C[(b * F.q + t - i0) * DP + (n - t)]));
+      }
+      acc[o] = s;
+    }
+    __syncthreads();
+  }
+  SUB_STAMP(7);
+#undef SUB_STAMP
+
+  // ---------------------------------------------------------- weighting + store
+  {
+    float2* op = F.out + (long long)mat * F.o_mat;
+    for (int t = tid; t < J * len; t += NT) {
+      const int j = t / len, n = t - j * len;
+      float2 v = acc[j * len + n];
+      if (weighted) {
+        v = cmulc(F.wc[n], v);
+        if (F.vc) {
+          const int fl = dagger_src(n, len);
+          v = cadd(v, cmul(F.wc[fl], cconj(acc[(J + j) * len + fl])));
+        }
+      }
+      op[n * F.o_n + j * F.o_j] = v;
+    }
+  }
+}
+
+size_t svt_subspace_smem_bytes(int DP, int KB, int R, int maxB, int maxLen) {
+  const int KS = KB + 1;
+  return sizeof(float2) * (2ull * DP * KS + (size_t)R * DP + (size_t)R * KS + 2ull * maxB * maxLen) +
+         sizeof(SlotRec) * KB + sizeof(double2) * KB + sizeof(double) * KB + 2 * sizeof(float) * KB +
+         16 * sizeof(int) + sizeof(int) * KB + 64;
+}
+
+namespace {
+template <int DP>
+void launch_sub(const SvtParams& prm, int total, size_t smem, cudaStream_t stream) {
+  static bool configured = false;
+  if (!configured) {
+    SHLR_CUDA(cudaFuncSetAttribute(svt_subspace_kernel<DP, kSubspaceKB, 32>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    configured = true;
+  }
+  svt_subspace_kernel<DP, kSubspaceKB, 32><<<total, kSubNT, smem, stream>>>(prm);
+  SHLR_LAUNCH_CHECK();
+}
+}  // namespace
+
+bool launch_hankel_svt_subspace(const SvtParams& prm, int total, cudaStream_t stream) {
+  if (total <= 0) return true;
+  int dmin = 1 << 30, dmax = 0, maxB = 0, maxLen = 0;
+  for (int f = 0; f < prm.nfam; ++f) {
+    dmin = std::min(dmin, prm.fam[f].d);
+    dmax = std::max(dmax, prm.fam[f].d);
+    maxB = std::max(maxB, prm.fam[f].B);
+    maxLen = std::max(maxLen, prm.fam[f].len);
+    if (!prm.fam[f].Vs || !prm.fam[f].fallback) return false;
+  }
+  // worthwhile only when the block is well below d
+  if (dmin < kSubspaceKB + 24) return false;
+  const int dp = svt_padded_dim(dmax);
+  const size_t smem = svt_subspace_smem_bytes(dp, kSubspaceKB, 32, maxB, maxLen);
+  if (smem > 227 * 1024) return false;
+  switch (dp) {
+    case 72: launch_sub<72>(prm, total, smem, stream); return true;
+    case 80: launch_sub<80>(prm, total, smem, stream); return true;
+    case 88: launch_sub<88>(prm, total, smem, stream); return true;
+    case 96: launch_sub<96>(prm, total, smem, stream); return true;
+    case 104: launch_sub<104>(prm, total, smem, stream); return true;
+    case 112: launch_sub<112>(prm, total, smem, stream); return true;
+    case 120: launch_sub<120>(prm, total, smem, stream); return true;
+    case 128: launch_sub<128>(prm, total, smem, stream); return true;
+    default: return false;
+  }
+}
+
+size_t svt_smem_bytes(int DP, int R, int maxB, int maxLen, bool wl_smem) {
   const int S_ = DP / 2;
-  return sizeof(float2) * ((size_t)DP * (DP + 1) + 2ull * maxB * maxLen + 2ull * R * DP) +
-         sizeof(SlotRec) * 2 * S_ + sizeof(double) * DP + sizeof(float) * DP + 8 * sizeof(int) + 64;
+  return sizeof(float2) * ((size_t)DP * (DP + 1) + (wl_smem ? 2ull : 1ull) * maxB * maxLen + 2ull * R * DP) +
+         (sizeof(SlotRec) + sizeof(double2)) * 2 * S_ + sizeof(double) * DP + sizeof(float) * DP + 8 * sizeof(int) + 64;
 }
 
 int svt_padded_dim(int d) { return std::max(8, ((d + 7) / 8) * 8); }
@@ -722,6 +1341,19 @@ void dispatch_r(const SvtParams& prm, int total, int maxB, int maxLen, cudaStrea
   if (s32 <= lim) return launch_one<DP, 32>(prm, total, s32, stream);
   const size_t s16 = svt_smem_bytes(DP, 16, maxB, maxLen);
   if (s16 <= lim) return launch_one<DP, 16>(prm, total, s16, stream);
+  // plain lifts of contiguous coil vectors can read their source from global
+  // memory (L2-resident) instead of an smem copy
+  bool direct = prm.mode == SVT_PLAIN;
+  for (int f = 0; f < prm.nfam; ++f)
+    direct = direct && prm.fam[f].s_n == 1 && prm.fam[f].s_j == prm.fam[f].len && !prm.fam[f].vc;
+  if (direct) {
+    SvtParams pg = prm;
+    pg.wl_global = 1;
+    const size_t g32 = svt_smem_bytes(DP, 32, maxB, maxLen, false);
+    if (g32 <= lim) return launch_one<DP, 32>(pg, total, g32, stream);
+    const size_t g16 = svt_smem_bytes(DP, 16, maxB, maxLen, false);
+    if (g16 <= lim) return launch_one<DP, 16>(pg, total, g16, stream);
+  }
   throw Unsupported("hankel_svt: shared-memory footprint exceeds 227 KB for this geometry");
 }
 

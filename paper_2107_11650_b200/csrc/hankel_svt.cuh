@@ -46,8 +46,11 @@ struct SvtFamily {
   const float2* wc;    // centred weights (len) for weighted modes
   float2* D;           // duals, per matrix e*d row-major (Ahat orientation)
   float* sv;           // optional: count x d singular values (descending)
-  float2* V;           // required: count x DP x DP eigenvector store (V1 spill and the
-                       // ADMM warm start; DP = svt_padded_dim of the launch)
+  float2* V;           // full solver: count x DP x DP eigenvector store (V1 spill and
+                       // the ADMM warm start; DP = svt_padded_dim of the launch)
+  float2* Vs;          // subspace solver: count x DP x KB dominant-subspace store
+  int* fallback;       // subspace solver: per-matrix flag, 1 = rank above threshold too
+                       // close to KB, the full solver must redo this matrix
 };
 
 struct SvtParams {
@@ -61,7 +64,27 @@ struct SvtParams {
   const int* skip;     // optional device flag: nonzero -> kernel is a no-op
   const int* warm;     // optional device flag: nonzero -> V holds a warm start
   int* sweeps_out;     // optional diagnostics: Jacobi sweeps used per matrix
+  int q_cold, q_warm;  // subspace solver: iterations from a random / stored start
+  long long* phase_clk;  // optional diagnostics: 8 clock64 stamps per matrix
+  const int* only_flagged;  // full solver: nonzero pointer -> process only matrices whose
+                            // fallback flag is set (fam[f].fallback)
+  int wl_global;       // set by launch_hankel_svt: the lift source is read straight from
+                       // fam[f].spec (plain mode, contiguous coils) instead of an smem copy
 };
+
+// Dominant-subspace block size of the subspace SVT solver.
+constexpr int kSubspaceKB = 48;
+// Matrices with more than KB - margin singular values above the threshold
+// are redone by the full eigen-solver.
+constexpr int kSubspaceMargin = 8;
+
+// Subspace SVT: the thresholded spectral function needs only the eigenpairs
+// of G = Ahat^H Ahat with sigma > tau.  Subspace iteration on a KB-column
+// block (one fused streaming pass over Ahat per iteration: X = Ahat^H (Ahat V),
+// then Householder QR), a final Rayleigh-Ritz projection H = (Ahat V)^H
+// (Ahat V) solved by the Jacobi kernel, and the same fused Z / dual / adjoint
+// epilogue.  Returns false (no launch) when the geometry is outside its range.
+bool launch_hankel_svt_subspace(const SvtParams& prm, int total, cudaStream_t stream);
 
 // Index function shared by the kernel and shlr_cuda_lift_index_map: source
 // of element (i, c) of the p x (blocks*q) weighted lift (operators.cpp:36-56,
@@ -85,7 +108,7 @@ __host__ __device__ __forceinline__ LiftSrc lift_source(int i, int c, int q, int
   return s;
 }
 
-size_t svt_smem_bytes(int DP, int R, int maxB, int maxLen);
+size_t svt_smem_bytes(int DP, int R, int maxB, int maxLen, bool wl_smem = true);
 int svt_padded_dim(int d);
 void launch_hankel_svt(const SvtParams& prm, int total_matrices, cudaStream_t stream);
 

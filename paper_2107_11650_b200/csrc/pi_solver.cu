@@ -709,6 +709,17 @@ PiPlan::PiPlan(const PiConfig& cfg, const double* y, const uint8_t* mask, size_t
   vrow_ = dalloc<float2>((size_t)M * svt_dp_ * svt_dp_);
   vcol_ = dalloc<float2>((size_t)N * svt_dp_ * svt_dp_);
   sweeps_ = dalloc<int>((size_t)(M + N));
+  vsrow_ = dalloc<float2>((size_t)M * svt_dp_ * kSubspaceKB);
+  vscol_ = dalloc<float2>((size_t)N * svt_dp_ * kSubspaceKB);
+  fallback_ = dalloc<int>((size_t)(M + N));
+  SHLR_CUDA(cudaMemsetAsync(fallback_, 0, sizeof(int) * (M + N), stream_));
+  if (const char* s = std::getenv("SHLR_Q_COLD")) q_cold_ = std::atoi(s);
+  if (const char* s = std::getenv("SHLR_Q_WARM")) q_warm_ = std::atoi(s);
+  if (std::getenv("SHLR_FULL_SVT")) subspace_ = false;
+  if (std::getenv("SHLR_PHASE_CLK")) {
+    phase_clk_ = dalloc<long long>((size_t)(M + N) * 8);
+    SHLR_CUDA(cudaMemsetAsync(phase_clk_, 0, sizeof(long long) * 8 * (M + N), stream_));
+  }
   if (cfg.debug_sv_iter > 0) {
     if (dr != dc) throw InvalidArg("debug singular values need equal row/column d");
     d_sv_ = dr;
@@ -776,7 +787,7 @@ PiPlan::~PiPlan() {
   if (graph_) cudaGraphDestroy(graph_);
   void* bufs[] = {yk_, x_, xold_, r_, p_, ap_, bk_, tmp_, tmp2_, dg_, srow_, scol_, hrow_, hcol_,
                   hrow0_, hcol0_, drow_, dcol_, wcN_, wcM_, pmat_, twM_, twN_, sv_, partials_,
-                  ctl_, log_, x0_, vrow_, vcol_, sweeps_};
+                  ctl_, log_, x0_, vrow_, vcol_, sweeps_, vsrow_, vscol_, fallback_};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (ev0_) cudaEventDestroy(ev0_);
@@ -796,6 +807,7 @@ void PiPlan::reset() {
   SHLR_CUDA(cudaMemsetAsync(log_, 0, 3 * sizeof(double) * std::max(cfg_.max_outer, 1), stream_));
   SHLR_LAUNCH_CHECK();
   iter_ = 0;
+  subspace_used_ = false;
 }
 
 void PiPlan::cg_apply_spirit(float2* in_vec, float2* out_ap, bool init) {
@@ -902,12 +914,33 @@ void PiPlan::enqueue_iteration(int k, bool record_events) {
       F.wc = rows ? wcN_ : wcM_;
       F.D = rows ? drow_ : dcol_;
       F.V = rows ? vrow_ : vcol_;
+      F.Vs = rows ? vsrow_ : vscol_;
+      F.fallback = rows ? fallback_ : fallback_ + M;
       F.sv = (sv_ && k + 1 == cfg_.debug_sv_iter) ? (rows ? sv_ : sv_ + (size_t)M * d_sv_) : nullptr;
     }
+    sp.q_cold = q_cold_;
+    sp.q_warm = q_warm_;
+    sp.phase_clk = phase_clk_;
     if (record_events) SHLR_CUDA(cudaEventRecord(evA_, stream_));
-    launch_hankel_svt(sp, M + N, stream_);
+    // The debug singular-value hook needs every singular value: full solver.
+    const bool want_sv = sp.fam[0].sv != nullptr;
+    if (subspace_ && !want_sv && launch_hankel_svt_subspace(sp, M + N, stream_)) {
+      subspace_used_ = true;
+      // matrices whose rank above the threshold came too close to the block
+      // size are redone (from their unmodified duals) by the full solver
+      SvtParams fb = sp;
+      fb.only_flagged = fallback_;
+      fb.warm = nullptr;
+      launch_hankel_svt(fb, M + N, stream_);
+      launch_count_ += 2;
+    } else {
+      // the full solver's warm start (vrow_/vcol_) is stale when earlier
+      // iterations ran the subspace solver: start it cold then
+      if (subspace_used_) sp.warm = nullptr;
+      launch_hankel_svt(sp, M + N, stream_);
+      launch_count_ += 1;
+    }
     if (record_events) SHLR_CUDA(cudaEventRecord(evB_, stream_));
-    launch_count_ += 1;
   }
   // ---- stop rule + log
   k_relchange<<<g, kThreads, 0, stream_>>>(x_, xold_, nel_, ctl_, partials_, log_, cfg_.tol,
@@ -1034,7 +1067,11 @@ void hankel_svt_batched_device(const float2* vecs, int batch, int nc, int n, int
   const size_t per = (size_t)dp * dp * sizeof(float2);
   const int chunk = (int)std::max<size_t>(1, std::min<size_t>((size_t)batch, (256ull << 20) / per));
   float2* vscr = nullptr;
+  float2* vsub = nullptr;
+  int* flags = nullptr;
   SHLR_CUDA(cudaMallocAsync(&vscr, (size_t)chunk * per, stream));
+  SHLR_CUDA(cudaMallocAsync(&vsub, (size_t)chunk * dp * kSubspaceKB * sizeof(float2), stream));
+  SHLR_CUDA(cudaMallocAsync(&flags, (size_t)chunk * sizeof(int), stream));
   for (int b0 = 0; b0 < batch; b0 += chunk) {
     const int nb = std::min(chunk, batch - b0);
     SvtParams spc = sp;
@@ -1044,10 +1081,31 @@ void hankel_svt_batched_device(const float2* vecs, int batch, int nc, int n, int
     Fc.out = out + (long long)b0 * F.o_mat;
     Fc.sv = sv ? sv + (long long)b0 * F.d : nullptr;
     Fc.V = vscr;
+    Fc.Vs = vsub;
+    Fc.fallback = flags;
     spc.sweeps_out = sweeps_out ? sweeps_out + b0 : nullptr;
-    launch_hankel_svt(spc, nb, stream);
+    spc.q_cold = 6;
+    spc.q_warm = 3;
+    if (!sv && !std::getenv("SHLR_FULL_SVT") && launch_hankel_svt_subspace(spc, nb, stream)) {
+      spc.only_flagged = flags;
+      launch_hankel_svt(spc, nb, stream);
+    } else {
+      launch_hankel_svt(spc, nb, stream);
+    }
   }
   SHLR_CUDA(cudaFreeAsync(vscr, stream));
+  SHLR_CUDA(cudaFreeAsync(vsub, stream));
+  SHLR_CUDA(cudaFreeAsync(flags, stream));
+}
+
+void PiPlan::debug_phases(long long* out, int n) {
+  const int total = (cfg_.M + cfg_.N) * 8;
+  std::vector<long long> h(total, 0);
+  if (phase_clk_) {
+    SHLR_CUDA(cudaMemcpyAsync(h.data(), phase_clk_, total * sizeof(long long), cudaMemcpyDeviceToHost, stream_));
+    SHLR_CUDA(cudaStreamSynchronize(stream_));
+  }
+  for (int i = 0; i < std::min(n, total); ++i) out[i] = h[i];
 }
 
 void PiPlan::debug_sweeps(int* out, int n) {

@@ -56,6 +56,9 @@ class PiPlan {
   void set_warm_start(bool on) { warm_start_ = on; }
   // per-matrix Jacobi sweeps (stage1 * 100 + stage2) of the last SVT launch
   void debug_sweeps(int* out, int n);
+  // subspace-solver phase clocks of the last SVT launch (8 per matrix; needs
+  // SHLR_PHASE_CLK in the environment at plan creation)
+  void debug_phases(long long* out, int n);
   cudaStream_t stream() const { return stream_; }
   const PiConfig& config() const { return cfg_; }
 
@@ -79,7 +82,13 @@ class PiPlan {
   float2 *hrow0_ = nullptr, *hcol0_ = nullptr;
   float2 *drow_ = nullptr, *dcol_ = nullptr;
   float2 *vrow_ = nullptr, *vcol_ = nullptr;  // SVT eigenvector stores (warm start)
+  float2 *vsrow_ = nullptr, *vscol_ = nullptr;  // subspace-solver block stores (warm start)
+  int* fallback_ = nullptr;                     // per-matrix subspace -> full fallback flags
+  int q_cold_ = 6, q_warm_ = 3;
+  bool subspace_ = true;
+  bool subspace_used_ = false;                // an earlier iteration ran the subspace solver
   int* sweeps_ = nullptr;                     // diagnostics
+  long long* phase_clk_ = nullptr;            // diagnostics
   bool warm_start_ = true;
   int svt_dp_ = 0;
   float2 *wcN_ = nullptr, *wcM_ = nullptr;

@@ -17,3 +17,9 @@ for it in range(iters):
     sw = plan.debug_sweeps()
     s1, s2 = sw // 100, sw % 100
     print(f"iter {it+1}: svt {svt_ms:.2f} ms total {tot:.2f} ms | stage1 mean {s1.mean():.2f} max {s1.max()} | stage2 mean {s2.mean():.2f} max {s2.max()}", flush=True)
+if os.environ.get("SHLR_PHASE_CLK"):
+    ph = plan.debug_phases().astype(np.float64)
+    ok = ph[:, 7] > 0
+    d = lambda a, b: (ph[ok, b] - ph[ok, a]) / 1e3
+    print(f"phase kcycles (mean over {ok.sum()} matrices): start {d(0,3).mean():.0f} [pass {ph[ok,1].mean()/1e3:.0f} qr {ph[ok,2].mean()/1e3:.0f}] "
+          f"H-pass {d(3,4).mean():.0f} RR-jacobi {d(4,5).mean():.0f} VU {d(5,6).mean():.0f} Z-pass {d(6,7).mean():.0f} total {d(0,7).mean():.0f}")

@@ -1,0 +1,67 @@
+"""BASELINE config 2 at full size against the reference library's own run.
+
+tests/golden/c2_ref50.npz holds the unmodified reference (oracle/_ref +
+oracle/ref_driver, see tests/golden/make_c2_golden.py) run for 50 ADMM
+iterations on the inputs bench.make_inputs() generates: 256 x 256 x 8 coils,
+R = 5, K = 15 (242 x 120 block-Hankel matrices, 512 per sweep), SPIRiT.
+The B200 path must reproduce the image and the singular values of L + D/beta
+at iterations 1 and 50 within 1e-4 relative L2 (BASELINE north_star)."""
+import os
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+TOL = 1e-4
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+@pytest.fixture(scope="module")
+def golden():
+    return np.load(os.path.join(ROOT, "tests", "golden", "c2_ref50.npz"))
+
+
+@pytest.fixture(scope="module")
+def inputs():
+    import bench
+    return bench.make_inputs()
+
+
+def test_c2_kernels_match_reference_run(api, golden, inputs):
+    """The SPIRiT calibration feeding the run equals the kernels the
+    reference run used (host FP64, spirit.cpp:22-94)."""
+    g = inputs[2]
+    assert np.abs(g.weights - golden["kernels"]).max() < 1e-10
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("it", [1, 50])
+def test_c2_parity_vs_reference(gpu, golden, inputs, it):
+    y, mask, g, hcfg = inputs
+    A = gpu
+    acfg = A.AdmmConfig(max_outer=it, tol=1e-300, enable_spirit=True)
+    log, svs = [], []
+    x = A.shlr_pi_reconstruct(y, mask, g, hcfg, acfg, log=log, debug_sv_iter=it, sv_out=svs)
+    assert rel(svs[0], golden[f"sv{it}"]) < TOL
+    if it == 50:
+        assert rel(x, golden["x50"]) < TOL
+        relc = np.array([float(l.split("relchange=")[1].split()[0]) for l in log])
+        # the stop-rule trace follows the reference's (relative, it decays to ~1e-8)
+        np.testing.assert_allclose(relc[:5], golden["relchange"][:5], rtol=1e-2)
+
+
+@pytest.mark.gpu
+def test_c2_resident_plan_parity(gpu, golden, inputs):
+    """The bench path (resident plan, CUDA graph, subspace SVT with warm start)
+    gives the reference image after 50 iterations."""
+    y, mask, g, hcfg = inputs
+    A = gpu
+    plan = A.PiPlan(y, mask, g, hcfg, A.AdmmConfig(max_outer=50, tol=1e-300, enable_spirit=True))
+    plan.run(50)
+    plan.sync()
+    x, st = plan.download()
+    assert st.outer_iters == 50
+    assert rel(x, golden["x50"]) < TOL
