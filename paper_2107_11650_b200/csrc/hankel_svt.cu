@@ -22,7 +22,9 @@ namespace {
 // rotate iff |g_ab| > tol_rel sqrt(g_aa g_bb) and |g_ab| > tol_abs max_u g_uu.
 constexpr float kTolRel1 = 1.0e-5f;
 constexpr float kTolAbs1 = 1.0e-7f;
+constexpr float kTolAbsRR = 1.0e-6f;  // Rayleigh-Ritz absolute floor (x max Ritz value)
 constexpr float kTolRel2 = 2.0e-6f;
+constexpr int kRitzMaxSweeps = 8;  // Rayleigh-Ritz Jacobi sweep cap (subspace solver)
 
 struct __align__(16) SlotRec {
   int a, b, flag, pad;  // storage indices of the pair, 1 = non-identity rotation
@@ -772,33 +774,32 @@ __device__ __forceinline__ float group8_sum(float v, unsigned mask = 0xffffffffu
 }
 
 // Q (rows < d, KB orthonormal columns, stride KS) of the Householder QR of M
-// (same shape); M is destroyed (its columns receive the reflectors).
+// (DP x KB, rows >= d zero); M is destroyed: column j receives the full
+// reflector v_j (0 above row j, 1 at row j), so the apply loops carry no
+// per-row predicates.
 //
 // Each column is owned by a group of 8 threads for the whole factorisation
-// and held in registers (rows s + 8t).  Step j: the owner of column j has
-// already formed reflector j from its registers (v_j -> column j of M, tau),
-// every owner of a column k > j applies it to its registers, and the owner of
-// column j+1 forms reflector j+1 -- one CTA barrier per column.  Forming Q
-// applies the stored reflectors backwards to register-resident columns of
-// the identity, with no barrier at all.
+// and held in registers (rows s + 8t); warp w owns columns 4w..4w+3, so warps
+// whose columns are finished (or do not exist) skip a step as a whole.  Step
+// j: every owner of a column k > j applies reflector j; the warp owning
+// column j+1 then forms reflector j+1 from its registers -- one CTA barrier
+// per column.  Forming Q applies the stored reflectors backwards to
+// register-resident columns of the identity, with no barrier at all.
 template <int KB, int KS, int DP>
 __device__ void householder_qr(float2* M, float2* Q, int d, float* tau) {
   constexpr int T = DP / 8;  // rows per thread
   const int g = threadIdx.x >> 3, s = threadIdx.x & 7;
-  static_assert(kSubNT / 8 >= KB && kSubNT / 8 == 64, "one 8-thread group per column");
+  static_assert(kSubNT / 8 >= KB, "one 8-thread group per column");
   static_assert(DP % 8 == 0, "DP multiple of 8");
-  // column of group g = 4w + l: the 4 groups of a warp take columns 8 apart
-  const int w = g >> 2, l = g & 3;
-  const int k = (w >> 3) * 32 + 8 * l + (w & 7);
+  const int w = g >> 2;
+  const int k = g;                 // this group's column
   const bool act = k < KB;
-  const unsigned gmask = 0xffu << (8 * l);  // this group's lanes
+  const bool warp_act = 4 * w < KB;
   float2 col[T];
 #pragma unroll
-  for (int t = 0; t < T; ++t) {
-    const int row = s + 8 * t;
-    col[t] = (act && row < d) ? M[row * KS + k] : make_float2(0.f, 0.f);
-  }
-  // reflector of this group's column (k == j) from its registers
+  for (int t = 0; t < T; ++t) col[t] = act ? M[(s + 8 * t) * KS + k] : make_float2(0.f, 0.f);
+  // executed by a whole warp (full-mask shuffles); the group owning column j
+  // stores reflector j
   auto reflect = [&](int j) {
     float ss = 0.f;
     float2 x0 = make_float2(0.f, 0.f);
@@ -808,75 +809,79 @@ __device__ void householder_qr(float2* M, float2* Q, int d, float* tau) {
       if (row >= j) ss = fmaf(col[t].x, col[t].x, fmaf(col[t].y, col[t].y, ss));
       if (row == j) x0 = col[t];
     }
-    ss += __shfl_xor_sync(gmask, ss, 4);
-    ss += __shfl_xor_sync(gmask, ss, 2);
-    ss += __shfl_xor_sync(gmask, ss, 1);
-    x0.x = __shfl_sync(gmask, x0.x, (8 * l) + (j & 7));
-    x0.y = __shfl_sync(gmask, x0.y, (8 * l) + (j & 7));
+    ss = group8_sum(ss);
+    x0.x = group8_sum(x0.x);  // one lane of the group holds row j
+    x0.y = group8_sum(x0.y);
     const float nrm = sqrtf(ss);
-    const float ax0 = hypotf(x0.x, x0.y);
+    const float ax0 = sqrtf(fmaf(x0.x, x0.x, x0.y * x0.y));
     float tj = 0.f;
     float2 inv_v0 = make_float2(0.f, 0.f);
     if (nrm > 0.f) {
       const float2 ph = ax0 > 0.f ? make_float2(x0.x / ax0, x0.y / ax0) : make_float2(1.f, 0.f);
-      const float n0 = ax0 + nrm;                   // v0 = x0 - alpha = ph (|x0| + nrm)
-      inv_v0 = make_float2(ph.x / n0, -ph.y / n0);  // 1 / v0
-      tj = 1.f + ax0 / nrm;                         // (alpha - x0) / alpha, real
+      const float rn0 = 1.f / (ax0 + nrm);          // v0 = x0 - alpha = ph (|x0| + nrm)
+      inv_v0 = make_float2(ph.x * rn0, -ph.y * rn0);  // 1 / v0
+      tj = 1.f + ax0 / nrm;                           // (alpha - x0) / alpha, real
     }
+    if (k == j) {
 #pragma unroll
-    for (int t = 0; t < T; ++t) {
-      const int row = s + 8 * t;
-      if (row > j && row < d) M[row * KS + j] = cmul(col[t], inv_v0);
+      for (int t = 0; t < T; ++t) {
+        const int row = s + 8 * t;
+        M[row * KS + j] = row > j ? cmul(col[t], inv_v0) : make_float2(row == j ? 1.f : 0.f, 0.f);
+      }
+      if (s == 0) tau[j] = tj;
     }
-    if (s == 0) tau[j] = tj;
   };
-  if (k == 0) reflect(0);
+  if (w == 0) reflect(0);
   __syncthreads();
   for (int j = 0; j < KB; ++j) {
-    const bool upd = act && k > j;
-    float2 part = make_float2(0.f, 0.f);
-    float2 v[T];
+    if (warp_act && 4 * w + 3 > j) {  // warp-uniform: some column k > j in this warp
+      float2 part = make_float2(0.f, 0.f);
+      float2 v[T];
 #pragma unroll
-    for (int t = 0; t < T; ++t) {
-      const int row = s + 8 * t;
-      v[t] = (row > j && row < d) ? M[row * KS + j] : make_float2(row == j ? 1.f : 0.f, 0.f);
-      cfmac(part, v[t], col[t]);  // sum conj(v) col
-    }
-    part.x = group8_sum(part.x);
-    part.y = group8_sum(part.y);
-    if (upd) {
-      const float2 tw = cscale(part, tau[j]);
+      for (int t = 0; t < T; ++t) {
+        v[t] = M[(s + 8 * t) * KS + j];
+        cfmac(part, v[t], col[t]);  // sum conj(v) col
+      }
+      part.x = group8_sum(part.x);
+      part.y = group8_sum(part.y);
+      const float2 tw = (act && k > j) ? cscale(part, tau[j]) : make_float2(0.f, 0.f);
 #pragma unroll
-      for (int t = 0; t < T; ++t) col[t] = csub(col[t], cmul(v[t], tw));
-      if (k == j + 1) reflect(j + 1);
+      for (int t = 0; t < T; ++t) {
+        col[t].x -= v[t].x * tw.x - v[t].y * tw.y;
+        col[t].y -= v[t].x * tw.y + v[t].y * tw.x;
+      }
+      if (j + 1 < KB && w == ((j + 1) >> 2)) reflect(j + 1);
     }
     __syncthreads();
   }
-  // explicit Q = H_0 ... H_{KB-1} [I; 0]: column k of the identity, reflectors backwards
+  // explicit Q = H_0 ... H_{KB-1} [I; 0]: column k of the identity, reflectors
+  // backwards (H_j leaves e_k alone for j > k)
 #pragma unroll
   for (int t = 0; t < T; ++t) col[t] = make_float2(s + 8 * t == k ? 1.f : 0.f, 0.f);
-  for (int j = KB - 1; j >= 0; --j) {
-    float2 part = make_float2(0.f, 0.f);
-    float2 v[T];
+  if (warp_act) {
+    for (int j = min(4 * w + 3, KB - 1); j >= 0; --j) {
+      float2 part = make_float2(0.f, 0.f);
+      float2 v[T];
 #pragma unroll
-    for (int t = 0; t < T; ++t) {
-      const int row = s + 8 * t;
-      v[t] = (row > j && row < d) ? M[row * KS + j] : make_float2(row == j ? 1.f : 0.f, 0.f);
-      cfmac(part, v[t], col[t]);
-    }
-    part.x = group8_sum(part.x);
-    part.y = group8_sum(part.y);
-    if (act && k >= j) {
-      const float2 tw = cscale(part, tau[j]);
+      for (int t = 0; t < T; ++t) {
+        v[t] = M[(s + 8 * t) * KS + j];
+        cfmac(part, v[t], col[t]);
+      }
+      part.x = group8_sum(part.x);
+      part.y = group8_sum(part.y);
+      const float2 tw = (act && k >= j) ? cscale(part, tau[j]) : make_float2(0.f, 0.f);
 #pragma unroll
-      for (int t = 0; t < T; ++t) col[t] = csub(col[t], cmul(v[t], tw));
+      for (int t = 0; t < T; ++t) {
+        col[t].x -= v[t].x * tw.x - v[t].y * tw.y;
+        col[t].y -= v[t].x * tw.y + v[t].y * tw.x;
+      }
     }
   }
   if (act) {
 #pragma unroll
     for (int t = 0; t < T; ++t) {
       const int row = s + 8 * t;
-      if (row < DP) Q[row * KS + k] = row < d ? col[t] : make_float2(0.f, 0.f);
+      Q[row * KS + k] = row < d ? col[t] : make_float2(0.f, 0.f);
     }
   }
 }
@@ -1087,7 +1092,7 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
     for (int u = tid; u < KB; u += 32) mx = fmax(mx, S.dg[u]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if (tid == 0) S.scal[0] = (float)(kTolAbs1 * mx);
+    if (tid == 0) S.scal[0] = (float)((prm.rr_tol_abs > 0.f ? prm.rr_tol_abs : kTolAbsRR) * mx);
   }
   __syncthreads();
   {
@@ -1105,8 +1110,11 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
     SUB_STAMP(4);
     // Ritz pairs both well below the threshold only mix the tail (shrink
     // factor 0 either way) and are not rotated
-    const float tail = 0.25f * prm.thresh * prm.thresh;
-    const int sw = jacobi<KB, WK>(S, ut, ub, kTolRel2, S.scal[0], prm.max_sweeps, tail);
+    // (a pair straddling the boundary can keep re-coupling through the
+    // unrotated tail: the sweep cap bounds that; such vectors have f ~ 0)
+    const float tail = prm.rr_tail * prm.thresh * prm.thresh;
+    const int sw = jacobi<KB, WK>(S, ut, ub, prm.rr_tol_rel > 0.f ? prm.rr_tol_rel : kTolRel2, S.scal[0],
+                                 min(prm.max_sweeps, kRitzMaxSweeps), tail);
     SUB_STAMP(5);
     if (prm.sweeps_out && tid == 0) prm.sweeps_out[blockIdx.x] = sw;
     if (tid < 4 * KB) store_v<KB, WK>(C, KS, ut, ub);  // U (KB x KB) into the chunk buffer

@@ -68,6 +68,8 @@ struct SvtParams {
   long long* phase_clk;  // optional diagnostics: 8 clock64 stamps per matrix
   const int* only_flagged;  // full solver: nonzero pointer -> process only matrices whose
                             // fallback flag is set (fam[f].fallback)
+  float rr_tol_rel, rr_tol_abs;  // subspace Rayleigh-Ritz rotation tolerances (0 = defaults)
+  float rr_tail;                 // pairs with both Ritz values < rr_tail * thresh^2 not rotated
   int wl_global;       // set by launch_hankel_svt: the lift source is read straight from
                        // fam[f].spec (plain mode, contiguous coils) instead of an smem copy
 };

@@ -716,6 +716,9 @@ PiPlan::PiPlan(const PiConfig& cfg, const double* y, const uint8_t* mask, size_t
   if (const char* s = std::getenv("SHLR_Q_COLD")) q_cold_ = std::atoi(s);
   if (const char* s = std::getenv("SHLR_Q_WARM")) q_warm_ = std::atoi(s);
   if (std::getenv("SHLR_FULL_SVT")) subspace_ = false;
+  if (const char* s = std::getenv("SHLR_RR_REL")) rr_tol_rel_ = (float)std::atof(s);
+  if (const char* s = std::getenv("SHLR_RR_ABS")) rr_tol_abs_ = (float)std::atof(s);
+  if (const char* s = std::getenv("SHLR_RR_TAIL")) rr_tail_ = (float)std::atof(s);
   if (std::getenv("SHLR_PHASE_CLK")) {
     phase_clk_ = dalloc<long long>((size_t)(M + N) * 8);
     SHLR_CUDA(cudaMemsetAsync(phase_clk_, 0, sizeof(long long) * 8 * (M + N), stream_));
@@ -920,6 +923,9 @@ void PiPlan::enqueue_iteration(int k, bool record_events) {
     }
     sp.q_cold = q_cold_;
     sp.q_warm = q_warm_;
+    sp.rr_tol_rel = rr_tol_rel_;
+    sp.rr_tol_abs = rr_tol_abs_;
+    sp.rr_tail = rr_tail_;
     sp.phase_clk = phase_clk_;
     if (record_events) SHLR_CUDA(cudaEventRecord(evA_, stream_));
     // The debug singular-value hook needs every singular value: full solver.

@@ -16,6 +16,8 @@ for it in range(iters):
     svt_ms, tot, _ = plan.timing()
     sw = plan.debug_sweeps()
     s1, s2 = sw // 100, sw % 100
+    hist = np.bincount(sw % 100, minlength=21)[:21]
+    print("   sweep histogram:", " ".join(f"{i}:{c}" for i, c in enumerate(hist) if c))
     print(f"iter {it+1}: svt {svt_ms:.2f} ms total {tot:.2f} ms | stage1 mean {s1.mean():.2f} max {s1.max()} | stage2 mean {s2.mean():.2f} max {s2.max()}", flush=True)
 if os.environ.get("SHLR_PHASE_CLK"):
     ph = plan.debug_phases().astype(np.float64)
