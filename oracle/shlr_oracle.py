@@ -13,7 +13,8 @@ follows (paths relative to ``/root/reference/proj``).  The restatement is
     ``tests/test_fft.cpp``, ``tests/test_sampling.cpp``, ``tests/test_solvers.cpp``),
     restated in ``tests/test_oracle_pins.py``;
   * against the reference itself, compiled unmodified into ``oracle/_ref`` (see
-    ``oracle/Makefile``), on identical inputs (``tests/test_oracle_vs_ref.py``).
+    ``oracle/Makefile``), through golden vectors it produced on seeded inputs
+    (``tests/golden/*.npz``, checked in ``tests/test_golden.py``).
 
 Arrays are complex128 numpy arrays with the reference's layouts: an M x N x J
 tensor is ``x[m, n, j]`` (row-major, coil fastest; ``tensor.hpp:16-119``).
