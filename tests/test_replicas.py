@@ -1,0 +1,61 @@
+"""Multi-GPU is "replicas only".  These tests check the
+host logic with world_size 2 over gloo on CPU: the rendezvous bench.py uses,
+max-over-ranks timing, and that the whole-job value is ranks x steps / max
+time."""
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(RANK=str(rank), WORLD_SIZE=str(world), LOCAL_RANK=str(rank),
+                      MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    sys.path.insert(0, ROOT)
+    import bench
+    dist, r, w, local = bench.dist_setup()
+    assert (r, w, local) == (rank, world, rank)
+    assert dist.get_backend() == "gloo"
+    bench.barrier(dist)
+    t = bench.max_over_ranks(dist, 10.0 * (rank + 1))   # rank 1 is the slow one
+    value = w * 5 / (t * 1e-3)                           # 5 steps per rank
+    dist.destroy_process_group()
+    q.put((rank, t, value))
+
+
+def test_max_over_ranks_and_whole_job_value():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    res = sorted(q.get(timeout=10) for _ in range(2))
+    assert [t for _, t, _ in res] == [20.0, 20.0]       # every rank sees the max
+    assert res[0][2] == pytest.approx(2 * 5 / 0.020)
+
+
+def test_gpu_arm_fails_loudly_without_device():
+    """No CPU fallback: on a host without a CUDA device the GPU arm exits
+    non-zero instead of timing anything else."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "1", "--warmup", "1",
+                        "--no-e2e", "--no-cpu"], capture_output=True, text=True, timeout=300)
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("host has a GPU")
+    assert r.returncode != 0
+    assert "no CUDA device" in (r.stderr + r.stdout)
