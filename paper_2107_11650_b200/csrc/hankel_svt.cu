@@ -10,6 +10,7 @@
 // outer iteration (kept in HBM), so a warm launch skips the Gram and stage 1.
 // The Gram diagonal is carried in FP64 (it is updated once per round).
 #include <algorithm>
+#include <type_traits>
 #include <string>
 
 #include "hankel_svt.cuh"
@@ -886,6 +887,371 @@ __device__ void householder_qr(float2* M, float2* Q, int d, float* tau) {
   }
 }
 
+// Eigen-decomposition of the n x n Hermitian Rayleigh-Ritz matrix H (full
+// storage in smem, stride KS, destroyed) for the subspace solver:
+//   1. Householder tridiagonalisation H = Q T Q^H (one reflector per column,
+//      3 CTA barriers per column; reflectors kept in H's columns);
+//   2. a diagonal phase similarity makes T real symmetric tridiagonal;
+//   3. eigenvalues by multisection on Sturm counts, 8 threads per eigenvalue
+//      (9 sub-intervals per step, 10 steps: below FP32 resolution);
+//   4. eigenvectors of T by the twisted factorisation (one thread per
+//      eigenvalue); members of clusters above `care` rebuilt by inverse
+//      iteration with reorthogonalisation; modified Gram-Schmidt in
+//      descending order;
+//   5. back-transform through the phases and the stored reflectors, one
+//      8-thread group per eigenvector held in registers (no barriers).
+// Out: evals[k] descending, U[i * KS + k] the matching unit eigenvectors.
+// scr: >= 12 n floats; work: >= 3 n n floats, may alias U (dead before U is
+// written).  Runs on kSubNT threads; ~ (3 n + 60) barriers in total.
+template <int n, int KS>
+__device__ void hermitian_eig_tridiag(float2* H, float* scr, float* work, float2* U, double* evals,
+                                      float care = 0.f, long long* clk = nullptr) {
+#define EIG_STAMP(k) \
+  if (clk && threadIdx.x == 0) clk[k] = clock64()
+  EIG_STAMP(0);
+  static_assert(n % 8 == 0 && n <= 64, "n must be a multiple of 8, <= 64");
+  constexpr int NT = kSubNT;
+  constexpr int CU = n / 8;  // columns (rows) per thread in the 8-thread-group mappings
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  float2* vbuf = reinterpret_cast<float2*>(scr);  // n: current reflector
+  float2* pbuf = vbuf + n;                         // n: p = tau A v
+  float2* ph = pbuf + n;                           // n: phases of the real similarity
+  float2* ee = ph + n;                             // n: complex subdiagonal of T
+  float* dd = reinterpret_cast<float*>(ee + n);    // n: diagonal of T
+  float* bb = dd + n;                              // n: |subdiagonal|
+  float* b2 = bb + n;                              // n: |subdiagonal|^2
+  float* th = b2 + n;                              // n: reflector tau
+
+  // ---------------------------------------------------------- 1. tridiagonalise
+  const int gi = tid >> 3, gs = tid & 7;  // row-group mapping: row j+1+gi, columns j+1+gs+8u
+  for (int j = 0; j < n - 2; ++j) {
+    if (warp == 0) {
+      const int i0 = j + 1 + lane, i1 = i0 + 32;
+      const float2 xa = i0 < n ? H[i0 * KS + j] : make_float2(0.f, 0.f);
+      const float2 xb = i1 < n ? H[i1 * KS + j] : make_float2(0.f, 0.f);
+      float ss = fmaf(xa.x, xa.x, fmaf(xa.y, xa.y, fmaf(xb.x, xb.x, xb.y * xb.y)));
+      ss = warp_sum_f(ss);
+      const float2 x0 = make_float2(__shfl_sync(0xffffffffu, xa.x, 0), __shfl_sync(0xffffffffu, xa.y, 0));
+      const float nrm = sqrtf(ss);
+      const float ax0 = sqrtf(fmaf(x0.x, x0.x, x0.y * x0.y));
+      float tj = 0.f;
+      float2 alpha = make_float2(0.f, 0.f), inv_v0 = make_float2(0.f, 0.f);
+      if (nrm > 0.f) {
+        const float2 phs = ax0 > 0.f ? make_float2(x0.x / ax0, x0.y / ax0) : make_float2(1.f, 0.f);
+        alpha = make_float2(-phs.x * nrm, -phs.y * nrm);
+        const float rn0 = 1.f / (ax0 + nrm);
+        inv_v0 = make_float2(phs.x * rn0, -phs.y * rn0);
+        tj = 1.f + ax0 / nrm;
+      }
+      if (i0 < n) {
+        const float2 v = i0 == j + 1 ? make_float2(1.f, 0.f) : cmul(xa, inv_v0);
+        vbuf[i0] = v;
+        H[i0 * KS + j] = v;
+      }
+      if (i1 < n) {
+        const float2 v = cmul(xb, inv_v0);
+        vbuf[i1] = v;
+        H[i1 * KS + j] = v;
+      }
+      if (lane == 0) {
+        th[j] = tj;
+        ee[j] = alpha;
+      }
+    }
+    __syncthreads();
+    const float tj = th[j];
+    {  // p = tau A v, A = H[j+1:, j+1:]
+      const int i = j + 1 + gi;
+      float2 part = make_float2(0.f, 0.f);
+      if (i < n) {
+#pragma unroll
+        for (int u = 0; u < CU; ++u) {
+          const int c = j + 1 + gs + 8 * u;
+          if (c < n) cfma(part, H[i * KS + c], vbuf[c]);
+        }
+      }
+      part.x = group8_sum(part.x);
+      part.y = group8_sum(part.y);
+      if (i < n && gs == 0) pbuf[i] = cscale(part, tj);
+    }
+    __syncthreads();
+    float kk;  // K = (tau / 2) v^H p (real for Hermitian A)
+    {
+      float t = 0.f;
+      for (int i = j + 1 + lane; i < n; i += 32) {
+        const float2 v = vbuf[i], pv = pbuf[i];
+        t = fmaf(v.x, pv.x, fmaf(v.y, pv.y, t));
+      }
+      kk = 0.5f * tj * warp_sum_f(t);
+    }
+    {  // A -= v w^H + w v^H, w = p - K v
+      const int i = j + 1 + gi;
+      if (i < n) {
+        const float2 vi = vbuf[i];
+        const float2 wi = csub(pbuf[i], cscale(vi, kk));
+#pragma unroll
+        for (int u = 0; u < CU; ++u) {
+          const int c = j + 1 + gs + 8 * u;
+          if (c < n) {
+            const float2 vc = vbuf[c];
+            const float2 wc = csub(pbuf[c], cscale(vc, kk));
+            float2 a = H[i * KS + c];
+            // a -= vi conj(wc) + wi conj(vc)
+            a.x -= vi.x * wc.x + vi.y * wc.y + wi.x * vc.x + wi.y * vc.y;
+            a.y -= vi.y * wc.x - vi.x * wc.y + wi.y * vc.x - wi.x * vc.y;
+            H[i * KS + c] = a;
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (tid < n) dd[tid] = H[tid * KS + tid].x;
+  if (tid == 0) ee[n - 2] = H[(n - 1) * KS + (n - 2)];
+  __syncthreads();
+  // reflector columns j <= n-3: zero above row j+1 (row j+1 already holds 1)
+  for (int t = tid; t < n * n; t += NT) {
+    const int i = t / n, c = t - i * n;
+    if (c <= n - 3 && i <= c) H[i * KS + c] = make_float2(0.f, 0.f);
+  }
+  EIG_STAMP(1);
+  // ---------------------------------------------------------- 2. real similarity
+  if (tid == 0) {
+    float2 p = make_float2(1.f, 0.f);
+    ph[0] = p;
+    for (int j = 0; j < n - 1; ++j) {
+      const float2 e = ee[j];
+      const float a = sqrtf(fmaf(e.x, e.x, e.y * e.y));
+      bb[j] = a;
+      b2[j] = a * a;
+      if (a > 0.f) p = cmul(p, make_float2(e.x / a, e.y / a));
+      ph[j + 1] = p;
+    }
+    bb[n - 1] = 0.f;
+    b2[n - 1] = 0.f;
+  }
+  __syncthreads();
+  EIG_STAMP(2);
+  // ---------------------------------------------------------- 3. eigenvalues (multisection)
+  float maxb2 = 0.f;
+  for (int i = 0; i < n - 1; ++i) maxb2 = fmaxf(maxb2, b2[i]);
+  const float pivmin = 1.0e-30f * fmaxf(1.f, maxb2);
+  {
+    const int g = gi, s = gs, l = g & 3;
+    const bool act = g < n;
+    float lo = 3.0e38f, hi = -3.0e38f;
+    for (int i = s; i < n; i += 8) {
+      const float r = (i > 0 ? bb[i - 1] : 0.f) + bb[i];
+      lo = fminf(lo, dd[i] - r);
+      hi = fmaxf(hi, dd[i] + r);
+    }
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+      lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    const float pad = 1e-6f * fmaxf(fabsf(lo), fabsf(hi)) + pivmin;
+    lo -= pad;
+    hi += pad;
+    const int mrank = n - 1 - g;  // ascending index of the g-th largest eigenvalue
+    for (int it = 0; it < 10; ++it) {
+      const float h = (hi - lo) * (1.f / 9.f);
+      const float x = lo + (float)(s + 1) * h;
+      int c = 0;
+      if (act) {
+        float q = dd[0] - x;
+        if (fabsf(q) < pivmin) q = -pivmin;
+        c = q < 0.f;
+#pragma unroll 8
+        for (int i = 1; i < n; ++i) {
+          q = (dd[i] - x) - __fdividef(b2[i - 1], q);
+          if (fabsf(q) < pivmin) q = -pivmin;
+          c += q < 0.f;
+        }
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, act && c > mrank);
+      const unsigned gb = (bal >> (8 * l)) & 0xffu;
+      if (gb) {
+        const int f = __ffs(gb) - 1;
+        const float nhi = lo + (float)(f + 1) * h;
+        lo = f > 0 ? lo + (float)f * h : lo;
+        hi = nhi;
+      } else {
+        lo = lo + 8.f * h;
+      }
+    }
+    if (act && s == 0) evals[g] = 0.5 * ((double)lo + (double)hi);
+  }
+  __syncthreads();
+  EIG_STAMP(3);
+  // ---------------------------------------------------------- 4. eigenvectors of T (twisted)
+  float* Dp = work;
+  float* Dm = work + n * n;
+  float* Y = work + 2 * n * n;  // [i * n + k]
+  if (tid < n) {
+    const int k = tid;
+    const float lam = (float)evals[k];
+    float q = dd[0] - lam;
+    if (fabsf(q) < pivmin) q = -pivmin;
+    Dp[k] = q;
+    for (int i = 1; i < n; ++i) {
+      q = (dd[i] - lam) - b2[i - 1] / q;
+      if (fabsf(q) < pivmin) q = -pivmin;
+      Dp[i * n + k] = q;
+    }
+    q = dd[n - 1] - lam;
+    if (fabsf(q) < pivmin) q = -pivmin;
+    Dm[(n - 1) * n + k] = q;
+    for (int i = n - 2; i >= 0; --i) {
+      q = (dd[i] - lam) - b2[i] / q;
+      if (fabsf(q) < pivmin) q = -pivmin;
+      Dm[i * n + k] = q;
+    }
+    int r = 0;
+    float best = 3.0e38f;
+    for (int i = 0; i < n; ++i) {
+      const float gm = fabsf(Dp[i * n + k] + Dm[i * n + k] - (dd[i] - lam));
+      if (gm < best) {
+        best = gm;
+        r = i;
+      }
+    }
+    float z = 1.f, nrm2 = 1.f;
+    Y[r * n + k] = 1.f;
+    for (int i = r - 1; i >= 0; --i) {
+      z = -(bb[i] / Dp[i * n + k]) * z;
+      Y[i * n + k] = z;
+      nrm2 = fmaf(z, z, nrm2);
+    }
+    z = 1.f;
+    for (int i = r + 1; i < n; ++i) {
+      z = -(bb[i - 1] / Dm[i * n + k]) * z;
+      Y[i * n + k] = z;
+      nrm2 = fmaf(z, z, nrm2);
+    }
+    const float inv = rsqrtf(nrm2);
+    for (int i = 0; i < n; ++i) Y[i * n + k] *= inv;
+  }
+  __syncthreads();
+  // clusters (gap < 1e-5 of the spectral radius): the twisted vectors
+  // of the members nearly coincide; rebuild members 2.. by inverse iteration
+  // (T - lam_k) x = y with reorthogonalisation against the earlier members
+  // (LAPACK stein-style), one thread, sequential -- clusters are rare.
+  if (tid == 0) {
+    const float tnorm = fmaxf(fabsf((float)evals[0]), fabsf((float)evals[n - 1]));
+    const float ctol = 1e-5f * tnorm, dfloor = 1e-7f * tnorm + pivmin;
+    int cs = 0;
+    for (int k = 1; k < n; ++k) {
+      if ((float)(evals[k - 1] - evals[k]) > ctol) {
+        cs = k;
+        continue;
+      }
+      // clusters below `care` (shrink factor 0) keep their MGS-orthonormalised
+      // twisted vectors: any orthonormal basis of that tail will do
+      if ((float)evals[cs] < care) continue;
+      const float lam = (float)evals[k];
+      for (int it = 0; it < 3; ++it) {
+        // orthogonalise the current iterate against members cs..k-1 and normalise
+        for (int p = cs; p < k; ++p) {
+          float dt = 0.f;
+          for (int i = 0; i < n; ++i) dt = fmaf(Y[i * n + p], Y[i * n + k], dt);
+          for (int i = 0; i < n; ++i) Y[i * n + k] = fmaf(-dt, Y[i * n + p], Y[i * n + k]);
+        }
+        float nn = 0.f;
+        for (int i = 0; i < n; ++i) nn = fmaf(Y[i * n + k], Y[i * n + k], nn);
+        if (!(nn > 1e-30f)) {  // fully dependent: restart from a fixed pseudo-random vector
+          for (int i = 0; i < n; ++i) Y[i * n + k] = hash_unit(0x9E3779B9u * (unsigned)(i + 1) + (unsigned)k);
+          continue;
+        }
+        const float inn = rsqrtf(nn);
+        for (int i = 0; i < n; ++i) Y[i * n + k] *= inn;
+        if (it == 2) break;
+        // one inverse-iteration step with the stored L D L^T of T - lam (D floored)
+        float w = Y[k];
+        auto dfl = [&](float dv) { return fabsf(dv) < dfloor ? copysignf(dfloor, dv) : dv; };
+        for (int i = 1; i < n; ++i) {
+          const float wi = Y[i * n + k] - (bb[i - 1] / dfl(Dp[(i - 1) * n + k])) * w;
+          Y[(i - 1) * n + k] = w / dfl(Dp[(i - 1) * n + k]);
+          w = wi;
+        }
+        float x = w / dfl(Dp[(n - 1) * n + k]);
+        Y[(n - 1) * n + k] = x;
+        for (int i = n - 2; i >= 0; --i) {
+          x = Y[i * n + k] - (bb[i] / dfl(Dp[i * n + k])) * x;
+          Y[i * n + k] = x;
+        }
+        float mx = 0.f;  // keep the iterate in range before reorthogonalising
+        for (int i = 0; i < n; ++i) mx = fmaxf(mx, fabsf(Y[i * n + k]));
+        if (mx > 0.f)
+          for (int i = 0; i < n; ++i) Y[i * n + k] /= mx;
+      }
+    }
+  }
+  __syncthreads();
+  EIG_STAMP(4);
+  // ---------------------------------------------------------- 5. MGS, phases, back-transform
+  {
+    const int g = gi, s = gs;
+    const bool act = g < n;
+    float y[CU];
+#pragma unroll
+    for (int t = 0; t < CU; ++t) y[t] = act ? Y[(s + 8 * t) * n + g] : 0.f;
+    for (int k = 0; k < n; ++k) {
+      float ss = 0.f;
+#pragma unroll
+      for (int t = 0; t < CU; ++t) ss = fmaf(y[t], y[t], ss);
+      ss = group8_sum(ss);
+      if (g == k) {
+        const float inv = rsqrtf(ss);
+#pragma unroll
+        for (int t = 0; t < CU; ++t) {
+          y[t] *= inv;
+          Y[(s + 8 * t) * n + k] = y[t];
+        }
+      }
+      __syncthreads();
+      float dot = 0.f;
+      float yk[CU];
+#pragma unroll
+      for (int t = 0; t < CU; ++t) {
+        yk[t] = Y[(s + 8 * t) * n + k];
+        dot = fmaf(y[t], yk[t], dot);
+      }
+      dot = group8_sum(dot);
+      if (act && g > k) {
+#pragma unroll
+        for (int t = 0; t < CU; ++t) y[t] = fmaf(-dot, yk[t], y[t]);
+      }
+    }
+    EIG_STAMP(5);
+    float2 u[CU];
+#pragma unroll
+    for (int t = 0; t < CU; ++t) u[t] = cscale(ph[s + 8 * t], y[t]);
+    for (int j = n - 3; j >= 0; --j) {
+      float2 part = make_float2(0.f, 0.f);
+      float2 v[CU];
+#pragma unroll
+      for (int t = 0; t < CU; ++t) {
+        v[t] = H[(s + 8 * t) * KS + j];
+        cfmac(part, v[t], u[t]);
+      }
+      part.x = group8_sum(part.x);
+      part.y = group8_sum(part.y);
+      const float2 tw = cscale(part, th[j]);
+#pragma unroll
+      for (int t = 0; t < CU; ++t) u[t] = csub(u[t], cmul(v[t], tw));
+    }
+    __syncthreads();  // Y / Dp / Dm (aliasing U) are dead
+    if (act) {
+#pragma unroll
+      for (int t = 0; t < CU; ++t) U[(s + 8 * t) * KS + g] = u[t];
+    }
+  }
+  __syncthreads();
+  EIG_STAMP(6);
+#undef EIG_STAMP
+}
+
 }  // namespace
 
 template <int DP, int KB, int R>
@@ -1082,11 +1448,18 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
         for (int n = 0; n < NC; ++n) {
           const int b = c16 + 16 * n;
           if (a == b) S.dg[a] = h[m][n].x;
-          else X[a * KS + b] = h[m][n];
+          X[a * KS + b] = h[m][n];
         }
     }
   }
   __syncthreads();
+  if (!prm.rr_jacobi) {
+    SUB_STAMP(4);
+    hermitian_eig_tridiag<KB, KS>(X, reinterpret_cast<float*>(S.rec), reinterpret_cast<float*>(C), C, S.dg,
+                                  0.25f * prm.thresh * prm.thresh);
+    SUB_STAMP(5);
+    if (prm.sweeps_out && tid == 0) prm.sweeps_out[blockIdx.x] = 0;
+  } else {
   if (tid < 32) {  // absolute rotation floor relative to the largest Ritz value
     double mx = 0.0;
     for (int u = tid; u < KB; u += 32) mx = fmax(mx, S.dg[u]);
@@ -1118,6 +1491,8 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
     SUB_STAMP(5);
     if (prm.sweeps_out && tid == 0) prm.sweeps_out[blockIdx.x] = sw;
     if (tid < 4 * KB) store_v<KB, WK>(C, KS, ut, ub);  // U (KB x KB) into the chunk buffer
+  }
+  __syncthreads();
   }
   // descending order of the Ritz values: the stored block stays sorted, so the
   // next warm-started QR processes dominant directions first
@@ -1188,25 +1563,34 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
     load_chunk_to<DP, R>(C, wl, F, Dg, i0, rows, prm.inv_beta);
     __syncthreads();
     {
-      float2 y[NC];
+      // only the first r (sorted) Ritz columns have f > 0
+      auto ritz_cols = [&](auto nbc) {
+        constexpr int NB = decltype(nbc)::value;
+        float2 y[NB];
 #pragma unroll
-      for (int n = 0; n < NC; ++n) y[n] = make_float2(0.f, 0.f);
-      for (int k = 0; k < d; ++k) {
-        const float2 a = C[yi * DP + k];
+        for (int n = 0; n < NB; ++n) y[n] = make_float2(0.f, 0.f);
+        for (int k = 0; k < d; ++k) {
+          const float2 a = C[yi * DP + k];
 #pragma unroll
-        for (int n = 0; n < NC; ++n) cfma(y[n], a, Vf[k * KS + c16 + 16 * n]);
-      }
+          for (int n = 0; n < NB; ++n) cfma(y[n], a, Vf[k * KS + c16 + 16 * n]);
+        }
 #pragma unroll
-      for (int n = 0; n < NC; ++n) Yc[yi * KS + c16 + 16 * n] = cscale(y[n], S.f[c16 + 16 * n]);
+        for (int n = 0; n < NB; ++n) Yc[yi * KS + c16 + 16 * n] = cscale(y[n], S.f[c16 + 16 * n]);
+      };
+      static_assert(NC <= 3, "NC > 3 needs more cases");
+      const int nb = (r + 15) >> 4;
+      if (nb <= 1) ritz_cols(std::integral_constant<int, 1>{});
+      else if (nb == 2 || NC == 2) ritz_cols(std::integral_constant<int, (NC >= 2 ? 2 : 1)>{});
+      else ritz_cols(std::integral_constant<int, NC>{});
     }
     __syncthreads();
     {
-      // Z[yi][k] = sum_j Yc[yi][j] conj(Vf[k][j]), k = c16 + 16 m
+      // Z[yi][k] = sum_{j < r} Yc[yi][j] conj(Vf[k][j]), k = c16 + 16 m
       constexpr int MZ = (DP + 15) / 16;
       float2 z[MZ];
 #pragma unroll
       for (int m = 0; m < MZ; ++m) z[m] = make_float2(0.f, 0.f);
-      for (int j = 0; j < KB; ++j) {
+      for (int j = 0; j < r; ++j) {
         const float2 yv = Yc[yi * KS + j];
 #pragma unroll
         for (int m = 0; m < MZ; ++m) {
