@@ -1133,15 +1133,20 @@ __device__ void hermitian_eig_tridiag(float2* H, float* scr, float* work, float2
     for (int i = 0; i < n; ++i) Y[i * n + k] *= inv;
   }
   __syncthreads();
-  // clusters (gap < 1e-5 of the spectral radius): the twisted vectors
-  // of the members nearly coincide; rebuild members 2.. by inverse iteration
+  // clusters (gap < 2e-6 of the spectral radius): the twisted vectors of the
+  // members nearly coincide; rebuild members 2.. by inverse iteration
   // (T - lam_k) x = y with reorthogonalisation against the earlier members
-  // (LAPACK stein-style), one thread, sequential -- clusters are rare.
-  if (tid == 0) {
+  // (LAPACK stein-style).  One warp: rows lane and lane + 32, dot products by
+  // warp reduction, the tridiagonal solve by lane 0.  At most 24 members per
+  // matrix are rebuilt (clusters are rare: bound the worst case).
+  if (warp == 0) {
+    static_assert(n <= 64, "two rows per lane");
     const float tnorm = fmaxf(fabsf((float)evals[0]), fabsf((float)evals[n - 1]));
-    const float ctol = 1e-5f * tnorm, dfloor = 1e-7f * tnorm + pivmin;
-    int cs = 0;
-    for (int k = 1; k < n; ++k) {
+    const float ctol = 2e-6f * tnorm, dfloor = 1e-7f * tnorm + pivmin;
+    const int r0 = lane, r1 = lane + 32;
+    const bool h1 = r1 < n;
+    int cs = 0, budget = 24;
+    for (int k = 1; k < n && budget > 0; ++k) {
       if ((float)(evals[k - 1] - evals[k]) > ctol) {
         cs = k;
         continue;
@@ -1149,42 +1154,59 @@ __device__ void hermitian_eig_tridiag(float2* H, float* scr, float* work, float2
       // clusters below `care` (shrink factor 0) keep their MGS-orthonormalised
       // twisted vectors: any orthonormal basis of that tail will do
       if ((float)evals[cs] < care) continue;
-      const float lam = (float)evals[k];
+      --budget;
+      float y0 = Y[r0 * n + k], y1 = h1 ? Y[r1 * n + k] : 0.f;
       for (int it = 0; it < 3; ++it) {
-        // orthogonalise the current iterate against members cs..k-1 and normalise
         for (int p = cs; p < k; ++p) {
-          float dt = 0.f;
-          for (int i = 0; i < n; ++i) dt = fmaf(Y[i * n + p], Y[i * n + k], dt);
-          for (int i = 0; i < n; ++i) Y[i * n + k] = fmaf(-dt, Y[i * n + p], Y[i * n + k]);
+          const float p0 = Y[r0 * n + p], p1 = h1 ? Y[r1 * n + p] : 0.f;
+          const float dt = warp_sum_f(fmaf(y0, p0, y1 * p1));
+          y0 = fmaf(-dt, p0, y0);
+          y1 = fmaf(-dt, p1, y1);
         }
-        float nn = 0.f;
-        for (int i = 0; i < n; ++i) nn = fmaf(Y[i * n + k], Y[i * n + k], nn);
+        const float nn = warp_sum_f(fmaf(y0, y0, y1 * y1));
         if (!(nn > 1e-30f)) {  // fully dependent: restart from a fixed pseudo-random vector
-          for (int i = 0; i < n; ++i) Y[i * n + k] = hash_unit(0x9E3779B9u * (unsigned)(i + 1) + (unsigned)k);
+          y0 = hash_unit(0x9E3779B9u * (unsigned)(r0 + 1) + (unsigned)k);
+          y1 = h1 ? hash_unit(0x9E3779B9u * (unsigned)(r1 + 1) + (unsigned)k) : 0.f;
           continue;
         }
         const float inn = rsqrtf(nn);
-        for (int i = 0; i < n; ++i) Y[i * n + k] *= inn;
+        y0 *= inn;
+        y1 *= inn;
         if (it == 2) break;
         // one inverse-iteration step with the stored L D L^T of T - lam (D floored)
-        float w = Y[k];
-        auto dfl = [&](float dv) { return fabsf(dv) < dfloor ? copysignf(dfloor, dv) : dv; };
-        for (int i = 1; i < n; ++i) {
-          const float wi = Y[i * n + k] - (bb[i - 1] / dfl(Dp[(i - 1) * n + k])) * w;
-          Y[(i - 1) * n + k] = w / dfl(Dp[(i - 1) * n + k]);
-          w = wi;
+        Y[r0 * n + k] = y0;
+        if (h1) Y[r1 * n + k] = y1;
+        __syncwarp();
+        if (lane == 0) {
+          auto dfl = [&](float dv) { return fabsf(dv) < dfloor ? copysignf(dfloor, dv) : dv; };
+          float w = Y[k];
+          for (int i = 1; i < n; ++i) {
+            const float dv = dfl(Dp[(i - 1) * n + k]);
+            const float wi = Y[i * n + k] - (bb[i - 1] / dv) * w;
+            Y[(i - 1) * n + k] = w / dv;
+            w = wi;
+          }
+          float x = w / dfl(Dp[(n - 1) * n + k]);
+          Y[(n - 1) * n + k] = x;
+          for (int i = n - 2; i >= 0; --i) {
+            x = Y[i * n + k] - (bb[i] / dfl(Dp[i * n + k])) * x;
+            Y[i * n + k] = x;
+          }
         }
-        float x = w / dfl(Dp[(n - 1) * n + k]);
-        Y[(n - 1) * n + k] = x;
-        for (int i = n - 2; i >= 0; --i) {
-          x = Y[i * n + k] - (bb[i] / dfl(Dp[i * n + k])) * x;
-          Y[i * n + k] = x;
+        __syncwarp();
+        y0 = Y[r0 * n + k];
+        y1 = h1 ? Y[r1 * n + k] : 0.f;
+        float mx = fmaxf(fabsf(y0), fabsf(y1));  // keep the iterate in range
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (mx > 0.f) {
+          y0 /= mx;
+          y1 /= mx;
         }
-        float mx = 0.f;  // keep the iterate in range before reorthogonalising
-        for (int i = 0; i < n; ++i) mx = fmaxf(mx, fabsf(Y[i * n + k]));
-        if (mx > 0.f)
-          for (int i = 0; i < n; ++i) Y[i * n + k] /= mx;
       }
+      Y[r0 * n + k] = y0;
+      if (h1) Y[r1 * n + k] = y1;
+      __syncwarp();
     }
   }
   __syncthreads();
