@@ -13,6 +13,8 @@
 #include <type_traits>
 #include <string>
 
+#include <cuda_pipeline.h>
+
 #include "hankel_svt.cuh"
 
 namespace shlr_b200 {
@@ -123,6 +125,80 @@ __device__ __forceinline__ void load_chunk_to(float2* dst, const float2* wl, con
       }
     }
     dst[t] = v;
+  }
+}
+
+// Asynchronous copy (cp.async, L2 -> smem) of the dual rows [i0, i0 + rows)
+// of one matrix -- rows * d contiguous complex64 in HBM -- into `stage`.
+// The caller waits with stage_d_wait() before reading it.
+__device__ __forceinline__ void stage_d_async(float2* stage, const float2* Dg, int i0, int rows, int d) {
+  const float2* src = Dg + (long long)i0 * d;
+  const int cnt = rows * d;
+  const bool al16 = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(stage)) & 15) == 0;
+  if (al16) {
+    const int n16 = cnt >> 1;
+    for (int t = threadIdx.x; t < n16; t += blockDim.x) __pipeline_memcpy_async(stage + 2 * t, src + 2 * t, 16);
+    if ((cnt & 1) && threadIdx.x == 0) __pipeline_memcpy_async(stage + cnt - 1, src + cnt - 1, 8);
+  } else {
+    for (int t = threadIdx.x; t < cnt; t += blockDim.x) __pipeline_memcpy_async(stage + t, src + t, 8);
+  }
+  __pipeline_commit();
+}
+__device__ __forceinline__ void stage_d_wait() {
+  __pipeline_wait_prior(0);
+  __syncthreads();
+}
+
+// Ahat chunk rows [i0, i0 + rows) into dst (R x DP, zero padded) from the
+// smem spectra and the staged duals (row stride d), or without duals.
+template <int DP, int R>
+__device__ __forceinline__ void build_chunk(float2* dst, const float2* wl, const SvtFamily& F,
+                                            const float2* dstage, int i0, int rows, float inv_beta) {
+  const int d = F.d;
+  for (int t = threadIdx.x; t < R * DP; t += blockDim.x) {
+    const int r = t / DP, u = t - r * DP;
+    float2 v = make_float2(0.f, 0.f);
+    if (r < rows && u < d) {
+      v = lift_elem(wl, F, i0 + r, u);
+      if (dstage) {
+        const float2 dd = dstage[r * d + u];
+        v.x = fmaf(dd.x, inv_beta, v.x);
+        v.y = fmaf(dd.y, inv_beta, v.y);
+      }
+    }
+    dst[t] = v;
+  }
+}
+
+// Yc (rows r2, r2+1 of the chunk; columns c16 + 16 n, n < NB) = C B for the
+// first 256 threads (2 x NB register tiles: 2 + NB shared loads per 2 NB
+// complex FMAs), optionally column-scaled.
+template <int DP, int KS, int NB>
+__device__ __forceinline__ void chunk_times_block(const float2* C, const float2* Bm, float2* Yc, int d,
+                                                  const float* scale) {
+  const int tid = threadIdx.x;
+  if (tid >= 256) return;
+  const int r2 = (tid >> 4) * 2, c16 = tid & 15;
+  float2 y0[NB], y1[NB];
+#pragma unroll
+  for (int n = 0; n < NB; ++n) y0[n] = y1[n] = make_float2(0.f, 0.f);
+  const float2* c0 = C + r2 * DP;
+  const float2* c1 = c0 + DP;
+#pragma unroll 2
+  for (int k = 0; k < d; ++k) {
+    const float2 a0 = c0[k], a1 = c1[k];
+#pragma unroll
+    for (int n = 0; n < NB; ++n) {
+      const float2 b = Bm[k * KS + c16 + 16 * n];
+      cfma(y0[n], a0, b);
+      cfma(y1[n], a1, b);
+    }
+  }
+#pragma unroll
+  for (int n = 0; n < NB; ++n) {
+    const float sc = scale ? scale[c16 + 16 * n] : 1.f;
+    Yc[r2 * KS + c16 + 16 * n] = cscale(y0[n], sc);
+    Yc[(r2 + 1) * KS + c16 + 16 * n] = cscale(y1[n], sc);
   }
 }
 
@@ -1364,28 +1440,24 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
   const int iters = warm ? prm.q_warm : prm.q_cold;
 
   // ---------------------------------------------------------- subspace iteration
+  // Duals are staged chunk by chunk with cp.async into a buffer that is free
+  // during the pass (X here, V in the epilogue pass): the copy of chunk c+1
+  // overlaps the GEMMs of chunk c.
   for (int it = 0; it < iters; ++it) {
     float2 xa[MR][NC];
 #pragma unroll
     for (int m = 0; m < MR; ++m)
 #pragma unroll
       for (int n = 0; n < NC; ++n) xa[m][n] = make_float2(0.f, 0.f);
+    __syncthreads();  // X (reflectors of the last QR) is free from here
+    if (Dg) stage_d_async(X, Dg, 0, min(R, e), d);
     for (int i0 = 0; i0 < e; i0 += R) {
       const int rows = min(R, e - i0);
-      load_chunk_to<DP, R>(C, wl, F, Dg, i0, rows, prm.inv_beta);
+      if (Dg) stage_d_wait();
+      build_chunk<DP, R>(C, wl, F, Dg ? X : nullptr, i0, rows, prm.inv_beta);
       __syncthreads();
-      {  // Yc = C V
-        float2 y[NC];
-#pragma unroll
-        for (int n = 0; n < NC; ++n) y[n] = make_float2(0.f, 0.f);
-        for (int k = 0; k < d; ++k) {
-          const float2 a = C[yi * DP + k];
-#pragma unroll
-          for (int n = 0; n < NC; ++n) cfma(y[n], a, V[k * KS + c16 + 16 * n]);
-        }
-#pragma unroll
-        for (int n = 0; n < NC; ++n) Yc[yi * KS + c16 + 16 * n] = y[n];
-      }
+      if (Dg && i0 + R < e) stage_d_async(X, Dg, i0 + R, min(R, e - i0 - R), d);
+      chunk_times_block<DP, KS, NC>(C, V, Yc, d, nullptr);  // Yc = C V
       __syncthreads();
       for (int i = 0; i < rows; ++i) {  // X += C^H Yc
         float2 yv[NC];
@@ -1401,8 +1473,9 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
           }
         }
       }
-      __syncthreads();
+      if (!Dg) __syncthreads();  // with duals the next stage_d_wait() is the barrier
     }
+    if (Dg) __syncthreads();
 #pragma unroll
     for (int m = 0; m < MR; ++m) {
       const int k = yi + 32 * m;
@@ -1431,22 +1504,15 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
     for (int m = 0; m < HM; ++m)
 #pragma unroll
       for (int n = 0; n < NC; ++n) h[m][n] = make_float2(0.f, 0.f);
+    __syncthreads();  // X is free from here
+    if (Dg) stage_d_async(X, Dg, 0, min(R, e), d);
     for (int i0 = 0; i0 < e; i0 += R) {
       const int rows = min(R, e - i0);
-      load_chunk_to<DP, R>(C, wl, F, Dg, i0, rows, prm.inv_beta);
+      if (Dg) stage_d_wait();
+      build_chunk<DP, R>(C, wl, F, Dg ? X : nullptr, i0, rows, prm.inv_beta);
       __syncthreads();
-      {
-        float2 y[NC];
-#pragma unroll
-        for (int n = 0; n < NC; ++n) y[n] = make_float2(0.f, 0.f);
-        for (int k = 0; k < d; ++k) {
-          const float2 a = C[yi * DP + k];
-#pragma unroll
-          for (int n = 0; n < NC; ++n) cfma(y[n], a, V[k * KS + c16 + 16 * n]);
-        }
-#pragma unroll
-        for (int n = 0; n < NC; ++n) Yc[yi * KS + c16 + 16 * n] = y[n];
-      }
+      if (Dg && i0 + R < e) stage_d_async(X, Dg, i0 + R, min(R, e - i0 - R), d);
+      chunk_times_block<DP, KS, NC>(C, V, Yc, d, nullptr);
       __syncthreads();
       for (int i = 0; i < rows; ++i) {
 #pragma unroll
@@ -1459,8 +1525,9 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
           }
         }
       }
-      __syncthreads();
+      if (!Dg) __syncthreads();
     }
+    if (Dg) __syncthreads();
     // H (full Hermitian, stride KB+1 = KS) into X, diagonal to S.dg
 #pragma unroll
     for (int m = 0; m < HM; ++m) {
@@ -1580,30 +1647,21 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
 
   // ---------------------------------------------------------- Z = (Ahat V) f V^H, duals, adjoint
   SUB_STAMP(6);
+  float2* Ds = V;  // the old basis is dead: stage the duals there
+  __syncthreads();
+  if (Dg) stage_d_async(Ds, Dg, 0, min(R, e), d);
   for (int i0 = 0; i0 < e; i0 += R) {
     const int rows = min(R, e - i0);
-    load_chunk_to<DP, R>(C, wl, F, Dg, i0, rows, prm.inv_beta);
+    if (Dg) stage_d_wait();
+    build_chunk<DP, R>(C, wl, F, Dg ? Ds : nullptr, i0, rows, prm.inv_beta);
     __syncthreads();
     {
       // only the first r (sorted) Ritz columns have f > 0
-      auto ritz_cols = [&](auto nbc) {
-        constexpr int NB = decltype(nbc)::value;
-        float2 y[NB];
-#pragma unroll
-        for (int n = 0; n < NB; ++n) y[n] = make_float2(0.f, 0.f);
-        for (int k = 0; k < d; ++k) {
-          const float2 a = C[yi * DP + k];
-#pragma unroll
-          for (int n = 0; n < NB; ++n) cfma(y[n], a, Vf[k * KS + c16 + 16 * n]);
-        }
-#pragma unroll
-        for (int n = 0; n < NB; ++n) Yc[yi * KS + c16 + 16 * n] = cscale(y[n], S.f[c16 + 16 * n]);
-      };
       static_assert(NC <= 3, "NC > 3 needs more cases");
       const int nb = (r + 15) >> 4;
-      if (nb <= 1) ritz_cols(std::integral_constant<int, 1>{});
-      else if (nb == 2 || NC == 2) ritz_cols(std::integral_constant<int, (NC >= 2 ? 2 : 1)>{});
-      else ritz_cols(std::integral_constant<int, NC>{});
+      if (nb <= 1) chunk_times_block<DP, KS, 1>(C, Vf, Yc, d, S.f);
+      else if (nb == 2 || NC == 2) chunk_times_block<DP, KS, (NC >= 2 ? 2 : 1)>(C, Vf, Yc, d, S.f);
+      else chunk_times_block<DP, KS, NC>(C, Vf, Yc, d, S.f);
     }
     __syncthreads();
     {
@@ -1628,7 +1686,7 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
           if (admm) {
             const float2 L = lift_elem(wl, F, i0 + yi, k);
             const long long gi = (long long)(i0 + yi) * d + k;
-            float2 dn = Dg[gi];
+            float2 dn = Ds[yi * d + k];
             dn.x = fmaf(prm.tau_dual, L.x - z[m].x, dn.x);
             dn.y = fmaf(prm.tau_dual, L.y - z[m].y, dn.y);
             Dg[gi] = dn;
@@ -1640,6 +1698,7 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
       }
     }
     __syncthreads();
+    if (Dg && i0 + R < e) stage_d_async(Ds, Dg, i0 + R, min(R, e - i0 - R), d);  // overlaps the adjoint
     for (int o = tid; o < B * len; o += NT) {
       const int b = o / len, n = o - b * len;
       float2 s = acc[o];
