@@ -151,15 +151,22 @@ __device__ __forceinline__ void stage_d_wait() {
 
 // Ahat chunk rows [i0, i0 + rows) into dst (R x DP, zero padded) from the
 // smem spectra and the staged duals (row stride d), or without duals.
+// lofs: per-index spectrum offsets (b * len + t of index = b * q + t) over the
+// lifted matrix's block index (columns of A when tall, rows of A^H when wide).
+__device__ __forceinline__ float2 lift_tab(const float2* wl, const int* lofs, bool wide, int i, int u) {
+  return wide ? cconj(wl[lofs[i] + u]) : wl[lofs[u] + i];
+}
+
 template <int DP, int R>
-__device__ __forceinline__ void build_chunk(float2* dst, const float2* wl, const SvtFamily& F,
+__device__ __forceinline__ void build_chunk(float2* dst, const float2* wl, const int* lofs, const SvtFamily& F,
                                             const float2* dstage, int i0, int rows, float inv_beta) {
   const int d = F.d;
+  const bool wide = F.wide;
   for (int t = threadIdx.x; t < R * DP; t += blockDim.x) {
     const int r = t / DP, u = t - r * DP;
     float2 v = make_float2(0.f, 0.f);
     if (r < rows && u < d) {
-      v = lift_elem(wl, F, i0 + r, u);
+      v = lift_tab(wl, lofs, wide, i0 + r, u);
       if (dstage) {
         const float2 dd = dstage[r * d + u];
         v.x = fmaf(dd.x, inv_beta, v.x);
@@ -167,6 +174,48 @@ __device__ __forceinline__ void build_chunk(float2* dst, const float2* wl, const
       }
     }
     dst[t] = v;
+  }
+}
+
+// Yc = C B over all 512 threads: the k range is split in two halves (threads
+// 0-255 -> Yc, 256-511 -> Yc2), each half a 2 x NB register tile per thread
+// (2 + NB shared loads per 2 NB complex FMAs).  The caller sums the halves
+// (sum_halves) after a barrier.
+template <int DP, int KS, int NB>
+__device__ __forceinline__ void chunk_times_block_split(const float2* C, const float2* Bm, float2* Yc,
+                                                        float2* Yc2, int d) {
+  const int h = threadIdx.x >> 8, t = threadIdx.x & 255;
+  const int r2 = (t >> 4) * 2, c16 = t & 15;
+  const int dh = (d + 1) >> 1;
+  const int kb = h ? dh : 0, ke = h ? d : dh;
+  float2 y0[NB], y1[NB];
+#pragma unroll
+  for (int n = 0; n < NB; ++n) y0[n] = y1[n] = make_float2(0.f, 0.f);
+  const float2* c0 = C + r2 * DP;
+  const float2* c1 = c0 + DP;
+#pragma unroll 2
+  for (int k = kb; k < ke; ++k) {
+    const float2 a0 = c0[k], a1 = c1[k];
+#pragma unroll
+    for (int n = 0; n < NB; ++n) {
+      const float2 b = Bm[k * KS + c16 + 16 * n];
+      cfma(y0[n], a0, b);
+      cfma(y1[n], a1, b);
+    }
+  }
+  float2* out = h ? Yc2 : Yc;
+#pragma unroll
+  for (int n = 0; n < NB; ++n) {
+    out[r2 * KS + c16 + 16 * n] = y0[n];
+    out[(r2 + 1) * KS + c16 + 16 * n] = y1[n];
+  }
+}
+template <int KS, int R>
+__device__ __forceinline__ void sum_halves(float2* Yc, const float2* Yc2, int ncols, const float* scale) {
+  for (int t = threadIdx.x; t < R * ncols; t += blockDim.x) {
+    const int r = t / ncols, c = t - r * ncols;
+    const float sc = scale ? scale[c] : 1.f;
+    Yc[r * KS + c] = cscale(cadd(Yc[r * KS + c], Yc2[r * KS + c]), sc);
   }
 }
 
@@ -1376,9 +1425,10 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
   float2* Yc = C + R * DP;                           // R x KS
   float2* wl = Yc + R * KS;                          // B x len
   float2* acc = wl + B * len;                        // B x len
+  float2* Yc2 = acc + B * len;                       // R x KS (second k-half of the chunk GEMM)
   Smem<KB> S;                                        // Rayleigh-Ritz Jacobi workspace
   S.G = X;
-  S.rec = reinterpret_cast<SlotRec*>(acc + B * len);
+  S.rec = reinterpret_cast<SlotRec*>(Yc2 + R * KS);
   S.dgr = reinterpret_cast<double2*>(S.rec + KB);
   S.dg = reinterpret_cast<double*>(S.dgr + KB);
   S.f = reinterpret_cast<float*>(S.dg + KB);
@@ -1387,6 +1437,7 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
   S.scal = reinterpret_cast<float*>(S.flags + 4);
   int* cnt = reinterpret_cast<int*>(S.scal + 4);
   int* perm = cnt + 4;                               // KB: descending-order position
+  int* lofs = perm + KB;                             // max(d, e): lift offsets (lift_tab)
 
   float2* Dg = admm ? F.D + (long long)mat * e * d : nullptr;
   float2* Vsg = F.Vs + (long long)mat * DP * KB;
@@ -1410,6 +1461,10 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
       }
     }
     for (int t = tid; t < B * len; t += NT) acc[t] = make_float2(0.f, 0.f);
+    for (int t = tid; t < (F.wide ? e : d); t += NT) {
+      const int b = t / F.q;
+      lofs[t] = b * len + (t - b * F.q);
+    }
     if (tid < 4) S.flags[tid] = 0;
     if (tid == 0) *cnt = 0;
   }
@@ -1454,11 +1509,14 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
     for (int i0 = 0; i0 < e; i0 += R) {
       const int rows = min(R, e - i0);
       if (Dg) stage_d_wait();
-      build_chunk<DP, R>(C, wl, F, Dg ? X : nullptr, i0, rows, prm.inv_beta);
+      build_chunk<DP, R>(C, wl, lofs, F, Dg ? X : nullptr, i0, rows, prm.inv_beta);
       __syncthreads();
       if (Dg && i0 + R < e) stage_d_async(X, Dg, i0 + R, min(R, e - i0 - R), d);
-      chunk_times_block<DP, KS, NC>(C, V, Yc, d, nullptr);  // Yc = C V
+      chunk_times_block_split<DP, KS, NC>(C, V, Yc, Yc2, d);  // Yc = C V
       __syncthreads();
+      sum_halves<KS, R>(Yc, Yc2, KB, nullptr);
+      __syncthreads();
+#pragma unroll 4
       for (int i = 0; i < rows; ++i) {  // X += C^H Yc
         float2 yv[NC];
 #pragma unroll
@@ -1509,10 +1567,12 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
     for (int i0 = 0; i0 < e; i0 += R) {
       const int rows = min(R, e - i0);
       if (Dg) stage_d_wait();
-      build_chunk<DP, R>(C, wl, F, Dg ? X : nullptr, i0, rows, prm.inv_beta);
+      build_chunk<DP, R>(C, wl, lofs, F, Dg ? X : nullptr, i0, rows, prm.inv_beta);
       __syncthreads();
       if (Dg && i0 + R < e) stage_d_async(X, Dg, i0 + R, min(R, e - i0 - R), d);
-      chunk_times_block<DP, KS, NC>(C, V, Yc, d, nullptr);
+      chunk_times_block_split<DP, KS, NC>(C, V, Yc, Yc2, d);
+      __syncthreads();
+      sum_halves<KS, R>(Yc, Yc2, KB, nullptr);
       __syncthreads();
       for (int i = 0; i < rows; ++i) {
 #pragma unroll
@@ -1653,15 +1713,17 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
   for (int i0 = 0; i0 < e; i0 += R) {
     const int rows = min(R, e - i0);
     if (Dg) stage_d_wait();
-    build_chunk<DP, R>(C, wl, F, Dg ? Ds : nullptr, i0, rows, prm.inv_beta);
+    build_chunk<DP, R>(C, wl, lofs, F, Dg ? Ds : nullptr, i0, rows, prm.inv_beta);
     __syncthreads();
     {
       // only the first r (sorted) Ritz columns have f > 0
       static_assert(NC <= 3, "NC > 3 needs more cases");
       const int nb = (r + 15) >> 4;
-      if (nb <= 1) chunk_times_block<DP, KS, 1>(C, Vf, Yc, d, S.f);
-      else if (nb == 2 || NC == 2) chunk_times_block<DP, KS, (NC >= 2 ? 2 : 1)>(C, Vf, Yc, d, S.f);
-      else chunk_times_block<DP, KS, NC>(C, Vf, Yc, d, S.f);
+      if (nb <= 1) chunk_times_block_split<DP, KS, 1>(C, Vf, Yc, Yc2, d);
+      else if (nb == 2 || NC == 2) chunk_times_block_split<DP, KS, (NC >= 2 ? 2 : 1)>(C, Vf, Yc, Yc2, d);
+      else chunk_times_block_split<DP, KS, NC>(C, Vf, Yc, Yc2, d);
+      __syncthreads();
+      sum_halves<KS, R>(Yc, Yc2, 16 * min(nb, NC), S.f);
     }
     __syncthreads();
     {
@@ -1684,7 +1746,7 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
         if (yi < rows && k < d) {
           float2 tv = z[m];
           if (admm) {
-            const float2 L = lift_elem(wl, F, i0 + yi, k);
+            const float2 L = lift_tab(wl, lofs, F.wide, i0 + yi, k);
             const long long gi = (long long)(i0 + yi) * d + k;
             float2 dn = Ds[yi * d + k];
             dn.x = fmaf(prm.tau_dual, L.x - z[m].x, dn.x);
@@ -1735,11 +1797,11 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
   }
 }
 
-size_t svt_subspace_smem_bytes(int DP, int KB, int R, int maxB, int maxLen) {
+size_t svt_subspace_smem_bytes(int DP, int KB, int R, int maxB, int maxLen, int maxE) {
   const int KS = KB + 1;
-  return sizeof(float2) * (2ull * DP * KS + (size_t)R * DP + (size_t)R * KS + 2ull * maxB * maxLen) +
+  return sizeof(float2) * (2ull * DP * KS + (size_t)R * DP + 2ull * R * KS + 2ull * maxB * maxLen) +
          sizeof(SlotRec) * KB + sizeof(double2) * KB + sizeof(double) * KB + 2 * sizeof(float) * KB +
-         16 * sizeof(int) + sizeof(int) * KB + 64;
+         16 * sizeof(int) + sizeof(int) * KB + sizeof(int) * std::max(DP, maxE) + 64;
 }
 
 namespace {
@@ -1758,18 +1820,19 @@ void launch_sub(const SvtParams& prm, int total, size_t smem, cudaStream_t strea
 
 bool launch_hankel_svt_subspace(const SvtParams& prm, int total, cudaStream_t stream) {
   if (total <= 0) return true;
-  int dmin = 1 << 30, dmax = 0, maxB = 0, maxLen = 0;
+  int dmin = 1 << 30, dmax = 0, maxB = 0, maxLen = 0, maxE = 0;
   for (int f = 0; f < prm.nfam; ++f) {
     dmin = std::min(dmin, prm.fam[f].d);
     dmax = std::max(dmax, prm.fam[f].d);
     maxB = std::max(maxB, prm.fam[f].B);
     maxLen = std::max(maxLen, prm.fam[f].len);
+    maxE = std::max(maxE, prm.fam[f].e);
     if (!prm.fam[f].Vs || !prm.fam[f].fallback) return false;
   }
   // worthwhile only when the block is well below d
   if (dmin < kSubspaceKB + 24) return false;
   const int dp = svt_padded_dim(dmax);
-  const size_t smem = svt_subspace_smem_bytes(dp, kSubspaceKB, 32, maxB, maxLen);
+  const size_t smem = svt_subspace_smem_bytes(dp, kSubspaceKB, 32, maxB, maxLen, maxE);
   if (smem > 227 * 1024) return false;
   switch (dp) {
     case 72: launch_sub<72>(prm, total, smem, stream); return true;
