@@ -1018,7 +1018,7 @@ __device__ void householder_qr(float2* M, float2* Q, int d, float* tau) {
 //      3 CTA barriers per column; reflectors kept in H's columns);
 //   2. a diagonal phase similarity makes T real symmetric tridiagonal;
 //   3. eigenvalues by multisection on Sturm counts, 8 threads per eigenvalue
-//      (9 sub-intervals per step, 10 steps: below FP32 resolution);
+//      (9 sub-intervals per step, 8 steps: FP32 resolution);
 //   4. eigenvectors of T by the twisted factorisation (one thread per
 //      eigenvalue); members of clusters above `care` rebuilt by inverse
 //      iteration with reorthogonalisation; modified Gram-Schmidt in
@@ -1141,19 +1141,22 @@ __device__ void hermitian_eig_tridiag(float2* H, float* scr, float* work, float2
   }
   EIG_STAMP(1);
   // ---------------------------------------------------------- 2. real similarity
-  if (tid == 0) {
+  if (tid < n) {  // |e_j| and the unit factors e_j / |e_j| in parallel
+    const float2 e = tid < n - 1 ? ee[tid] : make_float2(0.f, 0.f);
+    const float a = sqrtf(fmaf(e.x, e.x, e.y * e.y));
+    bb[tid] = a;
+    b2[tid] = a * a;
+    const float ia = a > 0.f ? 1.f / a : 0.f;
+    ee[tid] = a > 0.f ? make_float2(e.x * ia, e.y * ia) : make_float2(1.f, 0.f);
+  }
+  __syncthreads();
+  if (tid == 0) {  // phases: prefix products of the unit factors
     float2 p = make_float2(1.f, 0.f);
     ph[0] = p;
     for (int j = 0; j < n - 1; ++j) {
-      const float2 e = ee[j];
-      const float a = sqrtf(fmaf(e.x, e.x, e.y * e.y));
-      bb[j] = a;
-      b2[j] = a * a;
-      if (a > 0.f) p = cmul(p, make_float2(e.x / a, e.y / a));
+      p = cmul(p, ee[j]);
       ph[j + 1] = p;
     }
-    bb[n - 1] = 0.f;
-    b2[n - 1] = 0.f;
   }
   __syncthreads();
   EIG_STAMP(2);
@@ -1179,7 +1182,7 @@ __device__ void hermitian_eig_tridiag(float2* H, float* scr, float* work, float2
     lo -= pad;
     hi += pad;
     const int mrank = n - 1 - g;  // ascending index of the g-th largest eigenvalue
-    for (int it = 0; it < 10; ++it) {
+    for (int it = 0; it < 8; ++it) {  // 9^8 = 4.3e7: FP32 resolution of the interval
       const float h = (hi - lo) * (1.f / 9.f);
       const float x = lo + (float)(s + 1) * h;
       int c = 0;
@@ -1343,7 +1346,13 @@ __device__ void hermitian_eig_tridiag(float2* H, float* scr, float* work, float2
     float y[CU];
 #pragma unroll
     for (int t = 0; t < CU; ++t) y[t] = act ? Y[(s + 8 * t) * n + g] : 0.f;
-    for (int k = 0; k < n; ++k) {
+    // Gram-Schmidt over the eigenvectors whose eigenvalue is >= care (the
+    // only ones that enter the thresholded spectral function; the rest are a
+    // warm-start basis that the next QR re-orthonormalises) plus one
+    int nh = 1;
+    for (int k = 1; k < n; ++k) nh += (float)evals[k] >= care;
+    nh = min(n, nh + 1);
+    for (int k = 0; k < nh; ++k) {
       float ss = 0.f;
 #pragma unroll
       for (int t = 0; t < CU; ++t) ss = fmaf(y[t], y[t], ss);
@@ -1544,7 +1553,24 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
     __syncthreads();
     clk_pass += clock64() - clk_t;
     clk_t = clock64();
-    householder_qr<KB, KS, DP>(X, V, d, tau);
+    if (warm && prm.inner_norm && it + 1 < iters) {
+      // warm inner pass: X ~ V0 Lambda with V0 the previous (sorted) Ritz
+      // vectors, so unit columns are already a well-conditioned basis; the
+      // last pass is orthonormalised before the Rayleigh-Ritz projection
+      const int g = tid >> 3, s8 = tid & 7;
+      float ss = 0.f;
+      if (g < KB)
+        for (int row = s8; row < d; row += 8) {
+          const float2 x = X[row * KS + g];
+          ss = fmaf(x.x, x.x, fmaf(x.y, x.y, ss));
+        }
+      ss = group8_sum(ss);
+      const float inv = ss > 1e-30f ? rsqrtf(ss) : 0.f;
+      if (g < KB)
+        for (int row = s8; row < DP; row += 8) V[row * KS + g] = cscale(X[row * KS + g], inv);
+    } else {
+      householder_qr<KB, KS, DP>(X, V, d, tau);
+    }
     clk_qr += clock64() - clk_t;
     clk_t = clock64();
   }

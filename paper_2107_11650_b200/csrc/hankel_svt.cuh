@@ -71,6 +71,7 @@ struct SvtParams {
   float rr_tol_rel, rr_tol_abs;  // subspace Rayleigh-Ritz rotation tolerances (0 = defaults)
   float rr_tail;                 // pairs with both Ritz values < rr_tail * thresh^2 not rotated
   int rr_jacobi;                 // 1: Rayleigh-Ritz by parallel Jacobi instead of tridiagonal + bisection
+  int inner_norm;                // warm: normalise (instead of QR) after all but the last pass
   int wl_global;       // set by launch_hankel_svt: the lift source is read straight from
                        // fam[f].spec (plain mode, contiguous coils) instead of an smem copy
 };

@@ -927,6 +927,7 @@ void PiPlan::enqueue_iteration(int k, bool record_events) {
     sp.rr_tol_abs = rr_tol_abs_;
     sp.rr_tail = rr_tail_;
     sp.rr_jacobi = std::getenv("SHLR_RR_JACOBI") ? 1 : 0;
+    sp.inner_norm = std::getenv("SHLR_INNER_QR") ? 0 : 1;
     sp.phase_clk = phase_clk_;
     if (record_events) SHLR_CUDA(cudaEventRecord(evA_, stream_));
     // The debug singular-value hook needs every singular value: full solver.
