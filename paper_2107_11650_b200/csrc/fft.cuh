@@ -164,8 +164,13 @@ __device__ float2* smem_centered_dft(float2* a, float2* b, const FftTwiddles& tw
 // Transform along the middle axis of a tensor viewed as [outer][n][inner]
 // with a user Op providing load(o, k, i) and store(o, k, i, v).  Grid:
 // x = inner tiles of F fibres, y = outer.  Dynamic smem: 2 * n * F float2.
+// Threads of the smem-FFT kernels: 512 gives one radix-4 butterfly per
+// thread for an 8-fibre tile of length 256 and doubles the resident warps
+// per SM over 256 (these kernels are latency-bound, their data L2-resident).
+constexpr int kFftThreads = 512;
+
 template <class Op, bool INV>
-__global__ void __launch_bounds__(256) fft_axis_kernel(Op op, FftTwiddles tw, int outer,
+__global__ void __launch_bounds__(kFftThreads) fft_axis_kernel(Op op, FftTwiddles tw, int outer,
                                                        int inner, int F) {
   extern __shared__ float2 fft_smem[];
   if (op.skip()) return;
@@ -213,7 +218,7 @@ void launch_fft_axis(const Op& op, const FftTwiddles& tw, int outer, int inner, 
     configured = true;
   }
   dim3 grid((inner + F - 1) / F, outer);
-  fft_axis_kernel<Op, INV><<<grid, 256, smem, stream>>>(op, tw, outer, inner, F);
+  fft_axis_kernel<Op, INV><<<grid, kFftThreads, smem, stream>>>(op, tw, outer, inner, F);
   SHLR_LAUNCH_CHECK();
 }
 

@@ -193,7 +193,7 @@ __device__ __forceinline__ void chunk_times_block_split(const float2* C, const f
   for (int n = 0; n < NB; ++n) y0[n] = y1[n] = make_float2(0.f, 0.f);
   const float2* c0 = C + r2 * DP;
   const float2* c1 = c0 + DP;
-#pragma unroll 2
+#pragma unroll 4
   for (int k = kb; k < ke; ++k) {
     const float2 a0 = c0[k], a1 = c1[k];
 #pragma unroll
@@ -1478,8 +1478,11 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
     if (tid == 0) *cnt = 0;
   }
   long long clk_qr = 0, clk_pass = 0, clk_t = clock64();
+  long long clk_wait = 0, clk_build = 0, clk_g1 = 0, clk_sum = 0, clk_g2 = 0, clk_u = 0;
+#define SUB_ACC(v) \
+  if (prm.phase_clk) { const long long nw_ = clock64(); v += nw_ - clk_u; clk_u = nw_; }
 #define SUB_STAMP(k) \
-  if (prm.phase_clk && tid == 0) prm.phase_clk[(long long)blockIdx.x * 8 + (k)] = clock64()
+  if (prm.phase_clk && tid == 0) prm.phase_clk[(long long)blockIdx.x * kPhaseSlots + (k)] = clock64()
   SUB_STAMP(0);
 
   // ---------------------------------------------------------- starting block
@@ -1515,16 +1518,21 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
       for (int n = 0; n < NC; ++n) xa[m][n] = make_float2(0.f, 0.f);
     __syncthreads();  // X (reflectors of the last QR) is free from here
     if (Dg) stage_d_async(X, Dg, 0, min(R, e), d);
+    if (prm.phase_clk) clk_u = clock64();
     for (int i0 = 0; i0 < e; i0 += R) {
       const int rows = min(R, e - i0);
       if (Dg) stage_d_wait();
+      SUB_ACC(clk_wait);
       build_chunk<DP, R>(C, wl, lofs, F, Dg ? X : nullptr, i0, rows, prm.inv_beta);
       __syncthreads();
+      SUB_ACC(clk_build);
       if (Dg && i0 + R < e) stage_d_async(X, Dg, i0 + R, min(R, e - i0 - R), d);
       chunk_times_block_split<DP, KS, NC>(C, V, Yc, Yc2, d);  // Yc = C V
       __syncthreads();
+      SUB_ACC(clk_g1);
       sum_halves<KS, R>(Yc, Yc2, KB, nullptr);
       __syncthreads();
+      SUB_ACC(clk_sum);
 #pragma unroll 4
       for (int i = 0; i < rows; ++i) {  // X += C^H Yc
         float2 yv[NC];
@@ -1541,6 +1549,7 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
         }
       }
       if (!Dg) __syncthreads();  // with duals the next stage_d_wait() is the barrier
+      SUB_ACC(clk_g2);
     }
     if (Dg) __syncthreads();
 #pragma unroll
@@ -1575,8 +1584,13 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
     clk_t = clock64();
   }
   if (prm.phase_clk && tid == 0) {
-    prm.phase_clk[(long long)blockIdx.x * 8 + 1] = clk_pass;
-    prm.phase_clk[(long long)blockIdx.x * 8 + 2] = clk_qr;
+    prm.phase_clk[(long long)blockIdx.x * kPhaseSlots + 1] = clk_pass;
+    prm.phase_clk[(long long)blockIdx.x * kPhaseSlots + 2] = clk_qr;
+    prm.phase_clk[(long long)blockIdx.x * kPhaseSlots + 8] = clk_wait;
+    prm.phase_clk[(long long)blockIdx.x * kPhaseSlots + 9] = clk_build;
+    prm.phase_clk[(long long)blockIdx.x * kPhaseSlots + 10] = clk_g1;
+    prm.phase_clk[(long long)blockIdx.x * kPhaseSlots + 11] = clk_sum;
+    prm.phase_clk[(long long)blockIdx.x * kPhaseSlots + 12] = clk_g2;
   }
   SUB_STAMP(3);
 

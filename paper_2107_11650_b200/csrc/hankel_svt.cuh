@@ -65,7 +65,7 @@ struct SvtParams {
   const int* warm;     // optional device flag: nonzero -> V holds a warm start
   int* sweeps_out;     // optional diagnostics: Jacobi sweeps used per matrix
   int q_cold, q_warm;  // subspace solver: iterations from a random / stored start
-  long long* phase_clk;  // optional diagnostics: 8 clock64 stamps per matrix
+  long long* phase_clk;  // optional diagnostics: kPhaseSlots clock64 stamps per matrix
   const int* only_flagged;  // full solver: nonzero pointer -> process only matrices whose
                             // fallback flag is set (fam[f].fallback)
   float rr_tol_rel, rr_tol_abs;  // subspace Rayleigh-Ritz rotation tolerances (0 = defaults)
@@ -78,6 +78,8 @@ struct SvtParams {
 
 // Dominant-subspace block size of the subspace SVT solver.
 constexpr int kSubspaceKB = 48;
+// clock64 diagnostics slots per matrix (SvtParams::phase_clk)
+constexpr int kPhaseSlots = 16;
 // Matrices with more than KB - margin singular values above the threshold
 // are redone by the full eigen-solver.
 constexpr int kSubspaceMargin = 8;

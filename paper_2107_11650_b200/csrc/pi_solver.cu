@@ -416,7 +416,7 @@ __global__ void k_cg_init_from_ap(const float2* __restrict__ bk, const float2* _
 
 // SPIRiT column stage on [M][N*J], tile of F = PPT*J fibres (PPT pixels):
 // v = iF0(tmp); w = P v per pixel; tmp2 = F0(w).
-__global__ void __launch_bounds__(256) k_spirit_cols(const float2* __restrict__ tmp,
+__global__ void __launch_bounds__(kFftThreads) k_spirit_cols(const float2* __restrict__ tmp,
                                                      float2* __restrict__ tmp2,
                                                      const float2* __restrict__ pm, FftTwiddles tw,
                                                      int N, int J, int PPT, const SolverCtl* ctl,
@@ -465,7 +465,7 @@ __global__ void __launch_bounds__(256) k_spirit_cols(const float2* __restrict__ 
 // SPIRiT row forward stage, one CTA per row m: v = F1(tmp2 row);
 // ap = dg p + lambda1 v.  mode 0: CG iteration (reduce denom, finalize alpha);
 // mode 1: initial residual (apply to x, store ap only).
-__global__ void __launch_bounds__(256) k_spirit_rows_fwd(const float2* __restrict__ tmp2,
+__global__ void __launch_bounds__(kFftThreads) k_spirit_rows_fwd(const float2* __restrict__ tmp2,
                                                          const float2* __restrict__ vec,
                                                          const float* __restrict__ dg,
                                                          float2* __restrict__ ap, FftTwiddles tw,
@@ -720,8 +720,8 @@ PiPlan::PiPlan(const PiConfig& cfg, const double* y, const uint8_t* mask, size_t
   if (const char* s = std::getenv("SHLR_RR_ABS")) rr_tol_abs_ = (float)std::atof(s);
   if (const char* s = std::getenv("SHLR_RR_TAIL")) rr_tail_ = (float)std::atof(s);
   if (std::getenv("SHLR_PHASE_CLK")) {
-    phase_clk_ = dalloc<long long>((size_t)(M + N) * 8);
-    SHLR_CUDA(cudaMemsetAsync(phase_clk_, 0, sizeof(long long) * 8 * (M + N), stream_));
+    phase_clk_ = dalloc<long long>((size_t)(M + N) * kPhaseSlots);
+    SHLR_CUDA(cudaMemsetAsync(phase_clk_, 0, sizeof(long long) * kPhaseSlots * (M + N), stream_));
   }
   if (cfg.debug_sv_iter > 0) {
     if (dr != dc) throw InvalidArg("debug singular values need equal row/column d");
@@ -821,15 +821,16 @@ void PiPlan::cg_apply_spirit(float2* in_vec, float2* out_ap, bool init) {
   launch_fft_axis<SpiritRowInvOp, true>(op1, tN_, M, J, J, stream_);
   ++launch_count_;
   // stage 2: columns
-  const int ppt = std::max(1, 16 / J);
+  static const int ppt_env = std::getenv("SHLR_SPIRIT_PPT") ? std::atoi(std::getenv("SHLR_SPIRIT_PPT")) : 0;
+  const int ppt = ppt_env > 0 ? ppt_env : std::max(1, 8 / J);
   const size_t smem2 = 2 * (size_t)M * ppt * J * sizeof(float2);
-  k_spirit_cols<<<(N + ppt - 1) / ppt, kThreads, smem2, stream_>>>(tmp_, tmp2_, pmat_, tM_, N, J, ppt,
+  k_spirit_cols<<<(N + ppt - 1) / ppt, kFftThreads, smem2, stream_>>>(tmp_, tmp2_, pmat_, tM_, N, J, ppt,
                                                                    ctl_, init ? 1 : 0);
   SHLR_LAUNCH_CHECK();
   ++launch_count_;
   // stage 3: row FFT + combine (+ alpha)
   const size_t smem3 = 2 * (size_t)N * J * sizeof(float2);
-  k_spirit_rows_fwd<<<M, kThreads, smem3, stream_>>>(tmp2_, init ? in_vec : p_, dg_, out_ap, tN_, J,
+  k_spirit_rows_fwd<<<M, kFftThreads, smem3, stream_>>>(tmp2_, init ? in_vec : p_, dg_, out_ap, tN_, J,
                                                      (float)cfg_.lambda1, ctl_, partials_, init ? 1 : 0);
   SHLR_LAUNCH_CHECK();
   ++launch_count_;
@@ -1107,7 +1108,7 @@ void hankel_svt_batched_device(const float2* vecs, int batch, int nc, int n, int
 }
 
 void PiPlan::debug_phases(long long* out, int n) {
-  const int total = (cfg_.M + cfg_.N) * 8;
+  const int total = (cfg_.M + cfg_.N) * kPhaseSlots;
   std::vector<long long> h(total, 0);
   if (phase_clk_) {
     SHLR_CUDA(cudaMemcpyAsync(h.data(), phase_clk_, total * sizeof(long long), cudaMemcpyDeviceToHost, stream_));
