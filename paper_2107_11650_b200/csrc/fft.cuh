@@ -179,6 +179,7 @@ __global__ void __launch_bounds__(kFftThreads) fft_axis_kernel(Op op, FftTwiddle
   float2* b = fft_smem + (size_t)n * F;
   const int o = blockIdx.y;
   const int i0 = blockIdx.x * F;
+#pragma unroll 4
   for (int t = threadIdx.x; t < n * F; t += blockDim.x) {
     const int f = t % F, k = t / F;
     const int i = i0 + f;

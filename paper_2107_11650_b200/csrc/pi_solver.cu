@@ -341,7 +341,29 @@ __global__ void k_cg_b(float2* __restrict__ x, float2* __restrict__ r, const flo
   if (halted(ctl) || ctl->cg.done) return;
   const float a = (float)ctl->cg.alpha;
   double s = 0.0;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nel; i += (size_t)gridDim.x * blockDim.x) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  if (ap && (nel & 1) == 0) {
+    // two complex elements per 16-byte access, two accesses in flight per
+    // operand and thread: the kernel is L2-latency bound
+    const size_t n2 = nel >> 1;
+    const float4* p4 = reinterpret_cast<const float4*>(p);
+    const float4* ap4 = reinterpret_cast<const float4*>(ap);
+    float4* x4 = reinterpret_cast<float4*>(x);
+    float4* r4 = reinterpret_cast<float4*>(r);
+#pragma unroll 2
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n2; i += stride) {
+      const float4 pv = p4[i], av = ap4[i];
+      float4 xv = x4[i], rv = r4[i];
+      xv.x = fmaf(a, pv.x, xv.x); xv.y = fmaf(a, pv.y, xv.y);
+      xv.z = fmaf(a, pv.z, xv.z); xv.w = fmaf(a, pv.w, xv.w);
+      rv.x = fmaf(-a, av.x, rv.x); rv.y = fmaf(-a, av.y, rv.y);
+      rv.z = fmaf(-a, av.z, rv.z); rv.w = fmaf(-a, av.w, rv.w);
+      x4[i] = xv;
+      r4[i] = rv;
+      s += ((double)rv.x * rv.x + (double)rv.y * rv.y) + ((double)rv.z * rv.z + (double)rv.w * rv.w);
+    }
+  } else
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nel; i += stride) {
     const float2 pv = p[i];
     float2 apv;
     if (ap) {
@@ -429,6 +451,7 @@ __global__ void __launch_bounds__(kFftThreads) k_spirit_cols(const float2* __res
   const int n0 = blockIdx.x * PPT;  // first pixel column of the tile
   float2* a = sm;
   float2* b = sm + (size_t)M * F;
+#pragma unroll 4
   for (int t = threadIdx.x; t < M * F; t += blockDim.x) {
     const int f = t % F, k = t / F;
     const int n = n0 + f / J;
@@ -438,20 +461,54 @@ __global__ void __launch_bounds__(kFftThreads) k_spirit_cols(const float2* __res
   float2* res = smem_centered_dft<true>(a, b, tw, F);
   float2* oth = res == a ? b : a;
   const float isn = rsqrtf((float)M);
-  // per-pixel matvec into the other buffer
-  for (int t = threadIdx.x; t < M * F; t += blockDim.x) {
-    const int f = t % F, k = t / F;
-    const int pl = f / J, ai = f % J;
-    const int n = n0 + pl;
-    float2 acc = make_float2(0.f, 0.f);
-    if (n < N) {
-      const float2* pp = pm + (((long long)k * N + n) * J + ai) * J;
-      const float2* vv = res + k * F + pl * J;
-      const float sc = centered_out_scale(k, M, tw.logn, isn);
-      for (int bi = 0; bi < J; ++bi) cfma(acc, __ldg(pp + bi), vv[bi]);
-      acc = cscale(acc, sc);
+  // per-pixel matvec into the other buffer.  P streams from L2 (33.5 MB at
+  // config 2): the 8-coil path issues the 16-byte loads of four outputs
+  // before consuming any, so each thread keeps 16 loads in flight.
+  if (J == 8 && PPT == 1) {
+    // one warp per pixel row k: the pixel's 8 x 8 P block (512 B) is one
+    // coalesced 16-byte load per lane (lane = 4 ai + q holds entries 2q, 2q+1
+    // of row ai); 4-lane shuffle reduction; 4 rows in flight per warp
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int ai = lane >> 2, q = lane & 3;
+    constexpr int UNR = 4;
+    for (int k0 = wid; k0 < M; k0 += nw * UNR) {
+      float4 pv[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const int k = k0 + u * nw;
+        if (k < M) pv[u] = __ldg(reinterpret_cast<const float4*>(pm + ((long long)k * N + n0) * 64) + lane);
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const int k = k0 + u * nw;
+        if (k < M) {
+          const float2* vv = res + k * 8;
+          float2 acc = make_float2(0.f, 0.f);
+          cfma(acc, make_float2(pv[u].x, pv[u].y), vv[2 * q]);
+          cfma(acc, make_float2(pv[u].z, pv[u].w), vv[2 * q + 1]);
+          acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 1);
+          acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 1);
+          acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 2);
+          acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 2);
+          if (q == 0) oth[k * 8 + ai] = cscale(acc, centered_out_scale(k, M, tw.logn, isn));
+        }
+      }
     }
-    oth[t] = acc;
+  } else {
+    for (int t = threadIdx.x; t < M * F; t += blockDim.x) {
+      const int f = t % F, k = t / F;
+      const int pl = f / J, ai = f % J;
+      const int n = n0 + pl;
+      float2 acc = make_float2(0.f, 0.f);
+      if (n < N) {
+        const float2* pp = pm + (((long long)k * N + n) * J + ai) * J;
+        const float2* vv = res + k * F + pl * J;
+        const float sc = centered_out_scale(k, M, tw.logn, isn);
+        for (int bi = 0; bi < J; ++bi) cfma(acc, __ldg(pp + bi), vv[bi]);
+        acc = cscale(acc, sc);
+      }
+      oth[t] = acc;
+    }
   }
   __syncthreads();
   float2* res2 = smem_centered_dft<false>(oth, res, tw, F);
@@ -480,11 +537,13 @@ __global__ void __launch_bounds__(kFftThreads) k_spirit_rows_fwd(const float2* _
   const int m = blockIdx.x;
   float2* a = sm;
   float2* b = sm + (size_t)N * F;
+#pragma unroll 4
   for (int t = threadIdx.x; t < N * F; t += blockDim.x) a[t] = tmp2[m * NJ + t];
   __syncthreads();
   float2* res = smem_centered_dft<false>(a, b, tw, F);
   const float isn = rsqrtf((float)N);
   double s = 0.0;
+#pragma unroll 4
   for (int t = threadIdx.x; t < N * F; t += blockDim.x) {
     const int k = t / F;
     const long long idx = m * NJ + t;
