@@ -157,7 +157,7 @@ __device__ __forceinline__ float2 lift_tab(const float2* wl, const int* lofs, bo
   return wide ? cconj(wl[lofs[i] + u]) : wl[lofs[u] + i];
 }
 
-template <int DP, int R>
+template <int DP, int CS, int R>
 __device__ __forceinline__ void build_chunk(float2* dst, const float2* wl, const int* lofs, const SvtFamily& F,
                                             const float2* dstage, int i0, int rows, float inv_beta) {
   const int d = F.d;
@@ -173,7 +173,7 @@ __device__ __forceinline__ void build_chunk(float2* dst, const float2* wl, const
         v.y = fmaf(dd.y, inv_beta, v.y);
       }
     }
-    dst[t] = v;
+    dst[r * CS + u] = v;
   }
 }
 
@@ -1414,6 +1414,7 @@ template <int DP, int KB, int R>
 __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams prm) {
   constexpr int NT = kSubNT;
   constexpr int KS = KB + 1;       // row stride of the d x KB blocks (conflict-free column walks)
+  constexpr int CS = DP + 1;       // row stride of the R x d chunk (odd: conflict-free anti-diagonal walks)
   constexpr int NC = KB / 16;      // 16-column groups
   constexpr int MR = (DP + 31) / 32;
   static_assert(KB % 16 == 0 && KB % 8 == 0, "KB must be a multiple of 16");
@@ -1430,8 +1431,8 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float2* V = reinterpret_cast<float2*>(smem_raw);  // DP x KS
   float2* X = V + DP * KS;                           // DP x KS (also H for the Ritz solve)
-  float2* C = X + DP * KS;                           // R x DP  (Ahat chunk / U / T)
-  float2* Yc = C + R * DP;                           // R x KS
+  float2* C = X + DP * KS;                           // R x CS  (Ahat chunk / U / T)
+  float2* Yc = C + R * CS;                           // R x KS
   float2* wl = Yc + R * KS;                          // B x len
   float2* acc = wl + B * len;                        // B x len
   float2* Yc2 = acc + B * len;                       // R x KS (second k-half of the chunk GEMM)
@@ -1523,11 +1524,11 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
       const int rows = min(R, e - i0);
       if (Dg) stage_d_wait();
       SUB_ACC(clk_wait);
-      build_chunk<DP, R>(C, wl, lofs, F, Dg ? X : nullptr, i0, rows, prm.inv_beta);
+      build_chunk<DP, CS, R>(C, wl, lofs, F, Dg ? X : nullptr, i0, rows, prm.inv_beta);
       __syncthreads();
       SUB_ACC(clk_build);
       if (Dg && i0 + R < e) stage_d_async(X, Dg, i0 + R, min(R, e - i0 - R), d);
-      chunk_times_block_split<DP, KS, NC>(C, V, Yc, Yc2, d);  // Yc = C V
+      chunk_times_block_split<CS, KS, NC>(C, V, Yc, Yc2, d);  // Yc = C V
       __syncthreads();
       SUB_ACC(clk_g1);
       sum_halves<KS, R>(Yc, Yc2, KB, nullptr);
@@ -1542,7 +1543,7 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
         for (int m = 0; m < MR; ++m) {
           const int k = yi + 32 * m;
           if (k < DP) {
-            const float2 a = C[i * DP + k];
+            const float2 a = C[i * CS + k];
 #pragma unroll
             for (int n = 0; n < NC; ++n) cfmac(xa[m][n], a, yv[n]);
           }
@@ -1607,10 +1608,10 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
     for (int i0 = 0; i0 < e; i0 += R) {
       const int rows = min(R, e - i0);
       if (Dg) stage_d_wait();
-      build_chunk<DP, R>(C, wl, lofs, F, Dg ? X : nullptr, i0, rows, prm.inv_beta);
+      build_chunk<DP, CS, R>(C, wl, lofs, F, Dg ? X : nullptr, i0, rows, prm.inv_beta);
       __syncthreads();
       if (Dg && i0 + R < e) stage_d_async(X, Dg, i0 + R, min(R, e - i0 - R), d);
-      chunk_times_block_split<DP, KS, NC>(C, V, Yc, Yc2, d);
+      chunk_times_block_split<CS, KS, NC>(C, V, Yc, Yc2, d);
       __syncthreads();
       sum_halves<KS, R>(Yc, Yc2, KB, nullptr);
       __syncthreads();
@@ -1753,15 +1754,15 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
   for (int i0 = 0; i0 < e; i0 += R) {
     const int rows = min(R, e - i0);
     if (Dg) stage_d_wait();
-    build_chunk<DP, R>(C, wl, lofs, F, Dg ? Ds : nullptr, i0, rows, prm.inv_beta);
+    build_chunk<DP, CS, R>(C, wl, lofs, F, Dg ? Ds : nullptr, i0, rows, prm.inv_beta);
     __syncthreads();
     {
       // only the first r (sorted) Ritz columns have f > 0
       static_assert(NC <= 3, "NC > 3 needs more cases");
       const int nb = (r + 15) >> 4;
-      if (nb <= 1) chunk_times_block_split<DP, KS, 1>(C, Vf, Yc, Yc2, d);
-      else if (nb == 2 || NC == 2) chunk_times_block_split<DP, KS, (NC >= 2 ? 2 : 1)>(C, Vf, Yc, Yc2, d);
-      else chunk_times_block_split<DP, KS, NC>(C, Vf, Yc, Yc2, d);
+      if (nb <= 1) chunk_times_block_split<CS, KS, 1>(C, Vf, Yc, Yc2, d);
+      else if (nb == 2 || NC == 2) chunk_times_block_split<CS, KS, (NC >= 2 ? 2 : 1)>(C, Vf, Yc, Yc2, d);
+      else chunk_times_block_split<CS, KS, NC>(C, Vf, Yc, Yc2, d);
       __syncthreads();
       sum_halves<KS, R>(Yc, Yc2, 16 * min(nb, NC), S.f);
     }
@@ -1795,7 +1796,7 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
             tv.x = fmaf(-dn.x, prm.inv_beta, z[m].x);
             tv.y = fmaf(-dn.y, prm.inv_beta, z[m].y);
           }
-          C[yi * DP + k] = tv;
+          C[yi * CS + k] = tv;
         }
       }
     }
@@ -1806,11 +1807,11 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
       float2 s = acc[o];
       if (!F.wide) {
         const int ilo = max(i0, n - F.q + 1), ihi = min(i0 + rows - 1, n);
-        for (int i = ilo; i <= ihi; ++i) s = cadd(s, C[(i - i0) * DP + b * F.q + (n - i)]);
+        for (int i = ilo; i <= ihi; ++i) s = cadd(s, C[(i - i0) * CS + b * F.q + (n - i)]);
       } else {
         const int tlo = max(max(0, i0 - b * F.q), n - F.P + 1);
         const int thi = min(min(F.q - 1, i0 + rows - 1 - b * F.q), n);
-        for (int t = tlo; t <= thi; ++t) s = cadd(s, cconj(C[(b * F.q + t - i0) * DP + (n - t)]));
+        for (int t = tlo; t <= thi; ++t) s = cadd(s, cconj(C[(b * F.q + t - i0) * CS + (n - t)]));
       }
       acc[o] = s;
     }
@@ -1839,7 +1840,7 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
 
 size_t svt_subspace_smem_bytes(int DP, int KB, int R, int maxB, int maxLen, int maxE) {
   const int KS = KB + 1;
-  return sizeof(float2) * (2ull * DP * KS + (size_t)R * DP + 2ull * R * KS + 2ull * maxB * maxLen) +
+  return sizeof(float2) * (2ull * DP * KS + (size_t)R * (DP + 1) + 2ull * R * KS + 2ull * maxB * maxLen) +
          sizeof(SlotRec) * KB + sizeof(double2) * KB + sizeof(double) * KB + 2 * sizeof(float) * KB +
          16 * sizeof(int) + sizeof(int) * KB + sizeof(int) * std::max(DP, maxE) + 64;
 }
