@@ -320,7 +320,7 @@ def gpu_arm(args, dist, rank, world, local):
                    "lifted_matrix": f"{p}x{j * k}", "matrices_per_step": m + n},
         "hankel_svt": {"matrices_per_s": (m + n) / (svt_ms * 1e-3), "kernel_ms": svt_ms,
                        "share_of_step": svt_ms / (t_max_ms / args.steps),
-                       "solver": "subspace iteration (block 48, 2 passes warm) + Rayleigh-Ritz Jacobi, "
+                       "solver": "subspace iteration (block 48; 1 pass per ADMM iteration warm, 6 cold) + Rayleigh-Ritz by tridiagonalisation/multisection, "
                                  "full two-stage Jacobi for matrices with > 40 singular values above tau"},
         "roofline": {"bound": "fp32", "achieved": achieved_tf, "peak": fp32_peak, "unit": "TFLOP/s",
                      "frac": achieved_tf / fp32_peak, "traffic": traffic,

@@ -84,7 +84,7 @@ class PiPlan {
   float2 *vrow_ = nullptr, *vcol_ = nullptr;  // SVT eigenvector stores (warm start)
   float2 *vsrow_ = nullptr, *vscol_ = nullptr;  // subspace-solver block stores (warm start)
   int* fallback_ = nullptr;                     // per-matrix subspace -> full fallback flags
-  int q_cold_ = 6, q_warm_ = 2;
+  int q_cold_ = 6, q_warm_ = 1;
   bool subspace_ = true;
   float rr_tol_rel_ = 0.f, rr_tol_abs_ = 0.f;  // 0 = kernel defaults
   float rr_tail_ = 0.f;

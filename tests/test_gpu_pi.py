@@ -53,6 +53,30 @@ def test_config1_scale_parity(gpu):
     assert [l.split()[2] for l in log] == [l.split()[2] for l in st.log]
 
 
+def test_config1_full_run_parity(gpu):
+    """BASELINE config 1 as specified: 30 ADMM iterations on the 128^2 x 8-coil
+    phantom, through the resident plan (CUDA graph, subspace SVT with warm
+    start), image within 1e-4 of the oracle; the stop-rule trace too."""
+    A = gpu
+    y0 = phantom(128, 128, 8)
+    mk = A.mask_gauss_cartesian(128, 0.25, 16, 11650)
+    y = np.where(mk.bits[0][None, :, None].astype(bool), y0, 0)
+    iters = 30
+    plan = A.PiPlan(y, mk, None, A.HankelConfig(pencil=120), A.AdmmConfig(max_outer=iters, tol=1e-300))
+    plan.run(iters)
+    plan.sync()
+    log = []
+    x, st = plan.download(log)
+    plan.close()
+    xo, sto = O.shlr_pi_reconstruct(y, O.SamplingMask(1, 128, mk.bits), None, O.HankelConfig(pencil=120),
+                                    O.AdmmConfig(max_outer=iters, tol=1e-300))
+    assert st.outer_iters == iters
+    assert rel(x, xo) < TOL
+    rc = np.array([float(l.split("relchange=")[1].split()[0]) for l in log])
+    rco = np.array([float(l.split("relchange=")[1].split()[0]) for l in sto.log])
+    np.testing.assert_allclose(rc[:10], rco[:10], rtol=1e-2)
+
+
 def test_bitwise_determinism_and_plan_reset(gpu):
     A = gpu
     y = phantom(32, 32, 4, seed=3)
