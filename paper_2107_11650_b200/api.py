@@ -256,11 +256,11 @@ class PiPlan:
         _check(lib.shlr_cuda_pi_plan_set_warm_start(self._h, int(on)), "plan_set_warm_start")
 
     def debug_phases(self) -> np.ndarray:
-        n = (self.shape[0] + self.shape[1]) * 16
+        n = (self.shape[0] + self.shape[1]) * 24
         out = np.zeros(n, np.int64)
         _check(lib.shlr_cuda_pi_plan_debug_phases(self._h, out.ctypes.data_as(C.POINTER(C.c_longlong)), n),
                "plan_debug_phases")
-        return out.reshape(-1, 16)
+        return out.reshape(-1, 24)
 
     def debug_sweeps(self) -> np.ndarray:
         n = self.shape[0] + self.shape[1]

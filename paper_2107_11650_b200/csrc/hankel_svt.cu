@@ -1646,7 +1646,8 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
   if (!prm.rr_jacobi) {
     SUB_STAMP(4);
     hermitian_eig_tridiag<KB, KS>(X, reinterpret_cast<float*>(S.rec), reinterpret_cast<float*>(C), C, S.dg,
-                                  0.25f * prm.thresh * prm.thresh);
+                                  0.25f * prm.thresh * prm.thresh,
+                                  prm.phase_clk ? prm.phase_clk + (long long)blockIdx.x * kPhaseSlots + 16 : nullptr);
     SUB_STAMP(5);
     if (prm.sweeps_out && tid == 0) prm.sweeps_out[blockIdx.x] = 0;
   } else {

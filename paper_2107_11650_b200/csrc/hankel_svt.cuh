@@ -79,7 +79,7 @@ struct SvtParams {
 // Dominant-subspace block size of the subspace SVT solver.
 constexpr int kSubspaceKB = 48;
 // clock64 diagnostics slots per matrix (SvtParams::phase_clk)
-constexpr int kPhaseSlots = 16;
+constexpr int kPhaseSlots = 24;
 // Matrices with more than KB - margin singular values above the threshold
 // are redone by the full eigen-solver.
 constexpr int kSubspaceMargin = 8;

@@ -26,6 +26,8 @@ if os.environ.get("SHLR_PHASE_CLK"):
     print(f"phase kcycles (mean over {ok.sum()} matrices): start {d(0,3).mean():.0f} [pass {ph[ok,1].mean()/1e3:.0f} qr {ph[ok,2].mean()/1e3:.0f}] "
           f"H-pass {d(3,4).mean():.0f} RR-jacobi {d(4,5).mean():.0f} VU {d(5,6).mean():.0f} Z-pass {d(6,7).mean():.0f} total {d(0,7).mean():.0f}")
     print("pass split kcycles: wait %.0f build %.0f gemm1 %.0f sum %.0f gemm2 %.0f" % tuple(ph[ok, 8 + i].mean() / 1e3 for i in range(5)))
+    e = [(ph[ok, 17 + i] - ph[ok, 16 + i]).mean() / 1e3 for i in range(6)]
+    print("RR split kcycles: tridiag %.0f similarity %.0f bisection %.0f twisted+clusters %.0f mgs %.0f backtransform %.0f" % tuple(e))
     tot = d(0, 7)
     print("total kcycles percentiles 50/90/99/max:", np.percentile(tot, [50, 90, 99]).round(0), tot.max().round(0),
           "| RR max", d(4, 5).max().round(0), "| matrices stamped", int(ok.sum()))
