@@ -68,6 +68,41 @@ def svt_case(name, b, nc, n, p, tau, seed):
     np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
 
 
+def param_masks(n, l, rate, acs, seed):
+    """N x L parameter-imaging mask: echo e's column is mask_gauss_cartesian(n, rate, acs,
+    seed + e) from the reference's own generator (SURVEY 8 mapping table, config 4)."""
+    cols = []
+    with tempfile.TemporaryDirectory() as tmp:
+        for e in range(l):
+            run(["mask", "kind=gauss", f"n={n}", f"rate={rate!r}", f"acs={acs}", f"seed={seed + e}",
+                 "out=m.cplx"], tmp)
+            cols.append(read_cplx(os.path.join(tmp, "m.cplx")).real.astype(np.uint8).reshape(-1))
+    return np.stack(cols, axis=1)
+
+
+def param_case(name, shape, vc, seed, max_outer=4, pencil=0, pencil_param=0, tol=1e-300, rate=0.4,
+               acs=4, extra=()):
+    """shape (N, L, J) -> shlr_param_reconstruct_slice; (M, N, L, J) -> recon_param_dataset."""
+    rng = np.random.default_rng(seed)
+    y = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+    n, l = shape[-3], shape[-2]
+    bits = param_masks(n, l, rate, acs, seed)
+    with tempfile.TemporaryDirectory() as tmp:
+        write_cplx(y, os.path.join(tmp, "y.cplx"))
+        write_mask(bits, os.path.join(tmp, "m.cplx"))
+        args = ["param", "y=y.cplx", "mask=m.cplx", "out=o", f"vc={int(vc)}", f"pencil={pencil}",
+                f"pencil_param={pencil_param}", f"max_outer={max_outer}", f"tol={tol!r}"] + list(extra)
+        run(args, tmp)
+        stats = dict(ln.split("=", 1) for ln in open(os.path.join(tmp, "o.stats")).read().split()
+                     if "=" in ln)
+        out = dict(y=y, mask=bits, pencil=pencil, pencil_param=pencil_param, vc=vc, max_outer=max_outer,
+                   tol=tol, seed=seed, extra=np.array(list(extra), dtype=object),
+                   x=read_cplx(os.path.join(tmp, "o.x.cplx")),
+                   log=np.array(open(os.path.join(tmp, "o.log")).read().splitlines()),
+                   outer_iters=int(stats.get("outer_iters", -1)))
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+
+
 def mask_case():
     specs = [("gauss", 256, 0.2, 24, 11650), ("gauss", 128, 0.25, 16, 11650),
              ("gauss", 256, 0.34, 22, 42), ("gauss", 256, 1.0 / 6.0, 16, 11651),
@@ -85,6 +120,8 @@ def mask_case():
 def main():
     if not os.path.exists(DRIVER):
         raise SystemExit("build oracle/_ref first (make -C oracle)")
+    if sys.argv[1:] == ["param"]:
+        return param_cases()
     for vc in (0, 1):
         for sp in (0, 1):
             pi_case(f"pi_24x24x3_p9_vc{vc}_s{sp}", 24, 24, 3, 9, vc, sp, seed=10 + 2 * vc + sp)
@@ -97,7 +134,19 @@ def main():
     svt_case("svt_wide_64_4_p20", 5, 4, 64, 20, 6.0, seed=32)
     svt_case("svt_120x120_sq", 4, 8, 134, 120, 20.0, seed=33)
     mask_case()
+    param_cases()
     print("golden fixtures written to", HERE)
+
+
+def param_cases():
+    param_case("param_slice_24x8x2_vc0", (24, 8, 2), 0, seed=41, pencil=17)
+    param_case("param_slice_24x8x2_vc1", (24, 8, 2), 1, seed=42, pencil=17)
+    param_case("param_slice_20x12x3_default", (20, 12, 3), 1, seed=43, max_outer=3)
+    param_case("param_slice_16x9x2_early_stop", (16, 9, 2), 0, seed=44, max_outer=40, tol=1e-3,
+               pencil=11)
+    param_case("param_dataset_5x20x9x2_vc1", (5, 20, 9, 2), 1, seed=45, max_outer=3, pencil=14)
+    param_case("param_dataset_4x16x10x2_stop", (4, 16, 10, 2), 0, seed=46, max_outer=30, tol=2e-3,
+               pencil=11, extra=("lambda2=0.5",))
 
 
 if __name__ == "__main__":
