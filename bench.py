@@ -68,6 +68,33 @@ def make_inputs(cfg=CFG2):
     return y, mask, g, hcfg
 
 
+CFG4 = dict(M=256, N=256, L=12, J=4, K=13, rate=1.0 / 6.0, acs=16, vc=True, lam=1e4, lambda2=2.0,
+            beta=1.0, tau=1.0, cg_max=15, cg_tol=1e-8, outer=50)
+WORKLOAD4 = ("config4: T2 mapping 256x256, 4 coils, 12 echoes (TE=10e ms), SHLR-VP (virtual coils), "
+             "per-echo R=6 Gaussian Cartesian masks (16 ACS lines, seed 11650+e), Hankel window K=13 "
+             "(PE lift 244x104: 3072 per iter; echo lift 5x32: 65536 per iter), lambda2=2, "
+             "256 FE slices batched, 50 outer iterations")
+
+
+def make_param_inputs(cfg=CFG4, m=None):
+    """Config 4 (BASELINE.json configs[3]): seeded T2 phantom k-space (M, N, L, J),
+    the N x L per-echo mask (column e = mask_gauss_cartesian(N, 1/6, acs, 11650 + e),
+    SURVEY 8 mapping table), zero-filled, plus the configs."""
+    from paper_2107_11650_b200 import api as A
+    from paper_2107_11650_b200 import synth
+    M = m or cfg["M"]
+    _, k, tes, _ = synth.t2_phantom(M, cfg["N"], cfg["J"], cfg["L"])
+    bits = np.stack([A.mask_gauss_cartesian(cfg["N"], cfg["rate"], cfg["acs"], synth.SEED_MASK + e).bits[0]
+                     for e in range(cfg["L"])], axis=1)
+    mask = A.SamplingMask(cfg["N"], cfg["L"], bits, "gauss_cartesian", synth.SEED_MASK, cfg["rate"], cfg["acs"])
+    y = np.where(bits[None, :, :, None].astype(bool), k, 0)
+    hcfg = A.HankelConfig(pencil=cfg["N"] - cfg["K"] + 1)
+    acfg = A.AdmmConfig(lam=cfg["lam"], lambda2=cfg["lambda2"], beta=cfg["beta"], tau=cfg["tau"],
+                        max_outer=cfg["outer"], tol=1e-300, cg_max=cfg["cg_max"], cg_tol=cfg["cg_tol"],
+                        enable_vc=cfg["vc"])
+    return A.ParameterDataset(y, list(tes)), mask, hcfg, acfg
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 

@@ -121,6 +121,55 @@ int shlr_cuda_pi_plan_download(shlr_pi_plan* plan, double* x_out, shlr_stats* st
                                shlr_log_fn log_cb, void* log_ctx);
 void shlr_cuda_pi_plan_destroy(shlr_pi_plan* plan);
 
+/* ------------------------------------------------------------------------
+ * Parameter imaging (SHLR-P / SHLR-VP, Algorithm S2).
+ *
+ * Arguments of shlr_param_reconstruct_slice (proj/include/shlr/solvers.hpp:74-79)
+ * and recon_param_dataset (proj/include/shlr/parammap.hpp:35-40) after the
+ * host-side validation the reference does (solvers.cpp:199-206,
+ * parammap.cpp:27-30).  Pencils are resolved with HankelConfig::pencil_for(n)
+ * and HankelConfig::pencil_for_param(l) (proj/src/hankel.cpp:10-29).
+ *   m == 0: y is one N x L x J slice (FE image, PE k-space), the input of
+ *           shlr_param_reconstruct_slice;
+ *   m >= 1: y is an M x N x L x J dataset (k-space in FE and PE), the input
+ *           of recon_param_dataset: iFFT along FE, then every FE slice is an
+ *           independent ADMM with its own early stop -- all of them run
+ *           batched on the device.
+ * mask is N x L (row = phase encode, column = echo). */
+typedef struct shlr_param_args {
+  size_t m, n, l, j;
+  const double* y;             /* interleaved complex                          */
+  const uint8_t* mask;         /* n x l                                        */
+  const double* taps;          /* HankelConfig::filter_taps, interleaved       */
+  size_t ntaps;
+  size_t pencil_pe, pencil_par;
+  double lambda, lambda2, beta, tau, tol, cg_tol;
+  size_t max_outer, cg_max;
+  int enable_vc;
+} shlr_param_args;
+
+/* Full parameter reconstruction, host buffers in and out.  x_out: (m ? m : 1)
+ * x n x l x j interleaved complex (image domain along FE and PE, like the
+ * reference).  stats (nullable): for a slice, SolveStats of the slice; for a
+ * dataset, outer_iters = total outer iterations over all slices (the
+ * reference's *total_iters, parammap.cpp:52) and final_rel_change of the last
+ * slice.  log_cb receives every slice's per-iteration lines in slice order. */
+int shlr_cuda_param_reconstruct(const shlr_param_args* args, double* x_out, shlr_stats* stats,
+                                shlr_log_fn log_cb, void* log_ctx);
+
+/* Resident-plan API of the parameter path (same contract as the PI plan). */
+typedef struct shlr_param_plan shlr_param_plan;
+int shlr_cuda_param_plan_create(const shlr_param_args* args, shlr_param_plan** out);
+int shlr_cuda_param_plan_reset(shlr_param_plan* plan);
+int shlr_cuda_param_plan_run(shlr_param_plan* plan, size_t iters);
+int shlr_cuda_param_plan_sync(shlr_param_plan* plan);
+int shlr_cuda_param_plan_set_timing(shlr_param_plan* plan, int on);
+int shlr_cuda_param_plan_timing(shlr_param_plan* plan, double* svt_ms, double* total_ms,
+                                int* launches_per_iter);
+int shlr_cuda_param_plan_download(shlr_param_plan* plan, double* x_out, shlr_stats* stats,
+                                  shlr_log_fn log_cb, void* log_ctx);
+void shlr_cuda_param_plan_destroy(shlr_param_plan* plan);
+
 /* Batched Hankel-SVT unit (BASELINE config 5): for each of `batch` matrices,
  * lift_plain (proj/src/operators.cpp:93-103) the nc vectors of length n with
  * pencil p, svt with threshold tau (solvers.cpp:11-21), adjoint_lift_plain
@@ -167,6 +216,8 @@ int shlr_mask_random2d(size_t rows, size_t cols, double rate, size_t center,
                        uint64_t seed, uint8_t* bits_out);
 int shlr_acs_range(size_t n, size_t acs, size_t* start, size_t* end);
 size_t shlr_pencil_for(size_t pencil, size_t len);
+/* HankelConfig::pencil_for_param (proj/src/hankel.cpp:20-29); 0 = invalid. */
+size_t shlr_pencil_for_param(size_t pencil_param, size_t len);
 /* SPIRiT kernel calibration (proj/src/spirit.cpp:22-94) on an a x b x j ACS
  * block (interleaved complex, row-major): the Tikhonov filter
  * s / (s^2 + mu^2), mu = tikhonov * s_max, computed as the equivalent ridge

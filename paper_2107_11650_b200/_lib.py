@@ -39,6 +39,21 @@ class ShlrPiArgs(C.Structure):
     ]
 
 
+class ShlrParamArgs(C.Structure):
+    _fields_ = [
+        ("m", C.c_size_t), ("n", C.c_size_t), ("l", C.c_size_t), ("j", C.c_size_t),
+        ("y", C.POINTER(C.c_double)),
+        ("mask", C.POINTER(C.c_uint8)),
+        ("taps", C.POINTER(C.c_double)),
+        ("ntaps", C.c_size_t),
+        ("pencil_pe", C.c_size_t), ("pencil_par", C.c_size_t),
+        ("lam", C.c_double), ("lambda2", C.c_double), ("beta", C.c_double),
+        ("tau", C.c_double), ("tol", C.c_double), ("cg_tol", C.c_double),
+        ("max_outer", C.c_size_t), ("cg_max", C.c_size_t),
+        ("enable_vc", C.c_int),
+    ]
+
+
 class ShlrStats(C.Structure):
     _fields_ = [("outer_iters", C.c_size_t), ("final_rel_change", C.c_double)]
 
@@ -65,6 +80,18 @@ PROTOTYPES = {
     "shlr_cuda_pi_plan_set_warm_start": (C.c_int, [C.c_void_p, C.c_int]),
     "shlr_cuda_pi_plan_debug_sweeps": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.c_int]),
     "shlr_cuda_pi_plan_debug_phases": (C.c_int, [C.c_void_p, C.POINTER(C.c_longlong), C.c_int]),
+    "shlr_cuda_param_reconstruct": (C.c_int, [C.POINTER(ShlrParamArgs), C.POINTER(C.c_double),
+                                              C.POINTER(ShlrStats), LOG_FN, C.c_void_p]),
+    "shlr_cuda_param_plan_create": (C.c_int, [C.POINTER(ShlrParamArgs), C.POINTER(C.c_void_p)]),
+    "shlr_cuda_param_plan_reset": (C.c_int, [C.c_void_p]),
+    "shlr_cuda_param_plan_run": (C.c_int, [C.c_void_p, C.c_size_t]),
+    "shlr_cuda_param_plan_sync": (C.c_int, [C.c_void_p]),
+    "shlr_cuda_param_plan_set_timing": (C.c_int, [C.c_void_p, C.c_int]),
+    "shlr_cuda_param_plan_timing": (C.c_int, [C.c_void_p, C.POINTER(C.c_double),
+                                              C.POINTER(C.c_double), C.POINTER(C.c_int)]),
+    "shlr_cuda_param_plan_download": (C.c_int, [C.c_void_p, C.POINTER(C.c_double),
+                                                C.POINTER(ShlrStats), LOG_FN, C.c_void_p]),
+    "shlr_cuda_param_plan_destroy": (None, [C.c_void_p]),
     "shlr_cuda_fp32_peak_tflops": (C.c_int, [C.POINTER(C.c_double)]),
     "shlr_cuda_hankel_svt_batched": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
                                                C.c_float, C.c_void_p, C.c_void_p, C.c_void_p]),
@@ -84,6 +111,7 @@ PROTOTYPES = {
     "shlr_acs_range": (C.c_int, [C.c_size_t, C.c_size_t, C.POINTER(C.c_size_t),
                                  C.POINTER(C.c_size_t)]),
     "shlr_pencil_for": (C.c_size_t, [C.c_size_t, C.c_size_t]),
+    "shlr_pencil_for_param": (C.c_size_t, [C.c_size_t, C.c_size_t]),
     "shlr_spirit_calibrate": (C.c_int, [C.POINTER(C.c_double), C.c_size_t, C.c_size_t, C.c_size_t,
                                         C.c_size_t, C.c_double, C.POINTER(C.c_double)]),
 }

@@ -10,6 +10,9 @@ Same names, argument meaning and error behaviour as ``proj/include/shlr``:
 * ``shlr_pi_reconstruct`` -- ``solvers.hpp:64-70``; raises ``ValueError``
   where the reference throws ``std::invalid_argument`` and
   ``DivergenceError`` for ``shlr::DivergenceError``.
+* ``shlr_param_reconstruct_slice`` -- ``solvers.hpp:74-79`` and
+  ``recon_param_dataset`` / ``ParameterDataset`` -- ``parammap.hpp:11-40``
+  (all FE slices of a dataset run batched on the device).
 * ``hankel_svt_batched`` -- the config-5 lift_plain -> svt -> adjoint unit.
 
 Everything numerical runs in ``lib/libshlr_b200.so`` on the GPU; this module
@@ -24,8 +27,8 @@ from typing import Callable, List, Optional, Sequence, Tuple
 
 import numpy as np
 
-from ._lib import (LOG_FN, SHLR_EDIVERGE, SHLR_EINVAL, SHLR_EUNSUPPORTED, SHLR_OK, ShlrPiArgs,
-                   ShlrStats, last_error, lib)
+from ._lib import (LOG_FN, SHLR_EDIVERGE, SHLR_EINVAL, SHLR_EUNSUPPORTED, SHLR_OK, ShlrParamArgs,
+                   ShlrPiArgs, ShlrStats, last_error, lib)
 
 
 class DivergenceError(RuntimeError):
@@ -64,6 +67,12 @@ class HankelConfig:
         p = int(lib.shlr_pencil_for(self.pencil, length))
         if p == 0:
             raise ValueError("HankelConfig: pencil exceeds signal length")
+        return p
+
+    def pencil_for_param(self, length: int) -> int:
+        p = int(lib.shlr_pencil_for_param(self.pencil_param, length))
+        if p == 0:
+            raise ValueError("HankelConfig: parameter pencil exceeds signal length")
         return p
 
 
@@ -292,6 +301,159 @@ class PiPlan:
     def close(self):
         if self._h:
             lib.shlr_cuda_pi_plan_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ---------------------------------------------------------------- parameter imaging
+@dataclass
+class ParameterDataset:
+    """``shlr::ParameterDataset`` (``parammap.hpp:11-20``): data M x N x L x J
+    (FE x PE x echoes x coils) plus the echo times in ms."""
+    data: np.ndarray
+    tes_ms: Sequence[float] = ()
+
+    def validate(self) -> None:  # parammap.cpp:10-19
+        if np.ndim(self.data) != 4:
+            raise ValueError("ParameterDataset: expected M x N x L x J")
+        if len(self.tes_ms) != np.shape(self.data)[2]:
+            raise ValueError("ParameterDataset: TE count != L")
+        for i, t in enumerate(self.tes_ms):
+            if t <= 0 or (i > 0 and t <= self.tes_ms[i - 1]):
+                raise ValueError("ParameterDataset: TEs must be positive and strictly increasing")
+
+
+def _param_args(y: np.ndarray, dataset: bool, mask: SamplingMask, hcfg: HankelConfig,
+                acfg: AdmmConfig, keep: list) -> ShlrParamArgs:
+    acfg.validate()
+    if dataset:
+        m, n, l, j = y.shape
+    else:
+        if y.ndim != 3:
+            raise ValueError("shlr_param_reconstruct_slice: expected N x L x J")
+        m, (n, l, j) = 0, y.shape
+    if mask.rows != n or mask.cols != l:
+        raise ValueError(("recon_param_dataset" if dataset else "shlr_param_reconstruct_slice")
+                         + ": mask dims mismatch")
+    yc = _c128(y)
+    bits = np.ascontiguousarray(np.asarray(mask.bits).reshape(n, l), dtype=np.uint8)
+    taps = _c128(list(hcfg.filter_taps))
+    keep += [yc, bits, taps]
+    a = ShlrParamArgs()
+    a.m, a.n, a.l, a.j = m, n, l, j
+    a.y = _dptr(yc)
+    a.mask = bits.ctypes.data_as(C.POINTER(C.c_uint8))
+    a.taps = _dptr(taps)
+    a.ntaps = len(hcfg.filter_taps)
+    a.pencil_pe = hcfg.pencil_for(n)
+    a.pencil_par = hcfg.pencil_for_param(l)
+    a.lam, a.lambda2, a.beta, a.tau = acfg.lam, acfg.lambda2, acfg.beta, acfg.tau
+    a.tol, a.cg_tol = acfg.tol, acfg.cg_tol
+    a.max_outer, a.cg_max = acfg.max_outer, acfg.cg_max
+    a.enable_vc = int(acfg.enable_vc)
+    return a
+
+
+def _run_param(a: ShlrParamArgs, out_shape, log, what: str):
+    x = np.empty(out_shape, np.complex128)
+    st = ShlrStats()
+    lines: List[str] = []
+
+    @LOG_FN
+    def _cb(_ctx, line):
+        lines.append(line.decode())
+
+    rc = lib.shlr_cuda_param_reconstruct(C.byref(a), _dptr(x), C.byref(st), _cb, None)
+    if log is not None:
+        log.extend(lines)
+    _check(rc, what)
+    return x, st
+
+
+def shlr_param_reconstruct_slice(y_m: np.ndarray, mask: SamplingMask, hcfg: HankelConfig,
+                                 acfg: AdmmConfig, log: Optional[List[str]] = None,
+                                 stats: Optional[SolveStats] = None) -> np.ndarray:
+    """``shlr::shlr_param_reconstruct_slice`` (``solvers.hpp:74-79``) on the GPU:
+    y_m is the zero-filled N x L x J plane at one FE position."""
+    keep: list = []
+    a = _param_args(np.asarray(y_m), False, mask, hcfg, acfg, keep)
+    x, st = _run_param(a, np.shape(y_m), log, "shlr_param_reconstruct_slice")
+    if stats is not None:
+        stats.outer_iters = int(st.outer_iters)
+        stats.final_rel_change = float(st.final_rel_change)
+    return x
+
+
+def recon_param_dataset(y: ParameterDataset, mask: SamplingMask, hcfg: HankelConfig,
+                        acfg: AdmmConfig, log: Optional[List[str]] = None,
+                        total_iters: Optional[List[int]] = None) -> ParameterDataset:
+    """``shlr::recon_param_dataset`` (``parammap.hpp:35-40``): iFFT along FE, then
+    every FE slice's ADMM (each with its own early stop) -- all slices batched
+    on the device.  ``total_iters`` (a list) receives the summed outer
+    iterations, the reference's ``*total_iters``."""
+    y.validate()
+    keep: list = []
+    data = np.asarray(y.data)
+    if mask.rows != data.shape[1] or mask.cols != data.shape[2]:
+        raise ValueError("recon_param_dataset: mask dims mismatch")
+    a = _param_args(data, True, mask, hcfg, acfg, keep)
+    x, st = _run_param(a, data.shape, log, "recon_param_dataset")
+    if total_iters is not None:
+        total_iters.append(int(st.outer_iters))
+    return ParameterDataset(x, list(y.tes_ms))
+
+
+class ParamPlan:
+    """Resident plan of the parameter path (``shlr_cuda_param_plan_*``)."""
+
+    def __init__(self, y, mask, hcfg, acfg, dataset: bool = True):
+        self._keep: list = []
+        y = np.asarray(y)
+        self._args = _param_args(y, dataset, mask, hcfg, acfg, self._keep)
+        self.shape = y.shape
+        self._h = C.c_void_p()
+        _check(lib.shlr_cuda_param_plan_create(C.byref(self._args), C.byref(self._h)), "plan_create")
+
+    def reset(self):
+        _check(lib.shlr_cuda_param_plan_reset(self._h), "plan_reset")
+
+    def run(self, iters: int):
+        _check(lib.shlr_cuda_param_plan_run(self._h, iters), "plan_run")
+
+    def sync(self):
+        _check(lib.shlr_cuda_param_plan_sync(self._h), "plan_sync")
+
+    def set_timing(self, on: bool):
+        _check(lib.shlr_cuda_param_plan_set_timing(self._h, int(on)), "plan_set_timing")
+
+    def timing(self):
+        s, t, n = C.c_double(), C.c_double(), C.c_int()
+        _check(lib.shlr_cuda_param_plan_timing(self._h, C.byref(s), C.byref(t), C.byref(n)), "timing")
+        return s.value, t.value, n.value
+
+    def download(self, log: Optional[List[str]] = None) -> Tuple[np.ndarray, SolveStats]:
+        x = np.empty(self.shape, np.complex128)
+        st = ShlrStats()
+        lines: List[str] = []
+
+        @LOG_FN
+        def _cb(_ctx, line):
+            lines.append(line.decode())
+
+        rc = lib.shlr_cuda_param_plan_download(self._h, _dptr(x), C.byref(st), _cb, None)
+        if log is not None:
+            log.extend(lines)
+        _check(rc, "plan_download")
+        return x, SolveStats(int(st.outer_iters), float(st.final_rel_change))
+
+    def close(self):
+        if self._h:
+            lib.shlr_cuda_param_plan_destroy(self._h)
             self._h = C.c_void_p()
 
     def __del__(self):

@@ -6,6 +6,7 @@
 #include <vector>
 
 #include "../../include/shlr_cuda.h"
+#include "param_solver.cuh"
 #include "pi_solver.cuh"
 
 namespace {
@@ -86,7 +87,51 @@ shlr_b200::PiConfig config_of(const shlr_pi_args* a) {
   return c;
 }
 
+// Mirrors AdmmConfig::validate and the checks of shlr_param_reconstruct_slice
+// (solvers.cpp:199-206) / recon_param_dataset (parammap.cpp:27-30).
+void validate_param(const shlr_param_args* a) {
+  using shlr_b200::InvalidArg;
+  if (!a) throw InvalidArg("shlr_param_reconstruct_slice: null args");
+  if (a->lambda <= 0 || a->lambda2 < 0 || a->beta <= 0 || a->tau <= 0 || a->tol <= 0 ||
+      a->cg_tol <= 0)
+    throw InvalidArg("AdmmConfig: invalid parameter");
+  if (a->n == 0 || a->l == 0 || a->j == 0 || !a->y)
+    throw InvalidArg("shlr_param_reconstruct_slice: expected N x L x J");
+  if (!a->mask) throw InvalidArg("shlr_param_reconstruct_slice: mask dims mismatch");
+  if (a->pencil_pe < 1 || a->pencil_pe > a->n)
+    throw InvalidArg("HankelConfig: pencil exceeds signal length");
+  if (a->pencil_par < 1 || a->pencil_par > a->l)
+    throw InvalidArg("HankelConfig: parameter pencil exceeds signal length");
+  if (!a->taps || a->ntaps == 0 || a->ntaps > a->n)
+    throw InvalidArg("weights_from_filter: taps invalid");
+}
+
+shlr_b200::ParamConfig param_config_of(const shlr_param_args* a) {
+  shlr_b200::ParamConfig c{};
+  c.S = a->m ? (int)a->m : 1;
+  c.dataset = a->m != 0;
+  c.N = (int)a->n;
+  c.L = (int)a->l;
+  c.J = (int)a->j;
+  c.Ppe = (int)a->pencil_pe;
+  c.Ppar = (int)a->pencil_par;
+  c.vc = a->enable_vc != 0;
+  c.lambda = a->lambda;
+  c.lambda2 = a->lambda2;
+  c.beta = a->beta;
+  c.tau = a->tau;
+  c.tol = a->tol;
+  c.cg_tol = a->cg_tol;
+  c.max_outer = (int)a->max_outer;
+  c.cg_max = (int)a->cg_max;
+  return c;
+}
+
 }  // namespace
+
+struct shlr_param_plan {
+  shlr_b200::ParamPlan* impl;
+};
 
 struct shlr_pi_plan {
   shlr_b200::PiPlan* impl;
@@ -324,6 +369,104 @@ int shlr_cuda_fft_along_axis(double* data, const size_t* dims, int ndim, int axi
     shlr_b200::fft_along_axis_host(data, dims, ndim, axis, inverse != 0);
     return SHLR_OK;
   });
+}
+
+int shlr_cuda_param_plan_create(const shlr_param_args* args, shlr_param_plan** out) {
+  return guarded([&] {
+    validate_param(args);
+    if (!out) throw shlr_b200::InvalidArg("null plan pointer");
+    require_device();
+    auto* impl = new shlr_b200::ParamPlan(param_config_of(args), args->y, args->mask, args->taps,
+                                          args->ntaps);
+    *out = new shlr_param_plan{impl};
+    return SHLR_OK;
+  });
+}
+
+int shlr_cuda_param_plan_reset(shlr_param_plan* plan) {
+  return guarded([&] {
+    if (!plan) throw shlr_b200::InvalidArg("null plan");
+    plan->impl->reset();
+    return SHLR_OK;
+  });
+}
+
+int shlr_cuda_param_plan_run(shlr_param_plan* plan, size_t iters) {
+  return guarded([&] {
+    if (!plan) throw shlr_b200::InvalidArg("null plan");
+    plan->impl->run(iters);
+    return SHLR_OK;
+  });
+}
+
+int shlr_cuda_param_plan_sync(shlr_param_plan* plan) {
+  return guarded([&] {
+    if (!plan) throw shlr_b200::InvalidArg("null plan");
+    plan->impl->sync();
+    return SHLR_OK;
+  });
+}
+
+int shlr_cuda_param_plan_set_timing(shlr_param_plan* plan, int on) {
+  return guarded([&] {
+    if (!plan) throw shlr_b200::InvalidArg("null plan");
+    plan->impl->set_timing(on != 0);
+    return SHLR_OK;
+  });
+}
+
+int shlr_cuda_param_plan_timing(shlr_param_plan* plan, double* svt_ms, double* total_ms,
+                                int* launches_per_iter) {
+  return guarded([&] {
+    if (!plan) throw shlr_b200::InvalidArg("null plan");
+    if (svt_ms) *svt_ms = plan->impl->svt_ms();
+    if (total_ms) *total_ms = plan->impl->total_ms();
+    if (launches_per_iter) *launches_per_iter = plan->impl->launches_per_iter();
+    return SHLR_OK;
+  });
+}
+
+int shlr_cuda_param_plan_download(shlr_param_plan* plan, double* x_out, shlr_stats* stats,
+                                  shlr_log_fn log_cb, void* log_ctx) {
+  return guarded([&] {
+    if (!plan || !x_out) throw shlr_b200::InvalidArg("null plan/output");
+    std::vector<int> outer;
+    std::vector<double> rel;
+    std::vector<std::string> lines;
+    int err = 0;
+    plan->impl->download(x_out, &outer, &rel, &lines, &err);
+    if (log_cb)
+      for (const auto& l : lines) log_cb(log_ctx, l.c_str());
+    if (stats) {
+      size_t total = 0;
+      for (int o : outer) total += (size_t)o;
+      stats->outer_iters = total;
+      stats->final_rel_change = rel.empty() ? 1.0 : rel.back();
+    }
+    if (err == 1) return fail(SHLR_EDIVERGE, "cg_solve: non-finite residual");
+    if (err == 2) return fail(SHLR_EDIVERGE, "cg_solve: operator not positive definite");
+    return SHLR_OK;
+  });
+}
+
+void shlr_cuda_param_plan_destroy(shlr_param_plan* plan) {
+  if (!plan) return;
+  delete plan->impl;
+  delete plan;
+}
+
+int shlr_cuda_param_reconstruct(const shlr_param_args* args, double* x_out, shlr_stats* stats,
+                                shlr_log_fn log_cb, void* log_ctx) {
+  shlr_param_plan* plan = nullptr;
+  int rc = shlr_cuda_param_plan_create(args, &plan);
+  if (rc != SHLR_OK) return rc;
+  rc = shlr_cuda_param_plan_run(plan, args->max_outer);
+  if (rc == SHLR_OK) rc = shlr_cuda_param_plan_sync(plan);
+  if (rc == SHLR_OK) rc = shlr_cuda_param_plan_download(plan, x_out, stats, log_cb, log_ctx);
+  std::string err = g_last_error;
+  shlr_cuda_param_plan_destroy(plan);
+  g_last_error = err;
+  return rc;
 }
 
 }  // extern "C"

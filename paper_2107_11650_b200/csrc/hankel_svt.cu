@@ -581,6 +581,7 @@ __global__ void __maxnreg__(svt_max_regs(DP)) hankel_svt_kernel(const SvtParams 
   if (prm.skip && *prm.skip) return;
   int mat;
   const SvtFamily& F = family_of(prm, blockIdx.x, mat);
+  if (F.halt && F.halt[mat / F.halt_div]) return;
   if (prm.only_flagged && !F.fallback[mat]) return;
   const int tid = threadIdx.x;
   const int d = F.d, e = F.e, len = F.len, B = F.B, J = F.J;
@@ -1423,6 +1424,7 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
   if (prm.skip && *prm.skip) return;
   int mat;
   const SvtFamily& F = family_of(prm, blockIdx.x, mat);
+  if (F.halt && F.halt[mat / F.halt_div]) return;
   const int tid = threadIdx.x;
   const int d = F.d, e = F.e, len = F.len, B = F.B, J = F.J;
   const bool admm = prm.mode != SVT_PLAIN;

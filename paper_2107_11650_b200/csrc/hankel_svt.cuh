@@ -51,6 +51,9 @@ struct SvtFamily {
   float2* Vs;          // subspace solver: count x DP x KB dominant-subspace store
   int* fallback;       // subspace solver: per-matrix flag, 1 = rank above threshold too
                        // close to KB, the full solver must redo this matrix
+  const int* halt;     // optional per-group stop flags: matrix `mat` is skipped when
+  int halt_div;        // halt[mat / halt_div] != 0 (independent ADMM problems batched in
+                       // one launch, each with its own early stop: parammap.cpp:37-51)
 };
 
 struct SvtParams {

@@ -83,6 +83,12 @@ size_t shlr_pencil_for(size_t pencil, size_t len) {
   return len / 3 + (len % 3 ? 1 : 0) + 1;
 }
 
+// HankelConfig::pencil_for_param (proj/src/hankel.cpp:20-29): the same rule
+// on its own field.
+size_t shlr_pencil_for_param(size_t pencil_param, size_t len) {
+  return shlr_pencil_for(pencil_param, len);
+}
+
 int shlr_mask_gauss_cartesian(size_t n, double rate, size_t acs, uint64_t seed, uint8_t* bits) {
   if (n == 0 || !(rate > 0.0) || rate > 1.0 || !bits) return SHLR_EINVAL;
   const size_t want = static_cast<size_t>(std::ceil(rate * static_cast<double>(n)));

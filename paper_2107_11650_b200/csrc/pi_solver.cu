@@ -12,6 +12,7 @@
 // pixel (proj/src/spirit.cpp:151-165), applied as row iFFT -> fused column
 // (iFFT, J x J matvec, FFT) -> row FFT.
 #include "pi_solver.cuh"
+#include "solver_util.cuh"
 
 #include <algorithm>
 #include <cmath>
@@ -22,30 +23,10 @@ namespace shlr_b200 {
 
 namespace {
 
-constexpr int kThreads = 256;
-
-// ------------------------------------------------------------ reductions
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
-// Deterministic block sum (valid in thread 0).
-__device__ double block_sum(double v, double* sh) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  v = warp_sum(v);
-  __syncthreads();
-  if (lane == 0) sh[warp] = v;
-  __syncthreads();
-  const int nw = (blockDim.x + 31) >> 5;
-  double t = 0.0;
-  if (warp == 0) {
-    t = lane < nw ? sh[lane] : 0.0;
-    t = warp_sum(t);
-  }
-  return t;
-}
+using util::block_sum;
+using util::dalloc;
+using util::grid_for;
+using util::kThreads;
 
 // Publishes `nv` per-block values and returns true in the last block to
 // arrive; that block then sums partials in a fixed order.
@@ -612,51 +593,6 @@ __global__ void k_from_double(const double* __restrict__ src, float2* __restrict
     dst[i] = make_float2((float)src[2 * i], (float)src[2 * i + 1]);
 }
 
-// ------------------------------------------------------------ host math (fp64)
-std::vector<double> hankel_counts_h(int n, int p) {
-  std::vector<double> c(n, 0.0);
-  const int q = n - p + 1;
-  for (int i = 0; i < p; ++i)
-    for (int j = 0; j < q; ++j) c[i + j] += 1.0;
-  return c;
-}
-
-// weights_centered (proj/src/hankel.cpp:75-97), as (re, im) pairs.
-std::vector<double> weights_centered_h(const double* taps, size_t ntaps, int n) {
-  std::vector<double> w(2 * n, 0.0), out(2 * n, 0.0);
-  for (int k = 0; k < n; ++k) {
-    double sr = 0, si = 0;
-    for (size_t t = 0; t < ntaps; ++t) {
-      const double ang = -2.0 * M_PI * (double)k * (double)t / (double)n;
-      const double c = std::cos(ang), s = std::sin(ang);
-      sr += taps[2 * t] * c - taps[2 * t + 1] * s;
-      si += taps[2 * t] * s + taps[2 * t + 1] * c;
-    }
-    w[2 * k] = sr;
-    w[2 * k + 1] = si;
-  }
-  const int c = n / 2;
-  for (int i = 0; i < n; ++i) {  // fftshift: out[(i + c) % n] = w[i]
-    out[2 * ((i + c) % n)] = w[2 * i];
-    out[2 * ((i + c) % n) + 1] = w[2 * i + 1];
-  }
-  return out;
-}
-
-int dagger_h(int i, int n) { return (2 * (n / 2) + n - i) % n; }
-
-template <class T>
-T* dalloc(size_t n) {
-  T* p = nullptr;
-  SHLR_CUDA(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
-  return p;
-}
-
-int grid_for(size_t n) {
-  const size_t blocks = (n + kThreads * 4 - 1) / (kThreads * 4);
-  return (int)std::max<size_t>(1, std::min<size_t>(blocks, (size_t)num_sms() * 4));
-}
-
 }  // namespace
 
 FftTwiddles make_twiddles(int n, float2** dev_storage, cudaStream_t stream) {
@@ -697,22 +633,12 @@ PiPlan::PiPlan(const PiConfig& cfg, const double* y, const uint8_t* mask, size_t
   red_blocks_ = grid_for(nel_);
 
   // ---- host-side constants (fp64, rounded once)
-  const auto wN = weights_centered_h(taps, ntaps, N);
-  const auto wM = weights_centered_h(taps, ntaps, M);
-  const auto cN = hankel_counts_h(N, cfg.Pr);
-  const auto cM = hankel_counts_h(M, cfg.Pc);
-  auto a_of = [&](const std::vector<double>& w, const std::vector<double>& cnt, int n) {
-    std::vector<double> a(n);
-    for (int k = 0; k < n; ++k) {
-      a[k] = (w[2 * k] * w[2 * k] + w[2 * k + 1] * w[2 * k + 1]) * cnt[k];
-      if (cfg.vc) {
-        const int f = dagger_h(k, n);
-        a[k] += (w[2 * f] * w[2 * f] + w[2 * f + 1] * w[2 * f + 1]) * cnt[f];
-      }
-    }
-    return a;
-  };
-  const auto aN = a_of(wN, cN, N), aM = a_of(wM, cM, M);
+  const auto wN = util::weights_centered_h(taps, ntaps, N);
+  const auto wM = util::weights_centered_h(taps, ntaps, M);
+  const auto cN = util::hankel_counts_h(N, cfg.Pr);
+  const auto cM = util::hankel_counts_h(M, cfg.Pc);
+  const auto aN = util::lift_normal_diag_h(wN, cN, N, cfg.vc);
+  const auto aM = util::lift_normal_diag_h(wM, cM, M, cfg.vc);
   std::vector<float> dg((size_t)M * N);
   for (int m = 0; m < M; ++m)
     for (int n = 0; n < N; ++n) {
@@ -720,20 +646,8 @@ PiPlan::PiPlan(const PiConfig& cfg, const double* y, const uint8_t* mask, size_t
       dg[(size_t)m * N + n] = (float)((s ? cfg.lambda : 0.0) + cfg.beta * aN[n] + cfg.beta * aM[m]);
     }
   // initial RHS adjoint spectra for Z = 0, D = 1: T = -1/beta
-  auto h0_of = [&](const std::vector<double>& w, const std::vector<double>& cnt, int n) {
-    std::vector<float2> h(n);
-    for (int k = 0; k < n; ++k) {
-      double re = w[2 * k] * cnt[k], im = -w[2 * k + 1] * cnt[k];  // conj(wc) * counts
-      if (cfg.vc) {
-        const int f = dagger_h(k, n);
-        re += w[2 * f] * cnt[f];
-        im += w[2 * f + 1] * cnt[f];
-      }
-      h[k] = make_float2((float)(-re / cfg.beta), (float)(-im / cfg.beta));
-    }
-    return h;
-  };
-  const auto hN = h0_of(wN, cN, N), hM = h0_of(wM, cM, M);
+  const auto hN = util::initial_weighted_adjoint_h(wN, cN, N, cfg.vc, cfg.beta);
+  const auto hM = util::initial_weighted_adjoint_h(wM, cM, M, cfg.vc, cfg.beta);
   std::vector<float2> wcNf(N), wcMf(M);
   for (int k = 0; k < N; ++k) wcNf[k] = make_float2((float)wN[2 * k], (float)wN[2 * k + 1]);
   for (int k = 0; k < M; ++k) wcMf[k] = make_float2((float)wM[2 * k], (float)wM[2 * k + 1]);

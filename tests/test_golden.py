@@ -16,6 +16,7 @@ import shlr_oracle as O
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 PI_CASES = sorted(glob.glob(os.path.join(GOLDEN, "pi_*.npz")))
 SVT_CASES = sorted(glob.glob(os.path.join(GOLDEN, "svt_*.npz")))
+PARAM_CASES = sorted(glob.glob(os.path.join(GOLDEN, "param_*.npz")))
 TOL = 1e-4  # BASELINE north_star: relative L2 for images and singular values
 
 
@@ -63,6 +64,35 @@ def test_oracle_matches_reference_svt(path):
     adj, sv = O.hankel_svt_unit(g["vecs"], int(g["p"]), float(g["tau"]))
     assert rel(adj, g["adj"]) < 1e-10
     assert rel(sv, g["sv"]) < 1e-12
+
+
+def param_configs(g, M):
+    """AdmmConfig / HankelConfig of a param fixture (defaults + the fixture's extra keys)."""
+    extra = dict(str(e).split("=", 1) for e in g["extra"])
+    acfg = M.AdmmConfig(max_outer=int(g["max_outer"]), tol=float(g["tol"]), enable_vc=bool(g["vc"]),
+                        lam2=float(extra.get("lambda2", 2.0)))
+    hcfg = M.HankelConfig(pencil=int(g["pencil"]), pencil_param=int(g["pencil_param"]))
+    return acfg, hcfg
+
+
+@pytest.mark.parametrize("path", PARAM_CASES, ids=os.path.basename)
+def test_oracle_matches_reference_param(path):
+    """Parameter imaging: shlr_param_reconstruct_slice (solvers.cpp:193-298) and
+    recon_param_dataset (parammap.cpp:21-54) against the reference's own run."""
+    g = load(path)
+    acfg, hcfg = param_configs(g, O)
+    n, l = g["mask"].shape
+    mask = O.SamplingMask(n, l, g["mask"])
+    if g["y"].ndim == 3:
+        x, st = O.shlr_param_reconstruct_slice(g["y"], mask, hcfg, acfg)
+        total, log = st.outer_iters, st.log
+    else:
+        x, total = O.recon_param_dataset(g["y"], mask, hcfg, acfg)
+        log = None
+    assert rel(x, g["x"]) < 1e-9
+    assert total == int(g["outer_iters"])
+    if log is not None:
+        assert log == [str(s) for s in g["log"]]
 
 
 def test_oracle_masks_bit_exact():

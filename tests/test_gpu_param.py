@@ -1,0 +1,151 @@
+"""Parameter imaging (SHLR-P / SHLR-VP, Algorithm S2) on the B200 path.
+
+* Reference fixtures (tests/golden/param_*.npz, produced by the reference's
+  own solvers.cpp / parammap.cpp through oracle/_ref/ref_driver): the GPU
+  reproduces the image within 1e-4 relative L2, the per-slice log lines
+  (iteration and CG-iteration counts exact, relchange to the printed 3
+  digits) and the total iteration count -- including slices that stop early
+  at different iterations.
+* A config-4-shaped case (K = 13 window, vc, 4 coils, 12 echoes) against the
+  numpy oracle on the same inputs.
+* BASELINE config 4 at full size (256 FE slices x 256 PE x 12 echoes x 4
+  coils): selected slices against the oracle, run-to-run bitwise
+  determinism."""
+import os
+
+import numpy as np
+import pytest
+
+import shlr_oracle as O
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+CASES = sorted(f for f in os.listdir(GOLDEN) if f.startswith("param_"))
+TOL = 1e-4
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b)))
+
+
+def log_values(lines):
+    out = []
+    for ln in lines:
+        kv = dict(t.split("=") for t in str(ln).split())
+        out.append((int(kv["iter"]), float(kv["relchange"]), int(kv["cg_iters"]), float(kv["cg_res"])))
+    return out
+
+
+def gpu_configs(A, g):
+    extra = dict(str(e).split("=", 1) for e in g["extra"])
+    acfg = A.AdmmConfig(max_outer=int(g["max_outer"]), tol=float(g["tol"]), enable_vc=bool(g["vc"]),
+                        lambda2=float(extra.get("lambda2", 2.0)))
+    hcfg = A.HankelConfig(pencil=int(g["pencil"]), pencil_param=int(g["pencil_param"]))
+    return acfg, hcfg
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", CASES)
+def test_gpu_param_matches_reference(gpu, name):
+    A = gpu
+    g = dict(np.load(os.path.join(GOLDEN, name), allow_pickle=True))
+    acfg, hcfg = gpu_configs(A, g)
+    n, l = g["mask"].shape
+    mask = A.SamplingMask(n, l, g["mask"])
+    log = []
+    if g["y"].ndim == 3:
+        st = A.SolveStats()
+        x = A.shlr_param_reconstruct_slice(g["y"], mask, hcfg, acfg, log=log, stats=st)
+        total = st.outer_iters
+    else:
+        tot = []
+        x = A.recon_param_dataset(A.ParameterDataset(g["y"], [10.0 * (e + 1) for e in range(l)]), mask,
+                                  hcfg, acfg, log=log, total_iters=tot).data
+        total = tot[0]
+    assert rel(x, g["x"]) < TOL
+    assert total == int(g["outer_iters"])
+    got, want = log_values(log), log_values(g["log"])
+    assert [(a[0], a[2]) for a in got] == [(b[0], b[2]) for b in want]
+    for a, b in zip(got, want):
+        assert abs(a[1] - b[1]) <= 2e-3 * abs(b[1]) + 1e-12
+
+
+def _config4_like(seed, m, n, l, j, k):
+    rng = np.random.default_rng(seed)
+    t = np.arange(l)
+    # exponential decays along the echoes (low rank in the echo lift) plus noise
+    amp = rng.uniform(0.2, 1.0, size=(m, n, 1, j)) * np.exp(-t[None, None, :, None] * 10.0
+                                                          / rng.uniform(30, 150, size=(m, n, 1, 1)))
+    img = amp * np.exp(1j * rng.uniform(0, 2 * np.pi, size=(m, n, 1, j)))
+    ksp = np.fft.fftshift(np.fft.fft2(np.fft.ifftshift(img, axes=(0, 1)), axes=(0, 1)),
+                          axes=(0, 1)) / np.sqrt(m * n)
+    ksp += 0.01 * (rng.standard_normal(ksp.shape) + 1j * rng.standard_normal(ksp.shape))
+    bits = np.stack([O.mask_gauss_cartesian(n, 0.3, 8, 100 + e).bits[0] for e in range(l)], axis=1)
+    return np.where(bits[None, :, :, None].astype(bool), ksp, 0), bits
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("vc", [False, True])
+def test_gpu_param_config4_shape_vs_oracle(gpu, vc):
+    """K = 13 (pencil N - 12), 4 coils, 12 echoes -> echo lifts 5 x 32 (the
+    config-4 echo geometry) and PE lifts (N-12) x 4*13 (x2 with vc)."""
+    A = gpu
+    m, n, l, j = 3, 48, 12, 4
+    y, bits = _config4_like(7 + vc, m, n, l, j, 13)
+    acfg = A.AdmmConfig(max_outer=6, tol=1e-300, enable_vc=vc)
+    hcfg = A.HankelConfig(pencil=n - 12)
+    tot = []
+    x = A.recon_param_dataset(A.ParameterDataset(y, [10.0 * (e + 1) for e in range(l)]),
+                              A.SamplingMask(n, l, bits), hcfg, acfg, total_iters=tot).data
+    xo, to = O.recon_param_dataset(y, O.SamplingMask(n, l, bits), O.HankelConfig(pencil=n - 12),
+                                   O.AdmmConfig(max_outer=6, tol=1e-300, enable_vc=vc))
+    assert tot[0] == to == m * 6
+    assert rel(x, xo) < TOL
+
+
+@pytest.fixture(scope="module")
+def c4_inputs():
+    import bench
+    return bench.make_param_inputs()
+
+
+@pytest.mark.gpu
+def test_gpu_param_config4_full_size(gpu, c4_inputs):
+    """BASELINE config 4 at full size (3 outer iterations): slices 0, 97 and 128
+    (the centre, highest energy) against the oracle's slice solve on the same
+    hybrid data; a second run is bitwise identical (reference determinism,
+    test_solvers.cpp:198-210)."""
+    A = gpu
+    ds, mask, hcfg, acfg = c4_inputs
+    acfg.max_outer = 3
+    log = []
+    x = A.recon_param_dataset(ds, mask, hcfg, acfg, log=log).data
+    assert np.isfinite(x).all() and len(log) == 3 * ds.data.shape[0]
+    x2 = A.recon_param_dataset(ds, mask, hcfg, acfg).data
+    assert np.array_equal(x, x2)
+    hybrid = O.fft_along_axis(ds.data, 0, True)
+    om = O.SamplingMask(mask.rows, mask.cols, mask.bits)
+    oa = O.AdmmConfig(max_outer=3, tol=1e-300, enable_vc=acfg.enable_vc, lam2=acfg.lambda2)
+    for s in (0, 97, 128):
+        xo, _ = O.shlr_param_reconstruct_slice(hybrid[s], om, O.HankelConfig(pencil=hcfg.pencil), oa)
+        assert rel(x[s], xo) < TOL, s
+
+
+@pytest.mark.gpu
+def test_gpu_param_errors(gpu):
+    A = gpu
+    y = np.zeros((16, 9, 2), np.complex128)
+    with pytest.raises(ValueError):
+        A.shlr_param_reconstruct_slice(y, A.SamplingMask(16, 8, np.ones((16, 8), np.uint8)),
+                                       A.HankelConfig(), A.AdmmConfig())
+    with pytest.raises(ValueError):
+        A.shlr_param_reconstruct_slice(y, A.SamplingMask(16, 9, np.ones((16, 9), np.uint8)),
+                                       A.HankelConfig(pencil_param=10), A.AdmmConfig())
+    # zero data: b = 0 -> CG returns zeros (solvers.cpp:30-33), x stays 0
+    st = A.SolveStats()
+    x = A.shlr_param_reconstruct_slice(y, A.SamplingMask(16, 9, np.ones((16, 9), np.uint8)),
+                                       A.HankelConfig(pencil=11), A.AdmmConfig(max_outer=2, tol=1e-300),
+                                       stats=st)
+    assert st.outer_iters == 2
+    xo, _ = O.shlr_param_reconstruct_slice(y, O.SamplingMask(16, 9, np.ones((16, 9), np.uint8)),
+                                           O.HankelConfig(pencil=11), O.AdmmConfig(max_outer=2, tol=1e-300))
+    assert rel(x, xo) < TOL
