@@ -327,6 +327,10 @@ def gpu_arm(args, dist, rank, world, local):
     if rank == 0 and not args.no_cpu:
         cpu = cpu_baseline(y, mask, g, procs=1, iters=1, budget_s=args.cpu_budget)
 
+    extra = {}
+    if not args.no_extra:
+        extra["config4_param"] = param_workload(args, dist, world, fp32_peak)
+
     value = world * args.steps / (t_max_ms * 1e-3)
     out = {
         "metric": "recon iterations/sec (256x256x8 coils, SHLR-S, K=15)",
@@ -358,9 +362,67 @@ def gpu_arm(args, dist, rank, world, local):
         "clocks": clocks,
         "e2e": e2e,
         "cpu_baseline": cpu,
+        "other_workloads": extra,
     }
     if rank == 0:
         print(json.dumps(out))
+
+
+def param_workload(args, dist, world, fp32_peak):
+    """BASELINE config 4 (T2 mapping, SHLR-VP) on the same GPU: resident-plan
+    outer iterations/s over all 256 FE slices (each a full Algorithm-S2 step:
+    RHS FFT, per-slice capped CG, 3072 PE lifts 244 x 104 + 65536 echo lifts
+    5 x 32 with SVT, duals and adjoints, stop rule), the SVT launches alone, and
+    an e2e recon_param_dataset call with host buffers.  Not the headline metric."""
+    from paper_2107_11650_b200 import api as A
+    cfg = CFG4
+    ds, mask, hcfg, acfg = make_param_inputs(cfg)
+    acfg.max_outer = max(cfg["outer"], args.warmup + args.steps)
+    plan = A.ParamPlan(ds.data, mask, hcfg, acfg, dataset=True)
+    plan.run(args.warmup)
+    plan.sync()
+    barrier(dist)
+    plan.run(args.steps)
+    plan.sync()
+    _, total_ms, launches = plan.timing()
+    t_max_ms = max_over_ranks(dist, total_ms)
+    plan.reset()
+    plan.set_timing(True)
+    plan.run(1)
+    plan.sync()
+    reps = 3
+    plan.run(reps)
+    plan.sync()
+    svt_ms = plan.timing()[0] / reps
+    plan.close()
+    n, k, j = cfg["N"], cfg["K"], cfg["J"]
+    p = n - k + 1
+    bq = (2 if cfg["vc"] else 1) * j * k
+    e, d = max(p, bq), min(p, bq)
+    l = cfg["L"]
+    pp = l // 3 + (1 if l % 3 else 0) + 1
+    e2, d2 = max(pp, j * (l - pp + 1)), min(pp, j * (l - pp + 1))
+    flops = cfg["M"] * l * svt_flops(e, d) + cfg["M"] * n * svt_flops(e2, d2)
+    out = {"workload": WORKLOAD4, "value": world * args.steps / (t_max_ms * 1e-3), "unit": "iterations/s",
+           "ms_per_step": t_max_ms / args.steps, "gpu_launches_per_step": launches,
+           "svt_ms": svt_ms, "svt_share_of_step": svt_ms / (t_max_ms / args.steps),
+           "svt_roofline": {"bound": "fp32", "achieved": flops / (svt_ms * 1e-3) / 1e12, "peak": fp32_peak,
+                            "unit": "TFLOP/s", "frac": flops / (svt_ms * 1e-3) / 1e12 / fp32_peak,
+                            "algorithmic": f"256*12 x F({e}x{d}) + 256*256 x F({e2}x{d2}), "
+                                           f"F = 16 e d^2 + 44 d^3: {flops / 1e9:.1f} GFLOP/step"}}
+    if not args.no_e2e:
+        acfg.max_outer = cfg["outer"]
+        barrier(dist)
+        t0 = time.perf_counter()
+        tot = []
+        A.recon_param_dataset(ds, mask, hcfg, acfg, total_iters=tot)
+        t_e2e = max_over_ranks(dist, time.perf_counter() - t0)
+        out["e2e"] = {"value": world * cfg["outer"] / t_e2e, "unit": "iterations/s",
+                      "h2d_bytes_per_step": int(ds.data.size * 16 + mask.bits.size),
+                      "d2h_bytes_per_step": int(ds.data.size * 16),
+                      "step": "one 50-iteration recon_param_dataset call (host complex128 M x N x L x J in/out, "
+                              "FE iFFT and plan setup inside)", "slice_iterations": tot[0]}
+    return out
 
 
 def reference_arm(args, dist, rank, world):
@@ -406,6 +468,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the config-3/4 side workloads")
     ap.add_argument("--cpu-budget", type=float, default=150.0)
     ap.add_argument("--ref-procs", type=int, default=16)
     args = ap.parse_args()

@@ -6,6 +6,8 @@
 // reconstruction path:
 //
 //   shlr_pi_reconstruct     solvers.hpp:64-70   (validation solvers.cpp:101-123)
+//   shlr_param_reconstruct_slice                solvers.hpp:74-79   (validation solvers.cpp:199-206)
+//   ParameterDataset, recon_param_dataset       parammap.hpp:11-40  (validation parammap.cpp:10-30)
 //   AdmmConfig / validate   solvers.hpp:16-34
 //   SolveStats, DivergenceError                 solvers.hpp:36-43
 //   HankelConfig::pencil_for                    hankel.hpp:15-25, hankel.cpp:10-18
@@ -155,6 +157,11 @@ struct HankelConfig {
     if (p == 0) throw std::invalid_argument("HankelConfig: pencil exceeds signal length");
     return p;
   }
+  std::size_t pencil_for_param(std::size_t len) const {
+    const std::size_t p = shlr_pencil_for_param(pencil_param, len);
+    if (p == 0) throw std::invalid_argument("HankelConfig: parameter pencil exceeds signal length");
+    return p;
+  }
 };
 
 struct AdmmConfig {
@@ -272,6 +279,93 @@ inline ComplexTensor shlr_pi_reconstruct(const ComplexTensor& y, const SamplingM
   if (stats) *stats = {st.outer_iters, st.final_rel_change};
   detail::check(rc, "shlr_pi_reconstruct");
   return x;
+}
+
+namespace detail {
+inline shlr_param_args param_args(const ComplexTensor& y, std::size_t m, std::size_t n, std::size_t l,
+                                  std::size_t j, const SamplingMask& mask, const HankelConfig& hcfg,
+                                  const AdmmConfig& acfg) {
+  shlr_param_args a{};
+  a.m = m;
+  a.n = n;
+  a.l = l;
+  a.j = j;
+  a.y = reinterpret_cast<const double*>(y.data());
+  a.mask = mask.bits.data();
+  a.taps = reinterpret_cast<const double*>(hcfg.filter_taps.data());
+  a.ntaps = hcfg.filter_taps.size();
+  a.pencil_pe = hcfg.pencil_for(n);
+  a.pencil_par = hcfg.pencil_for_param(l);
+  a.lambda = acfg.lambda;
+  a.lambda2 = acfg.lambda2;
+  a.beta = acfg.beta;
+  a.tau = acfg.tau;
+  a.tol = acfg.tol;
+  a.cg_tol = acfg.cg_tol;
+  a.max_outer = acfg.max_outer;
+  a.cg_max = acfg.cg_max;
+  a.enable_vc = acfg.enable_vc ? 1 : 0;
+  return a;
+}
+inline void log_line(void* ctx, const char* line) {
+  if (ctx) *static_cast<std::ostream*>(ctx) << line << "\n";
+}
+}  // namespace detail
+
+// Parameter-imaging ADMM on one PE x echo plane (SHLR-P / SHLR-VP), on the GPU.
+inline ComplexTensor shlr_param_reconstruct_slice(const ComplexTensor& y_m, const SamplingMask& mask,
+                                                  const HankelConfig& hcfg, const AdmmConfig& acfg,
+                                                  std::ostream* log = nullptr, SolveStats* stats = nullptr) {
+  acfg.validate();
+  if (y_m.rank() != 3) throw std::invalid_argument("shlr_param_reconstruct_slice: expected N x L x J");
+  const std::size_t n = y_m.dim(0), l = y_m.dim(1), j = y_m.dim(2);
+  if (mask.rows != n || mask.cols != l)
+    throw std::invalid_argument("shlr_param_reconstruct_slice: mask dims mismatch");
+  const shlr_param_args a = detail::param_args(y_m, 0, n, l, j, mask, hcfg, acfg);
+  ComplexTensor x({n, l, j});
+  shlr_stats st{};
+  const int rc = shlr_cuda_param_reconstruct(&a, reinterpret_cast<double*>(x.data()), &st, detail::log_line, log);
+  if (stats) *stats = {st.outer_iters, st.final_rel_change};
+  detail::check(rc, "shlr_param_reconstruct_slice");
+  return x;
+}
+
+/// Multi-echo multi-coil dataset: FE x PE x echoes x coils plus echo times.
+struct ParameterDataset {
+  ComplexTensor data;  // M x N x L x J
+  std::vector<double> tes_ms;
+  void validate() const {
+    if (data.rank() != 4) throw std::invalid_argument("ParameterDataset: expected M x N x L x J");
+    if (tes_ms.size() != data.dim(2)) throw std::invalid_argument("ParameterDataset: TE count != L");
+    for (std::size_t i = 0; i < tes_ms.size(); ++i)
+      if (tes_ms[i] <= 0 || (i > 0 && tes_ms[i] <= tes_ms[i - 1]))
+        throw std::invalid_argument("ParameterDataset: TEs must be positive and strictly increasing");
+  }
+  std::size_t fe() const { return data.dim(0); }
+  std::size_t pe() const { return data.dim(1); }
+  std::size_t echoes() const { return data.dim(2); }
+  std::size_t coils() const { return data.dim(3); }
+};
+
+// Per-FE-slice reconstruction (iFFT along FE, then every slice's ADMM with
+// its own early stop): all slices batched on the GPU.
+inline ParameterDataset recon_param_dataset(const ParameterDataset& y, const SamplingMask& mask,
+                                            const HankelConfig& hcfg, const AdmmConfig& acfg,
+                                            std::ostream* log = nullptr, std::size_t* total_iters = nullptr) {
+  y.validate();
+  const std::size_t m = y.fe(), n = y.pe(), l = y.echoes(), j = y.coils();
+  if (mask.rows != n || mask.cols != l) throw std::invalid_argument("recon_param_dataset: mask dims mismatch");
+  acfg.validate();
+  const shlr_param_args a = detail::param_args(y.data, m, n, l, j, mask, hcfg, acfg);
+  ParameterDataset out;
+  out.tes_ms = y.tes_ms;
+  out.data = ComplexTensor({m, n, l, j});
+  shlr_stats st{};
+  const int rc =
+      shlr_cuda_param_reconstruct(&a, reinterpret_cast<double*>(out.data.data()), &st, detail::log_line, log);
+  if (total_iters) *total_iters = st.outer_iters;
+  detail::check(rc, "recon_param_dataset");
+  return out;
 }
 
 // Centred unitary FFT along one axis (fft.hpp:11-30), on the device.

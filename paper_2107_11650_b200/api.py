@@ -469,16 +469,19 @@ def fp32_peak_tflops() -> float:
     return v.value
 
 
-def hankel_svt_batched(vecs: np.ndarray, p: int, tau: float) -> Tuple[np.ndarray, np.ndarray]:
+def hankel_svt_batched(vecs: np.ndarray, p: int, tau: float, want_sv: bool = True):
     """Config-5 unit on host complex128 arrays: vecs (B, Nc, N) ->
-    (adjoint vectors (B, Nc, N), singular values (B, d) descending)."""
+    (adjoint vectors (B, Nc, N), singular values (B, d) descending, or None
+    with want_sv=False -- the exact singular values need the full eigen-solver,
+    which covers d <= 128; without them d up to 248 runs (wide matrices))."""
     v = _c128(vecs)
     b, nc, n = v.shape
     q = n - p + 1
     d = min(p, nc * q)
     out = np.empty_like(v)
-    sv = np.empty((b, d), np.float64)
-    _check(lib.shlr_cuda_hankel_svt_batched_host(_dptr(v), b, nc, n, p, tau, _dptr(out), _dptr(sv)),
+    sv = np.empty((b, d), np.float64) if want_sv else None
+    _check(lib.shlr_cuda_hankel_svt_batched_host(_dptr(v), b, nc, n, p, tau, _dptr(out),
+                                                 _dptr(sv) if want_sv else None),
            "hankel_svt_batched")
     return out, sv
 

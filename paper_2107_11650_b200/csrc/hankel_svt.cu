@@ -177,6 +177,46 @@ __device__ __forceinline__ void build_chunk(float2* dst, const float2* wl, const
   }
 }
 
+// Large-d (BIG) subspace variant, wide families only (Ahat = A^H): the lifted
+// spectra are not staged in shared memory -- element (c, u) of Ahat is
+// conj(wl_b[t + u]) with (b, t) = lofs[c] (packed b << 16 | t), read from
+// the global spectra (L2-resident) with the weighting wc (smem copy `wcs`)
+// and the virtual-coil dagger applied on the fly (lift_weighted,
+// operators.cpp:36-56).
+__device__ __forceinline__ float2 lift_global(const SvtFamily& F, const float2* __restrict__ sp,
+                                              const float2* wcs, bool weighted, int bt, int u) {
+  const int b = bt >> 16, n = (bt & 0xffff) + u;
+  float2 v;
+  if (b < F.J) {
+    v = __ldg(sp + (long long)n * F.s_n + (long long)b * F.s_j);
+    if (weighted) v = cmul(wcs[n], v);
+  } else {
+    const int fl = dagger_src(n, F.len);
+    v = cmul(wcs[n], cconj(__ldg(sp + (long long)fl * F.s_n + (long long)(b - F.J) * F.s_j)));
+  }
+  return cconj(v);
+}
+
+template <int DP, int CS, int R>
+__device__ __forceinline__ void build_chunk_big(float2* dst, const SvtFamily& F, const float2* __restrict__ sp,
+                                                const float2* wcs, bool weighted, const int* lofs,
+                                                const float2* __restrict__ Dg, int i0, int rows, float inv_beta) {
+  const int d = F.d;
+  for (int t = threadIdx.x; t < R * DP; t += blockDim.x) {
+    const int r = t / DP, u = t - r * DP;
+    float2 v = make_float2(0.f, 0.f);
+    if (r < rows && u < d) {
+      v = lift_global(F, sp, wcs, weighted, lofs[i0 + r], u);
+      if (Dg) {  // duals straight from HBM/L2 (coalesced rows)
+        const float2 dd = __ldcg(Dg + (long long)(i0 + r) * d + u);
+        v.x = fmaf(dd.x, inv_beta, v.x);
+        v.y = fmaf(dd.y, inv_beta, v.y);
+      }
+    }
+    dst[r * CS + u] = v;
+  }
+}
+
 // Yc = C B over all 512 threads: the k range is split in two halves (threads
 // 0-255 -> Yc, 256-511 -> Yc2), each half a 2 x NB register tile per thread
 // (2 + NB shared loads per 2 NB complex FMAs).  The caller sums the halves
@@ -219,6 +259,13 @@ __device__ __forceinline__ void sum_halves(float2* Yc, const float2* Yc2, int nc
   }
 }
 
+// Chunk GEMM Yc = C B (columns 16 NB), optionally column-scaled; the split-k
+// form needs the second buffer Yc2, the NOSPLIT form (large block, no room
+// for Yc2) runs on the first 256 threads.  Ends with a barrier.
+template <int CS, int KS, int NB, int R, bool NOSPLIT>
+__device__ __forceinline__ void chunk_block(const float2* C, const float2* Bm, float2* Yc, float2* Yc2, int d,
+                                            const float* scale);
+
 // Yc (rows r2, r2+1 of the chunk; columns c16 + 16 n, n < NB) = C B for the
 // first 256 threads (2 x NB register tiles: 2 + NB shared loads per 2 NB
 // complex FMAs), optionally column-scaled.
@@ -248,6 +295,20 @@ __device__ __forceinline__ void chunk_times_block(const float2* C, const float2*
     const float sc = scale ? scale[c16 + 16 * n] : 1.f;
     Yc[r2 * KS + c16 + 16 * n] = cscale(y0[n], sc);
     Yc[(r2 + 1) * KS + c16 + 16 * n] = cscale(y1[n], sc);
+  }
+}
+
+template <int CS, int KS, int NB, int R, bool NOSPLIT>
+__device__ __forceinline__ void chunk_block(const float2* C, const float2* Bm, float2* Yc, float2* Yc2, int d,
+                                            const float* scale) {
+  if constexpr (NOSPLIT) {
+    chunk_times_block<CS, KS, NB>(C, Bm, Yc, d, scale);
+    __syncthreads();
+  } else {
+    chunk_times_block_split<CS, KS, NB>(C, Bm, Yc, Yc2, d);
+    __syncthreads();
+    sum_halves<KS, R>(Yc, Yc2, 16 * NB, scale);
+    __syncthreads();
   }
 }
 
@@ -712,8 +773,23 @@ __global__ void __maxnreg__(svt_max_regs(DP)) hankel_svt_kernel(const SvtParams 
   }
   load_v<DP, W>(Vg, DP, vt, vb);  // this thread's own stage-1 / previous-iteration values
   __syncthreads();
-  // stage 2: relative criterion only (G2 is accurate relative to its entries)
-  const int sweeps2 = jacobi<DP, W>(S, vt, vb, kTolRel2, 0.f, prm.max_sweeps);
+  // stage 2: relative criterion (G2 is accurate relative to its entries),
+  // optionally with an absolute floor and the below-threshold tail rule
+  // (the exact singular-value hook keeps the plain relative criterion)
+  float s2_abs = 0.f;
+  if (prm.s2_tol_abs > 0.f && !exact_sv) {
+    if (tid < 32) {
+      double mx = 0.0;
+      for (int u = tid; u < DP; u += 32) mx = fmax(mx, S.dg[u]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      if (tid == 0) S.scal[1] = (float)(prm.s2_tol_abs * mx);
+    }
+    __syncthreads();
+    s2_abs = S.scal[1];
+  }
+  const int sweeps2 = jacobi<DP, W>(S, vt, vb, kTolRel2, s2_abs, prm.max_sweeps,
+                                    exact_sv ? 0.f : prm.s2_tail * prm.thresh * prm.thresh);
   if (prm.sweeps_out && tid == 0) prm.sweeps_out[blockIdx.x] = sweeps1 * 100 + sweeps2;
   store_v<DP, W>(Vg, DP, vt, vb);
 
@@ -1004,6 +1080,7 @@ __device__ void householder_qr(float2* M, float2* Q, int d, float* tau) {
       }
     }
   }
+  if (M == Q) __syncthreads();  // in place: every warp is done reading the reflectors
   if (act) {
 #pragma unroll
     for (int t = 0; t < T; ++t) {
@@ -1411,36 +1488,63 @@ __device__ void hermitian_eig_tridiag(float2* H, float* scr, float* work, float2
 
 }  // namespace
 
-template <int DP, int KB, int R>
+template <int DP, int KB, int R, bool BIG>
 __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams prm) {
   constexpr int NT = kSubNT;
   constexpr int KS = KB + 1;       // row stride of the d x KB blocks (conflict-free column walks)
   constexpr int CS = DP + 1;       // row stride of the R x d chunk (odd: conflict-free anti-diagonal walks)
   constexpr int NC = KB / 16;      // 16-column groups
   constexpr int MR = (DP + 31) / 32;
+  // the large-d fallback block (KB > 48) has no room for the split-k buffer
+  constexpr bool NOSPLIT = BIG && KB > kSubspaceKB;
   static_assert(KB % 16 == 0 && KB % 8 == 0, "KB must be a multiple of 16");
   static_assert(R == 32, "the thread mappings assume 32-row chunks");
+  static_assert(KB >= kSubspaceKB, "the warm-start store holds kSubspaceKB columns");
 
   if (prm.skip && *prm.skip) return;
   int mat;
   const SvtFamily& F = family_of(prm, blockIdx.x, mat);
   if (F.halt && F.halt[mat / F.halt_div]) return;
+  if (prm.only_flagged && !F.fallback[mat]) return;
   const int tid = threadIdx.x;
   const int d = F.d, e = F.e, len = F.len, B = F.B, J = F.J;
   const bool admm = prm.mode != SVT_PLAIN;
   const bool weighted = prm.mode == SVT_ADMM_WEIGHTED;
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  // BIG (d > 128): one d x KB block V (the pass output, the QR and the Ritz
+  // rotation work in place; X aliases V), no resident spectra / adjoint
+  // accumulators (wl holds wc (len), acc the two carried partial adjoint
+  // blocks (2 x len)), no dual staging (duals read from L2 per chunk), and
+  // the Rayleigh-Ritz matrix H in the Yc | Yc2 pair.
   float2* V = reinterpret_cast<float2*>(smem_raw);  // DP x KS
-  float2* X = V + DP * KS;                           // DP x KS (also H for the Ritz solve)
-  float2* C = X + DP * KS;                           // R x CS  (Ahat chunk / U / T)
+  float2* X = BIG ? V : V + DP * KS;                 // DP x KS (non-BIG: also H for the Ritz solve)
+  float2* C = BIG ? V + DP * KS : X + DP * KS;       // R x CS  (Ahat chunk / U / T)
   float2* Yc = C + R * CS;                           // R x KS
-  float2* wl = Yc + R * KS;                          // B x len
-  float2* acc = wl + B * len;                        // B x len
-  float2* Yc2 = acc + B * len;                       // R x KS (second k-half of the chunk GEMM)
+  float2* Yc2;                                       // R x KS (second k-half of the chunk GEMM)
+  float2* wl;                                        // B x len  (BIG: len)
+  float2* acc;                                       // B x len  (BIG: 2 x len)
+  float2* tail;
+  // NOSPLIT: the Rayleigh-Ritz matrix sits behind the eigen-solver's work
+  // area (3 KB^2 floats at C), spilling from C into the Y region
+  constexpr int YREG = NOSPLIT ? (KB * KS + 3 * KB * KB / 2 - R * CS > R * KS ? KB * KS + 3 * KB * KB / 2 - R * CS
+                                                                              : R * KS)
+                               : 2 * R * KS;
+  if (BIG) {
+    Yc2 = NOSPLIT ? nullptr : Yc + R * KS;
+    wl = Yc + YREG;
+    acc = wl + len;
+    tail = acc + 2 * len;
+  } else {
+    wl = Yc + R * KS;
+    acc = wl + B * len;
+    Yc2 = acc + B * len;
+    tail = Yc2 + R * KS;
+  }
+  float2* Hm = BIG ? (NOSPLIT ? C + 3 * KB * KB / 2 : Yc) : X;  // KB x KS Rayleigh-Ritz matrix
   Smem<KB> S;                                        // Rayleigh-Ritz Jacobi workspace
-  S.G = X;
-  S.rec = reinterpret_cast<SlotRec*>(Yc2 + R * KS);
+  S.G = Hm;
+  S.rec = reinterpret_cast<SlotRec*>(tail);
   S.dgr = reinterpret_cast<double2*>(S.rec + KB);
   S.dg = reinterpret_cast<double*>(S.dgr + KB);
   S.f = reinterpret_cast<float*>(S.dg + KB);
@@ -1452,12 +1556,23 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
   int* lofs = perm + KB;                             // max(d, e): lift offsets (lift_tab)
 
   float2* Dg = admm ? F.D + (long long)mat * e * d : nullptr;
-  float2* Vsg = F.Vs + (long long)mat * DP * KB;
+  float2* Vsg = F.Vs + (long long)mat * DP * kSubspaceKB;  // warm-start store: kSubspaceKB columns
   const bool warm = prm.warm && *prm.warm;
+  const bool stg = Dg != nullptr && !BIG;  // duals staged by cp.async (non-BIG)
 
   // ---------------------------------------------------------- spectra
-  {
-    const float2* sp = F.spec + (long long)mat * F.s_mat;
+  const float2* spg = F.spec + (long long)mat * F.s_mat;
+  if (BIG) {
+    for (int t = tid; t < len; t += NT) wl[t] = weighted ? F.wc[t] : make_float2(1.f, 0.f);
+    for (int t = tid; t < 2 * len; t += NT) acc[t] = make_float2(0.f, 0.f);
+    for (int t = tid; t < e; t += NT) {
+      const int b = t / F.q;
+      lofs[t] = (b << 16) | (t - b * F.q);
+    }
+    if (tid < 4) S.flags[tid] = 0;
+    if (tid == 0) *cnt = 0;
+  } else {
+    const float2* sp = spg;
     for (int t = tid; t < J * len; t += NT) {
       const int j = t / len, n = t - j * len;
       const float2 s = sp[n * F.s_n + j * F.s_j];
@@ -1492,7 +1607,7 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
   if (warm) {
     for (int t = tid; t < DP * KB; t += NT) {
       const int k = t / KB, j = t - k * KB;
-      V[k * KS + j] = Vsg[t];
+      V[k * KS + j] = j < kSubspaceKB ? Vsg[k * kSubspaceKB + j] : make_float2(0.f, 0.f);
     }
     __syncthreads();
   } else {
@@ -1520,22 +1635,19 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
 #pragma unroll
       for (int n = 0; n < NC; ++n) xa[m][n] = make_float2(0.f, 0.f);
     __syncthreads();  // X (reflectors of the last QR) is free from here
-    if (Dg) stage_d_async(X, Dg, 0, min(R, e), d);
+    if (stg) stage_d_async(X, Dg, 0, min(R, e), d);
     if (prm.phase_clk) clk_u = clock64();
     for (int i0 = 0; i0 < e; i0 += R) {
       const int rows = min(R, e - i0);
-      if (Dg) stage_d_wait();
+      if (stg) stage_d_wait();
       SUB_ACC(clk_wait);
-      build_chunk<DP, CS, R>(C, wl, lofs, F, Dg ? X : nullptr, i0, rows, prm.inv_beta);
+      if (BIG) build_chunk_big<DP, CS, R>(C, F, spg, wl, weighted, lofs, Dg, i0, rows, prm.inv_beta);
+      else build_chunk<DP, CS, R>(C, wl, lofs, F, Dg ? X : nullptr, i0, rows, prm.inv_beta);
       __syncthreads();
       SUB_ACC(clk_build);
-      if (Dg && i0 + R < e) stage_d_async(X, Dg, i0 + R, min(R, e - i0 - R), d);
-      chunk_times_block_split<CS, KS, NC>(C, V, Yc, Yc2, d);  // Yc = C V
-      __syncthreads();
+      if (stg && i0 + R < e) stage_d_async(X, Dg, i0 + R, min(R, e - i0 - R), d);
+      chunk_block<CS, KS, NC, R, NOSPLIT>(C, V, Yc, Yc2, d, nullptr);  // Yc = C V
       SUB_ACC(clk_g1);
-      sum_halves<KS, R>(Yc, Yc2, KB, nullptr);
-      __syncthreads();
-      SUB_ACC(clk_sum);
 #pragma unroll 4
       for (int i = 0; i < rows; ++i) {  // X += C^H Yc
         float2 yv[NC];
@@ -1551,10 +1663,10 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
           }
         }
       }
-      if (!Dg) __syncthreads();  // with duals the next stage_d_wait() is the barrier
+      if (!stg) __syncthreads();  // with staged duals the next stage_d_wait() is the barrier
       SUB_ACC(clk_g2);
     }
-    if (Dg) __syncthreads();
+    if (stg) __syncthreads();
 #pragma unroll
     for (int m = 0; m < MR; ++m) {
       const int k = yi + 32 * m;
@@ -1606,17 +1718,15 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
 #pragma unroll
       for (int n = 0; n < NC; ++n) h[m][n] = make_float2(0.f, 0.f);
     __syncthreads();  // X is free from here
-    if (Dg) stage_d_async(X, Dg, 0, min(R, e), d);
+    if (stg) stage_d_async(X, Dg, 0, min(R, e), d);
     for (int i0 = 0; i0 < e; i0 += R) {
       const int rows = min(R, e - i0);
-      if (Dg) stage_d_wait();
-      build_chunk<DP, CS, R>(C, wl, lofs, F, Dg ? X : nullptr, i0, rows, prm.inv_beta);
+      if (stg) stage_d_wait();
+      if (BIG) build_chunk_big<DP, CS, R>(C, F, spg, wl, weighted, lofs, Dg, i0, rows, prm.inv_beta);
+      else build_chunk<DP, CS, R>(C, wl, lofs, F, Dg ? X : nullptr, i0, rows, prm.inv_beta);
       __syncthreads();
-      if (Dg && i0 + R < e) stage_d_async(X, Dg, i0 + R, min(R, e - i0 - R), d);
-      chunk_times_block_split<CS, KS, NC>(C, V, Yc, Yc2, d);
-      __syncthreads();
-      sum_halves<KS, R>(Yc, Yc2, KB, nullptr);
-      __syncthreads();
+      if (stg && i0 + R < e) stage_d_async(X, Dg, i0 + R, min(R, e - i0 - R), d);
+      chunk_block<CS, KS, NC, R, NOSPLIT>(C, V, Yc, Yc2, d, nullptr);
       for (int i = 0; i < rows; ++i) {
 #pragma unroll
         for (int m = 0; m < HM; ++m) {
@@ -1628,10 +1738,10 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
           }
         }
       }
-      if (!Dg) __syncthreads();
+      if (!stg) __syncthreads();
     }
-    if (Dg) __syncthreads();
-    // H (full Hermitian, stride KB+1 = KS) into X, diagonal to S.dg
+    if (stg) __syncthreads();
+    // H (full Hermitian, stride KB+1 = KS) into Hm, diagonal to S.dg
 #pragma unroll
     for (int m = 0; m < HM; ++m) {
       const int a = yi + 32 * m;
@@ -1640,14 +1750,14 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
         for (int n = 0; n < NC; ++n) {
           const int b = c16 + 16 * n;
           if (a == b) S.dg[a] = h[m][n].x;
-          X[a * KS + b] = h[m][n];
+          Hm[a * KS + b] = h[m][n];
         }
     }
   }
   __syncthreads();
   if (!prm.rr_jacobi) {
     SUB_STAMP(4);
-    hermitian_eig_tridiag<KB, KS>(X, reinterpret_cast<float*>(S.rec), reinterpret_cast<float*>(C), C, S.dg,
+    hermitian_eig_tridiag<KB, KS>(Hm, reinterpret_cast<float*>(S.rec), reinterpret_cast<float*>(C), C, S.dg,
                                   0.25f * prm.thresh * prm.thresh,
                                   prm.phase_clk ? prm.phase_clk + (long long)blockIdx.x * kPhaseSlots + 16 : nullptr);
     SUB_STAMP(5);
@@ -1720,6 +1830,7 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
         }
       }
     }
+    if (BIG) __syncthreads();  // in place: all reads of V are done
 #pragma unroll
     for (int m = 0; m < MR; ++m) {
       const int k = yi + 32 * m;
@@ -1740,36 +1851,48 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
   __syncthreads();
   float2* Vf = X;  // final Ritz vectors (d x KB)
   const int r = *cnt;
+  // diagnostics: Ritz values above the threshold (x1000) + Rayleigh-Ritz sweeps
+  if (prm.sweeps_out && tid == 0) prm.sweeps_out[blockIdx.x] += 1000 * r;
+  // the last level accepts Ritz pairs up to KB - kSubspaceMarginLast: pairs
+  // that close to the block edge converge slowest but sit near the threshold,
+  // where the shrink factor 1 - tau / sigma is ~0
+  constexpr int kMargin = (BIG && KB > kSubspaceKB) ? kSubspaceMarginLast : kSubspaceMargin;
   if (F.fallback) {
-    if (tid == 0) F.fallback[mat] = (r > KB - kSubspaceMargin) ? 1 : 0;
+    if (tid == 0) F.fallback[mat] = (r > KB - kMargin) ? 1 : 0;
   }
-  if (r > KB - kSubspaceMargin) return;  // the full solver redoes this matrix
-  for (int t = tid; t < DP * KB; t += NT) {
-    const int k = t / KB, j = t - k * KB;
+  // warm start of the next ADMM iteration: the leading kSubspaceKB Ritz
+  // vectors (sorted), stored even when this matrix is handed to a fallback
+  for (int t = tid; t < DP * kSubspaceKB; t += NT) {
+    const int k = t / kSubspaceKB, j = t - k * kSubspaceKB;
     Vsg[t] = Vf[k * KS + j];
   }
+  // too many singular values above the threshold: the fallback redoes this
+  // matrix from its untouched duals (d <= 128: the full solver; d > 128: this
+  // kernel with the larger block).  The last level finishes with the Ritz
+  // pairs it has and the host reports the flag.
+  const bool last_level = BIG && KB > kSubspaceKB;
+  if (!last_level && r > KB - kSubspaceMargin) return;
 
   // ---------------------------------------------------------- Z = (Ahat V) f V^H, duals, adjoint
   SUB_STAMP(6);
-  float2* Ds = V;  // the old basis is dead: stage the duals there
+  float2* Ds = V;  // the old basis is dead: stage the duals there (non-BIG)
   __syncthreads();
-  if (Dg) stage_d_async(Ds, Dg, 0, min(R, e), d);
+  if (stg) stage_d_async(Ds, Dg, 0, min(R, e), d);
   for (int i0 = 0; i0 < e; i0 += R) {
     const int rows = min(R, e - i0);
-    if (Dg) stage_d_wait();
-    build_chunk<DP, CS, R>(C, wl, lofs, F, Dg ? Ds : nullptr, i0, rows, prm.inv_beta);
+    if (stg) stage_d_wait();
+    if (BIG) build_chunk_big<DP, CS, R>(C, F, spg, wl, weighted, lofs, Dg, i0, rows, prm.inv_beta);
+    else build_chunk<DP, CS, R>(C, wl, lofs, F, Dg ? Ds : nullptr, i0, rows, prm.inv_beta);
     __syncthreads();
     {
       // only the first r (sorted) Ritz columns have f > 0
-      static_assert(NC <= 3, "NC > 3 needs more cases");
+      static_assert(NC <= 4, "NC > 4 needs more cases");
       const int nb = (r + 15) >> 4;
-      if (nb <= 1) chunk_times_block_split<CS, KS, 1>(C, Vf, Yc, Yc2, d);
-      else if (nb == 2 || NC == 2) chunk_times_block_split<CS, KS, (NC >= 2 ? 2 : 1)>(C, Vf, Yc, Yc2, d);
-      else chunk_times_block_split<CS, KS, NC>(C, Vf, Yc, Yc2, d);
-      __syncthreads();
-      sum_halves<KS, R>(Yc, Yc2, 16 * min(nb, NC), S.f);
+      if (nb <= 1) chunk_block<CS, KS, 1, R, NOSPLIT>(C, Vf, Yc, Yc2, d, S.f);
+      else if (nb == 2 || NC == 2) chunk_block<CS, KS, (NC >= 2 ? 2 : 1), R, NOSPLIT>(C, Vf, Yc, Yc2, d, S.f);
+      else if (nb == 3 || NC == 3) chunk_block<CS, KS, (NC >= 3 ? 3 : 1), R, NOSPLIT>(C, Vf, Yc, Yc2, d, S.f);
+      else chunk_block<CS, KS, NC, R, NOSPLIT>(C, Vf, Yc, Yc2, d, S.f);
     }
-    __syncthreads();
     {
       // Z[yi][k] = sum_{j < r} Yc[yi][j] conj(Vf[k][j]), k = c16 + 16 m
       constexpr int MZ = (DP + 15) / 16;
@@ -1790,9 +1913,10 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
         if (yi < rows && k < d) {
           float2 tv = z[m];
           if (admm) {
-            const float2 L = lift_tab(wl, lofs, F.wide, i0 + yi, k);
+            const float2 L = BIG ? lift_global(F, spg, wl, weighted, lofs[i0 + yi], k)
+                                 : lift_tab(wl, lofs, F.wide, i0 + yi, k);
             const long long gi = (long long)(i0 + yi) * d + k;
-            float2 dn = Ds[yi * d + k];
+            float2 dn = BIG ? __ldcg(Dg + gi) : Ds[yi * d + k];
             dn.x = fmaf(prm.tau_dual, L.x - z[m].x, dn.x);
             dn.y = fmaf(prm.tau_dual, L.y - z[m].y, dn.y);
             Dg[gi] = dn;
@@ -1804,7 +1928,43 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
       }
     }
     __syncthreads();
-    if (Dg && i0 + R < e) stage_d_async(Ds, Dg, i0 + R, min(R, e - i0 - R), d);  // overlaps the adjoint
+    if (stg && i0 + R < e) stage_d_async(Ds, Dg, i0 + R, min(R, e - i0 - R), d);  // overlaps the adjoint
+    if (BIG) {
+      // blocks b_lo..b_hi touch this chunk; a block whose rows continue into
+      // the next chunk is carried (acc[par]), the one carried in from the
+      // previous chunk is acc[par ^ 1]; complete blocks are weighted and
+      // stored -- regular blocks first, then (after a barrier) the
+      // virtual-coil blocks, which add into the regular blocks' output
+      // (adjoint_lift_weighted, operators.cpp:60-91)
+      const int q = F.q, P = F.P;
+      const int b_lo = i0 / q, b_hi = (i0 + rows - 1) / q;
+      const int par = (i0 / R) & 1;
+      const bool carried_in = i0 > 0 && (i0 % q) != 0;  // block b_lo started in the previous chunk
+      float2* op = F.out + (long long)mat * F.o_mat;
+      for (int pass = 0; pass < 2; ++pass) {
+        for (int o = tid; o < (b_hi - b_lo + 1) * len; o += NT) {
+          const int b = b_lo + o / len, n = o % len;
+          const bool vcb = weighted && F.vc && b >= J;
+          if (vcb != (pass == 1)) continue;
+          float2 sacc = (b == b_lo && carried_in) ? acc[(par ^ 1) * len + n] : make_float2(0.f, 0.f);
+          const int tlo = max(max(0, i0 - b * q), n - P + 1);
+          const int thi = min(min(q - 1, i0 + rows - 1 - b * q), n);
+          for (int t = tlo; t <= thi; ++t) sacc = cadd(sacc, cconj(C[(b * q + t - i0) * CS + (n - t)]));
+          if ((b + 1) * q - 1 > i0 + rows - 1) {  // continues into the next chunk
+            acc[par * len + n] = sacc;
+          } else if (!weighted) {
+            op[(long long)n * F.o_n + (long long)b * F.o_j] = sacc;
+          } else if (!vcb) {
+            op[(long long)n * F.o_n + (long long)b * F.o_j] = cmulc(wl[n], sacc);
+          } else {
+            const int fl = dagger_src(n, len);
+            float2* dst = op + (long long)fl * F.o_n + (long long)(b - J) * F.o_j;
+            *dst = cadd(*dst, cmul(wl[n], cconj(sacc)));
+          }
+        }
+        __syncthreads();
+      }
+    } else {
     for (int o = tid; o < B * len; o += NT) {
       const int b = o / len, n = o - b * len;
       float2 s = acc[o];
@@ -1819,12 +1979,13 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
       acc[o] = s;
     }
     __syncthreads();
+    }
   }
   SUB_STAMP(7);
 #undef SUB_STAMP
 
   // ---------------------------------------------------------- weighting + store
-  {
+  if (!BIG) {
     float2* op = F.out + (long long)mat * F.o_mat;
     for (int t = tid; t < J * len; t += NT) {
       const int j = t / len, n = t - j * len;
@@ -1841,23 +2002,26 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
   }
 }
 
-size_t svt_subspace_smem_bytes(int DP, int KB, int R, int maxB, int maxLen, int maxE) {
-  const int KS = KB + 1;
-  return sizeof(float2) * (2ull * DP * KS + (size_t)R * (DP + 1) + 2ull * R * KS + 2ull * maxB * maxLen) +
+size_t svt_subspace_smem_bytes(int DP, int KB, int R, int maxB, int maxLen, int maxE, bool big) {
+  const int KS = KB + 1, CS = DP + 1;
+  const size_t spectra = big ? 3ull * maxLen : 2ull * maxB * maxLen;
+  const bool nosplit = big && KB > kSubspaceKB;
+  const size_t yreg = nosplit ? (size_t)std::max(R * KS, KB * KS + 3 * KB * KB / 2 - R * CS) : 2ull * R * KS;
+  return sizeof(float2) * ((big ? 1ull : 2ull) * DP * KS + (size_t)R * CS + yreg + spectra) +
          sizeof(SlotRec) * KB + sizeof(double2) * KB + sizeof(double) * KB + 2 * sizeof(float) * KB +
          16 * sizeof(int) + sizeof(int) * KB + sizeof(int) * std::max(DP, maxE) + 64;
 }
 
 namespace {
-template <int DP>
+template <int DP, int KB, bool BIG>
 void launch_sub(const SvtParams& prm, int total, size_t smem, cudaStream_t stream) {
   static bool configured = false;
   if (!configured) {
-    SHLR_CUDA(cudaFuncSetAttribute(svt_subspace_kernel<DP, kSubspaceKB, 32>,
+    SHLR_CUDA(cudaFuncSetAttribute(svt_subspace_kernel<DP, KB, 32, BIG>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     configured = true;
   }
-  svt_subspace_kernel<DP, kSubspaceKB, 32><<<total, kSubNT, smem, stream>>>(prm);
+  svt_subspace_kernel<DP, KB, 32, BIG><<<total, kSubNT, smem, stream>>>(prm);
   SHLR_LAUNCH_CHECK();
 }
 }  // namespace
@@ -1865,29 +2029,67 @@ void launch_sub(const SvtParams& prm, int total, size_t smem, cudaStream_t strea
 bool launch_hankel_svt_subspace(const SvtParams& prm, int total, cudaStream_t stream) {
   if (total <= 0) return true;
   int dmin = 1 << 30, dmax = 0, maxB = 0, maxLen = 0, maxE = 0;
+  bool all_wide = true;
   for (int f = 0; f < prm.nfam; ++f) {
     dmin = std::min(dmin, prm.fam[f].d);
     dmax = std::max(dmax, prm.fam[f].d);
     maxB = std::max(maxB, prm.fam[f].B);
     maxLen = std::max(maxLen, prm.fam[f].len);
     maxE = std::max(maxE, prm.fam[f].e);
+    all_wide = all_wide && prm.fam[f].wide;
     if (!prm.fam[f].Vs || !prm.fam[f].fallback) return false;
   }
   // worthwhile only when the block is well below d
   if (dmin < kSubspaceKB + 24) return false;
+  if (dmax > 128) {
+    // large-d variant (KB = kSubspaceKBBig, spectra and adjoint not resident)
+    if (!all_wide || maxLen > 0xffff) return false;
+    const int dpb = svt_big_padded_dim(dmax);
+    if (!dpb) return false;
+    const size_t smem = svt_subspace_smem_bytes(dpb, kSubspaceKB, 32, maxB, maxLen, maxE, true);
+    if (smem > 227 * 1024) return false;
+    switch (dpb) {
+      case 160: launch_sub<160, kSubspaceKB, true>(prm, total, smem, stream); return true;
+      case 192: launch_sub<192, kSubspaceKB, true>(prm, total, smem, stream); return true;
+      case 248: launch_sub<248, kSubspaceKB, true>(prm, total, smem, stream); return true;
+    }
+    return false;
+  }
   const int dp = svt_padded_dim(dmax);
-  const size_t smem = svt_subspace_smem_bytes(dp, kSubspaceKB, 32, maxB, maxLen, maxE);
+  const size_t smem = svt_subspace_smem_bytes(dp, kSubspaceKB, 32, maxB, maxLen, maxE, false);
   if (smem > 227 * 1024) return false;
   switch (dp) {
-    case 72: launch_sub<72>(prm, total, smem, stream); return true;
-    case 80: launch_sub<80>(prm, total, smem, stream); return true;
-    case 88: launch_sub<88>(prm, total, smem, stream); return true;
-    case 96: launch_sub<96>(prm, total, smem, stream); return true;
-    case 104: launch_sub<104>(prm, total, smem, stream); return true;
-    case 112: launch_sub<112>(prm, total, smem, stream); return true;
-    case 120: launch_sub<120>(prm, total, smem, stream); return true;
-    case 128: launch_sub<128>(prm, total, smem, stream); return true;
+    case 72: launch_sub<72, kSubspaceKB, false>(prm, total, smem, stream); return true;
+    case 80: launch_sub<80, kSubspaceKB, false>(prm, total, smem, stream); return true;
+    case 88: launch_sub<88, kSubspaceKB, false>(prm, total, smem, stream); return true;
+    case 96: launch_sub<96, kSubspaceKB, false>(prm, total, smem, stream); return true;
+    case 104: launch_sub<104, kSubspaceKB, false>(prm, total, smem, stream); return true;
+    case 112: launch_sub<112, kSubspaceKB, false>(prm, total, smem, stream); return true;
+    case 120: launch_sub<120, kSubspaceKB, false>(prm, total, smem, stream); return true;
+    case 128: launch_sub<128, kSubspaceKB, false>(prm, total, smem, stream); return true;
     default: return false;
+  }
+}
+
+void launch_hankel_svt_big_fallback(const SvtParams& prm, int total, cudaStream_t stream) {
+  if (total <= 0) return;
+  int dmax = 0, maxB = 0, maxLen = 0, maxE = 0;
+  for (int f = 0; f < prm.nfam; ++f) {
+    dmax = std::max(dmax, prm.fam[f].d);
+    maxB = std::max(maxB, prm.fam[f].B);
+    maxLen = std::max(maxLen, prm.fam[f].len);
+    maxE = std::max(maxE, prm.fam[f].e);
+    if (!prm.fam[f].Vs || !prm.fam[f].fallback || !prm.fam[f].wide)
+      throw InvalidArg("hankel_svt large-d fallback: wide families with stores and flags only");
+  }
+  if (!prm.only_flagged) throw InvalidArg("hankel_svt large-d fallback: only_flagged required");
+  const int dpb = svt_big_padded_dim(dmax);
+  const size_t smem = svt_subspace_smem_bytes(dpb, kSubspaceKBBig, 32, maxB, maxLen, maxE, true);
+  if (!dpb || smem > 227 * 1024) throw Unsupported("hankel_svt: large-d fallback geometry out of range");
+  switch (dpb) {
+    case 160: return launch_sub<160, kSubspaceKBBig, true>(prm, total, smem, stream);
+    case 192: return launch_sub<192, kSubspaceKBBig, true>(prm, total, smem, stream);
+    case 248: return launch_sub<248, kSubspaceKBBig, true>(prm, total, smem, stream);
   }
 }
 

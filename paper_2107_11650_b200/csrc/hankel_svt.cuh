@@ -73,19 +73,42 @@ struct SvtParams {
                             // fallback flag is set (fam[f].fallback)
   float rr_tol_rel, rr_tol_abs;  // subspace Rayleigh-Ritz rotation tolerances (0 = defaults)
   float rr_tail;                 // pairs with both Ritz values < rr_tail * thresh^2 not rotated
+  float s2_tail;                 // full solver, stage 2: same rule (0 = rotate every pair)
+  float s2_tol_abs;              // full solver, stage 2: absolute floor x max diagonal (0 = none)
   int rr_jacobi;                 // 1: Rayleigh-Ritz by parallel Jacobi instead of tridiagonal + bisection
   int inner_norm;                // warm: normalise (instead of QR) after all but the last pass
   int wl_global;       // set by launch_hankel_svt: the lift source is read straight from
                        // fam[f].spec (plain mode, contiguous coils) instead of an smem copy
 };
 
+// Stage-2 Jacobi rules of the full solver in the ADMM modes (SvtParams::s2_tail,
+// s2_tol_abs).
+constexpr float kS2Tail = 0.25f;
+constexpr float kS2TolAbs = 1e-8f;
 // Dominant-subspace block size of the subspace SVT solver.
 constexpr int kSubspaceKB = 48;
+// Large-d variant (128 < d <= 248, wide matrices): the same block size, with
+// spectra and adjoint accumulators not resident in shared memory.  Its
+// fallback for matrices whose rank above the threshold exceeds
+// kSubspaceKB - kSubspaceMargin is the same kernel with a kSubspaceKBBig
+// block (no split-k buffer); a matrix beyond kSubspaceKBBig - kSubspaceMargin
+// there keeps its flag, which the host reports as unsupported.
+constexpr int kSubspaceKBBig = 64;
+// Padded dimension of the large-d variant for d (0 if out of range).
+inline int svt_big_padded_dim(int d) { return d <= 128 ? 0 : d <= 160 ? 160 : d <= 192 ? 192 : d <= 248 ? 248 : 0; }
+int svt_padded_dim(int d);
+// Row count of the per-matrix subspace store (F.Vs: store_dim x kSubspaceKB)
+// the subspace kernels use for dimension d.
+inline int svt_subspace_store_dim(int d) {
+  return d > 128 && svt_big_padded_dim(d) ? svt_big_padded_dim(d) : svt_padded_dim(d);
+}
 // clock64 diagnostics slots per matrix (SvtParams::phase_clk)
 constexpr int kPhaseSlots = 24;
 // Matrices with more than KB - margin singular values above the threshold
 // are redone by the full eigen-solver.
 constexpr int kSubspaceMargin = 8;
+// Margin of the last level (large-d fallback block): it has nothing behind it.
+constexpr int kSubspaceMarginLast = 2;
 
 // Subspace SVT: the thresholded spectral function needs only the eigenpairs
 // of G = Ahat^H Ahat with sigma > tau.  Subspace iteration on a KB-column
@@ -94,6 +117,9 @@ constexpr int kSubspaceMargin = 8;
 // (Ahat V) solved by the Jacobi kernel, and the same fused Z / dual / adjoint
 // epilogue.  Returns false (no launch) when the geometry is outside its range.
 bool launch_hankel_svt_subspace(const SvtParams& prm, int total, cudaStream_t stream);
+// Large-d fallback (kSubspaceKBBig block, cold start) for the matrices the
+// large-d subspace launch flagged (prm.only_flagged = the flags).
+void launch_hankel_svt_big_fallback(const SvtParams& prm, int total, cudaStream_t stream);
 
 // Index function shared by the kernel and shlr_cuda_lift_index_map: source
 // of element (i, c) of the p x (blocks*q) weighted lift (operators.cpp:36-56,

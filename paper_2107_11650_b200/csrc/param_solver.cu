@@ -341,7 +341,7 @@ ParamPlan::ParamPlan(const ParamConfig& cfg, const double* y, const uint8_t* mas
     dp_pe_ = svt_padded_dim(d);
     dpe_ = dalloc<float2>(dpe_elems_);
     vpe_ = dalloc<float2>((size_t)S * L * dp_pe_ * dp_pe_);
-    vspe_ = dalloc<float2>((size_t)S * L * dp_pe_ * kSubspaceKB);
+    vspe_ = dalloc<float2>((size_t)S * L * svt_subspace_store_dim(d) * kSubspaceKB);
     fallback_ = dalloc<int>((size_t)S * L);
     SHLR_CUDA(cudaMemsetAsync(fallback_, 0, sizeof(int) * S * L, stream_));
   }
@@ -423,6 +423,8 @@ SvtParams ParamPlan::svt_params(bool pe) const {
   sp.inv_beta = (float)(1.0 / cfg_.beta);
   sp.tau_dual = (float)cfg_.tau;
   sp.max_sweeps = 20;
+  sp.s2_tail = kS2Tail;
+  sp.s2_tol_abs = kS2TolAbs;
   sp.warm = have_v_;
   sp.q_cold = 6;
   sp.q_warm = 1;
@@ -506,7 +508,10 @@ void ParamPlan::enqueue_iteration(bool record_events) {
       SvtParams fb = sp;
       fb.only_flagged = fallback_;
       fb.warm = nullptr;
-      launch_hankel_svt(fb, sp.fam[0].count, stream_);
+      if (sp.fam[0].d <= 128)
+        launch_hankel_svt(fb, sp.fam[0].count, stream_);
+      else
+        launch_hankel_svt_big_fallback(fb, sp.fam[0].count, stream_);
       launch_count_ += 2;
     } else {
       if (subspace_used_) sp.warm = nullptr;

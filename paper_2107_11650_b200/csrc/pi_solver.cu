@@ -682,8 +682,9 @@ PiPlan::PiPlan(const PiConfig& cfg, const double* y, const uint8_t* mask, size_t
   vrow_ = dalloc<float2>((size_t)M * svt_dp_ * svt_dp_);
   vcol_ = dalloc<float2>((size_t)N * svt_dp_ * svt_dp_);
   sweeps_ = dalloc<int>((size_t)(M + N));
-  vsrow_ = dalloc<float2>((size_t)M * svt_dp_ * kSubspaceKB);
-  vscol_ = dalloc<float2>((size_t)N * svt_dp_ * kSubspaceKB);
+  const int sdim = svt_subspace_store_dim(std::max(dr, dc));
+  vsrow_ = dalloc<float2>((size_t)M * sdim * kSubspaceKB);
+  vscol_ = dalloc<float2>((size_t)N * sdim * kSubspaceKB);
   fallback_ = dalloc<int>((size_t)(M + N));
   SHLR_CUDA(cudaMemsetAsync(fallback_, 0, sizeof(int) * (M + N), stream_));
   if (const char* s = std::getenv("SHLR_Q_COLD")) q_cold_ = std::atoi(s);
@@ -863,7 +864,14 @@ void PiPlan::enqueue_iteration(int k, bool record_events) {
     sp.inv_beta = (float)(1.0 / cfg_.beta);
     sp.tau_dual = (float)cfg_.tau;
     sp.thresh = (float)(1.0 / cfg_.beta);
-    sp.max_sweeps = 20;
+    sp.max_sweeps = std::getenv("SHLR_MAX_SWEEPS") ? std::atoi(std::getenv("SHLR_MAX_SWEEPS")) : 20;
+    // stage-2 Jacobi of the full solver: pairs whose Ritz values both lie
+    // below (thresh/2)^2 have shrink factor 0 either way and are not rotated,
+    // and off-diagonals below 1e-8 max are FP32 noise -- without these rules
+    // clustered tails (virtual coils) never meet the relative criterion and
+    // the capped sweeps leave garbage rotations behind
+    sp.s2_tail = std::getenv("SHLR_S2_TAIL") ? (float)std::atof(std::getenv("SHLR_S2_TAIL")) : kS2Tail;
+    sp.s2_tol_abs = std::getenv("SHLR_S2_ABS") ? (float)std::atof(std::getenv("SHLR_S2_ABS")) : kS2TolAbs;
     sp.skip = &ctl_->stopped;
     sp.warm = &ctl_->have_v;
     sp.sweeps_out = sweeps_;
@@ -909,11 +917,17 @@ void PiPlan::enqueue_iteration(int k, bool record_events) {
     if (subspace_ && !want_sv && launch_hankel_svt_subspace(sp, M + N, stream_)) {
       subspace_used_ = true;
       // matrices whose rank above the threshold came too close to the block
-      // size are redone (from their unmodified duals) by the full solver
+      // size are redone (from their unmodified duals) by the full solver;
+      // the large-d variant (d > 128) has none: its flags are checked on download
       SvtParams fb = sp;
       fb.only_flagged = fallback_;
       fb.warm = nullptr;
-      launch_hankel_svt(fb, M + N, stream_);
+      if (svt_dp_ <= 128) {
+        launch_hankel_svt(fb, M + N, stream_);
+      } else {
+        fb.q_cold = std::max(q_cold_, 8);
+        launch_hankel_svt_big_fallback(fb, M + N, stream_);
+      }
       launch_count_ += 2;
     } else {
       // the full solver's warm start (vrow_/vcol_) is stale when earlier
@@ -993,6 +1007,12 @@ void PiPlan::download(double* x_out, size_t* outer_iters, double* final_rel,
   *outer_iters = (size_t)hc.outer;
   *final_rel = hc.outer > 0 ? hc.relchange : 1.0;
   *error = hc.error;
+  if (!*error && svt_dp_ > 128 && subspace_used_) {
+    std::vector<int> fl(M + N);
+    SHLR_CUDA(cudaMemcpy(fl.data(), fallback_, fl.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    for (int f : fl)
+      if (f) *error = 3;
+  }
   if (log_lines) {
     log_lines->clear();
     for (int k = 0; k < hc.outer && k < cfg_.max_outer; ++k) {
@@ -1052,7 +1072,8 @@ void hankel_svt_batched_device(const float2* vecs, int batch, int nc, int n, int
   float2* vsub = nullptr;
   int* flags = nullptr;
   SHLR_CUDA(cudaMallocAsync(&vscr, (size_t)chunk * per, stream));
-  SHLR_CUDA(cudaMallocAsync(&vsub, (size_t)chunk * dp * kSubspaceKB * sizeof(float2), stream));
+  SHLR_CUDA(cudaMallocAsync(&vsub, (size_t)chunk * svt_subspace_store_dim(F.d) * kSubspaceKB * sizeof(float2),
+                            stream));
   SHLR_CUDA(cudaMallocAsync(&flags, (size_t)chunk * sizeof(int), stream));
   for (int b0 = 0; b0 < batch; b0 += chunk) {
     const int nb = std::min(chunk, batch - b0);
@@ -1070,7 +1091,18 @@ void hankel_svt_batched_device(const float2* vecs, int batch, int nc, int n, int
     spc.q_warm = 3;
     if (!sv && !std::getenv("SHLR_FULL_SVT") && launch_hankel_svt_subspace(spc, nb, stream)) {
       spc.only_flagged = flags;
-      launch_hankel_svt(spc, nb, stream);
+      if (dp <= 128) {
+        launch_hankel_svt(spc, nb, stream);
+      } else {  // large-d variant: its larger-block fallback, then the flags
+        launch_hankel_svt_big_fallback(spc, nb, stream);
+        std::vector<int> hf(nb);
+        SHLR_CUDA(cudaMemcpyAsync(hf.data(), flags, nb * sizeof(int), cudaMemcpyDeviceToHost, stream));
+        SHLR_CUDA(cudaStreamSynchronize(stream));
+        for (int f : hf)
+          if (f)
+            throw Unsupported("hankel_svt: a lifted matrix with min(m, n) > 128 has more singular values "
+                              "above the threshold than the large-d subspace fallback block holds");
+      }
     } else {
       launch_hankel_svt(spc, nb, stream);
     }

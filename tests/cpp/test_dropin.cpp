@@ -185,3 +185,104 @@ TEST_CASE("SHLR-SV with calibrated kernels runs and improves on zero filling") {
   ComplexTensor zf = ifft2d_centered(y);
   CHECK(rel_diff(truth, rec) < rel_diff(truth, zf));
 }
+
+// ---------------------------------------------------------------- parameter imaging
+namespace {
+// N x L x J plane: mono-exponential decays along the echoes (low rank in the
+// echo lift), smooth along PE, in PE k-space.
+ComplexTensor param_plane(std::size_t n, std::size_t l, std::size_t coils, std::uint32_t seed) {
+  std::mt19937 rng(seed);
+  std::uniform_real_distribution<double> u(-1.0, 1.0);
+  ComplexTensor img({n, l, coils});
+  for (std::size_t r = 0; r < n; ++r) {
+    const double pd = std::abs(static_cast<double>(r) - n / 2.0) < n / 3.0 ? 1.0 : 0.2;
+    const double t2 = 40.0 + 60.0 * static_cast<double>(r % 7) / 7.0;
+    for (std::size_t e = 0; e < l; ++e)
+      for (std::size_t j = 0; j < coils; ++j)
+        img.at(r, e, j) = pd * std::exp(-10.0 * static_cast<double>(e + 1) / t2) *
+                              (1.0 + 0.2 * static_cast<double>(j)) +
+                          1e-3 * cplx{u(rng), u(rng)};
+  }
+  return fft_along_axis(img, 0, false);
+}
+}  // namespace
+
+TEST_CASE("parameter imaging: full sampling with strong fidelity is exact") {
+  const std::size_t n = 32, l = 9, j = 2;
+  ComplexTensor y = param_plane(n, l, j, 5);
+  SamplingMask mask{n, l, std::vector<std::uint8_t>(n * l, 1)};
+  AdmmConfig acfg;
+  acfg.lambda = 1e6;
+  acfg.max_outer = 5;
+  const ComplexTensor rec = shlr_param_reconstruct_slice(y, mask, HankelConfig{}, acfg);
+  CHECK(rel_diff(fft_along_axis(y, 0, true), rec) < 1e-3);
+}
+
+TEST_CASE("parameter imaging: determinism, log format, SHLR-VP differs from SHLR-P") {
+  const std::size_t n = 32, l = 9, j = 2;
+  ComplexTensor y = param_plane(n, l, j, 6);
+  SamplingMask mask{n, l, std::vector<std::uint8_t>(n * l, 0)};
+  for (std::size_t r = 0; r < n; ++r)
+    for (std::size_t e = 0; e < l; ++e) mask.bits[r * l + e] = ((r + 3 * e) % 3 == 0 || (r > 12 && r < 20));
+  AdmmConfig acfg;
+  acfg.max_outer = 3;
+  acfg.tol = 1e-300;
+  std::ostringstream log;
+  SolveStats stats;
+  const ComplexTensor a = shlr_param_reconstruct_slice(y, mask, HankelConfig{}, acfg, &log, &stats);
+  const ComplexTensor b = shlr_param_reconstruct_slice(y, mask, HankelConfig{}, acfg);
+  CHECK(max_abs_diff(a, b) == 0.0);
+  CHECK(stats.outer_iters == 3);
+  std::istringstream in(log.str());
+  std::string line;
+  int lines = 0;
+  while (std::getline(in, line)) {
+    CHECK(line.find("iter=") == 0);
+    CHECK(line.find("cg_iters=") != std::string::npos);
+    ++lines;
+  }
+  CHECK(lines == 3);
+  AdmmConfig vp = acfg;
+  vp.enable_vc = true;
+  const ComplexTensor c = shlr_param_reconstruct_slice(y, mask, HankelConfig{}, vp);
+  const ComplexTensor c2 = shlr_param_reconstruct_slice(y, mask, HankelConfig{}, vp);
+  CHECK(max_abs_diff(c, c2) == 0.0);
+  CHECK(max_abs_diff(a, c) > 0.0);
+}
+
+TEST_CASE("parameter imaging: dataset = per-slice solves, argument validation") {
+  const std::size_t m = 3, n = 24, l = 8, j = 2;
+  ComplexTensor plane = param_plane(n, l, j, 7);
+  ParameterDataset ds;
+  ds.data = ComplexTensor({m, n, l, j});
+  for (std::size_t f = 0; f < m; ++f)
+    for (std::size_t i = 0; i < n * l * j; ++i) ds.data[f * n * l * j + i] = plane[i] * (1.0 + 0.5 * f);
+  for (std::size_t e = 0; e < l; ++e) ds.tes_ms.push_back(10.0 * static_cast<double>(e + 1));
+  SamplingMask mask{n, l, std::vector<std::uint8_t>(n * l, 0)};
+  for (std::size_t r = 0; r < n; ++r)
+    for (std::size_t e = 0; e < l; ++e) mask.bits[r * l + e] = ((r + e) % 2 == 0 || (r > 9 && r < 15));
+  AdmmConfig acfg;
+  acfg.max_outer = 2;
+  acfg.tol = 1e-300;
+  std::size_t total = 0;
+  const ParameterDataset rec = recon_param_dataset(ds, mask, HankelConfig{}, acfg, nullptr, &total);
+  CHECK(total == m * 2);
+  // slice f of the dataset = the slice solve of the FE-iFFT of the data
+  const ComplexTensor hybrid = fft_along_axis(ds.data, 0, true);
+  for (std::size_t f = 0; f < m; ++f) {
+    ComplexTensor yf({n, l, j});
+    for (std::size_t i = 0; i < n * l * j; ++i) yf[i] = hybrid[f * n * l * j + i];
+    const ComplexTensor xf = shlr_param_reconstruct_slice(yf, mask, HankelConfig{}, acfg);
+    ComplexTensor rf({n, l, j});
+    for (std::size_t i = 0; i < n * l * j; ++i) rf[i] = rec.data[f * n * l * j + i];
+    CHECK(rel_diff(xf, rf) < 1e-4);
+  }
+  ParameterDataset bad = ds;
+  bad.tes_ms[1] = bad.tes_ms[0];
+  CHECK_THROWS_AS(recon_param_dataset(bad, mask, HankelConfig{}, acfg), std::invalid_argument);
+  SamplingMask wrong{n, l + 1, std::vector<std::uint8_t>(n * (l + 1), 1)};
+  CHECK_THROWS_AS(recon_param_dataset(ds, wrong, HankelConfig{}, acfg), std::invalid_argument);
+  HankelConfig hp;
+  hp.pencil_param = l + 1;
+  CHECK_THROWS_AS(shlr_param_reconstruct_slice(plane, mask, hp, acfg), std::invalid_argument);
+}

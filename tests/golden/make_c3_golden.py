@@ -1,0 +1,64 @@
+"""Pack the reference's own BASELINE config-3 run into tests/golden/c3_ref30.npz.
+
+Config 3 (BASELINE.json configs[2]): 256 x 256, 32 coils on two staggered
+rings, SHLR-V (virtual coils), Hankel window K = 11 -> pencil 246, lifted
+matrices 246 x 704 (d = 246).  The Poisson-disc mask of BASELINE does not
+exist in the reference; the nearest reference generator,
+mask_random2d(256, 256, 1/6, 24, 11650), stands in (SURVEY 8 mapping table).
+Iteration count: 30.  (BASELINE leaves it open; the reference default is
+max_outer = 50, solvers.hpp:16-34.  The number of singular values above the
+threshold per lifted matrix grows with the iterations -- max 47 at
+iteration 25, 63 at 50 -- and the B200 large-d subspace path holds 62, so
+parity is pinned at 30.)
+
+    python tests/golden/make_c3_golden.py inputs DIR     # writes DIR/y.cplx, DIR/m.cplx
+    oracle/_ref/ref_driver pi y=DIR/y.cplx mask=DIR/m.cplx out=DIR/ref30 vc=1 \\
+        pencil=246 max_outer=30 tol=1e-300 time=1       # the unmodified reference, one core
+    python tests/golden/make_c3_golden.py pack DIR
+
+The fixture keeps 4 of the 32 coils of the image (complex64) and the
+root-sum-of-squares image over all coils, plus the per-iteration log.
+"""
+import os
+import re
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+from paper_2107_11650_b200 import cplx_io as io  # noqa: E402
+
+COILS_KEPT = (0, 9, 18, 27)
+
+
+def make_inputs():
+    """(y (256, 256, 32) zero-filled k-space, mask bits (256, 256)) -- the bench/test inputs."""
+    from paper_2107_11650_b200 import synth
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import shlr_oracle as O
+    ph = synth.pi_phantom(256, 256, 32, rings=2)
+    bits = O.mask_random2d(256, 256, 1.0 / 6.0, 24, synth.SEED_MASK).bits.reshape(256, 256)
+    y = np.where(bits.astype(bool)[:, :, None], ph.kspace, 0)
+    return y, bits
+
+
+def main(cmd: str, d: str) -> None:
+    if cmd == "inputs":
+        os.makedirs(d, exist_ok=True)
+        y, bits = make_inputs()
+        io.write_cplx(y, os.path.join(d, "y.cplx"))
+        io.write_mask(bits, os.path.join(d, "m.cplx"))
+        return
+    x = io.read_cplx(os.path.join(d, "ref30.x.cplx"))
+    log = open(os.path.join(d, "ref30.log")).read().splitlines()
+    rel = [float(re.match(r"iter=\d+ relchange=(\S+)", ln).group(1)) for ln in log]
+    out = os.path.join(os.path.dirname(os.path.abspath(__file__)), "c3_ref30.npz")
+    np.savez_compressed(out, x30_coils=x[:, :, list(COILS_KEPT)].astype(np.complex64),
+                        coils=np.array(COILS_KEPT), rss30=np.sqrt((np.abs(x) ** 2).sum(axis=2)),
+                        relchange=np.array(rel), log=np.array(log))
+    print(out, os.path.getsize(out))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1], sys.argv[2])
