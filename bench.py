@@ -330,6 +330,7 @@ def gpu_arm(args, dist, rank, world, local):
     extra = {}
     if not args.no_extra:
         extra["config4_param"] = param_workload(args, dist, world, fp32_peak)
+        extra["config3_large_d"] = large_d_workload(args, dist, world, fp32_peak)
 
     value = world * args.steps / (t_max_ms * 1e-3)
     out = {
@@ -422,6 +423,56 @@ def param_workload(args, dist, world, fp32_peak):
                       "d2h_bytes_per_step": int(ds.data.size * 16),
                       "step": "one 50-iteration recon_param_dataset call (host complex128 M x N x L x J in/out, "
                               "FE iFFT and plan setup inside)", "slice_iterations": tot[0]}
+    return out
+
+
+WORKLOAD3 = ("config3: 256x256x32 coils (two staggered rings), SHLR-V (virtual coils), R=6 2D random mask "
+             "(mask_random2d(256,256,1/6,24): the reference's nearest generator to BASELINE's Poisson disc), "
+             "Hankel window K=11 (pencil 246, 512 lifted 246x704 matrices/iter, d=246), 30 outer iterations")
+
+
+def large_d_workload(args, dist, world, fp32_peak):
+    """BASELINE config 3 on the same GPU (30 iterations; see make_c3_golden.py for
+    why 30): the large-d subspace SVT path.  Timed over iterations 1-30 as a
+    whole (the rank above the threshold, and with it the share of matrices
+    that need the 64-column fallback level, grows with the iteration)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+    import make_c3_golden as G
+    from paper_2107_11650_b200 import api as A
+    iters = 30
+    y, bits = G.make_inputs()
+    mask = A.SamplingMask(256, 256, bits)
+    hcfg = A.HankelConfig(pencil=246)
+    acfg = A.AdmmConfig(max_outer=iters, tol=1e-300, enable_vc=True)
+    plan = A.PiPlan(y, mask, None, hcfg, acfg)
+    plan.run(1)   # graph capture + context warm-up on the first iteration
+    plan.sync()
+    plan.reset()
+    barrier(dist)
+    plan.run(iters)
+    plan.sync()
+    _, total_ms, launches = plan.timing()
+    t_max_ms = max_over_ranks(dist, total_ms)
+    plan.download()   # raises if a lifted matrix exceeded the large-d block
+    plan.close()
+    e, d = 704, 246
+    flops = 512 * svt_flops(e, d)
+    out = {"workload": WORKLOAD3, "value": world * iters / (t_max_ms * 1e-3), "unit": "iterations/s",
+           "ms_per_step": t_max_ms / iters, "steps": iters, "gpu_launches_per_step": launches,
+           "algorithmic_tflops": flops * iters / (t_max_ms * 1e-3) / 1e12,
+           "algorithmic_frac_of_fp32_peak": flops * iters / (t_max_ms * 1e-3) / 1e12 / fp32_peak,
+           "algorithmic": f"512 x F(704x246), F = 16 e d^2 + 44 d^3 = {svt_flops(e, d) / 1e9:.3f} GFLOP "
+                          "per matrix (whole step counted as SVT time: upper bound on the step, lower bound "
+                          "on the SVT rate)"}
+    if not args.no_e2e:
+        barrier(dist)
+        t0 = time.perf_counter()
+        st = A.SolveStats()
+        A.shlr_pi_reconstruct(y, mask, None, hcfg, acfg, stats=st)
+        t_e2e = max_over_ranks(dist, time.perf_counter() - t0)
+        out["e2e"] = {"value": world * st.outer_iters / t_e2e, "unit": "iterations/s",
+                      "h2d_bytes_per_step": int(y.size * 16 + bits.size), "d2h_bytes_per_step": int(y.size * 16),
+                      "step": "one 30-iteration shlr_cuda_pi_reconstruct call with host buffers"}
     return out
 
 
