@@ -121,6 +121,16 @@ bool launch_hankel_svt_subspace(const SvtParams& prm, int total, cudaStream_t st
 // large-d subspace launch flagged (prm.only_flagged = the flags).
 void launch_hankel_svt_big_fallback(const SvtParams& prm, int total, cudaStream_t stream);
 
+// One-thread-per-matrix Hankel-SVT for tiny plain lifts (small_svt.cu): the
+// parameter-imaging echo term (5 x 32 at config 4).  Plain / plain-ADMM
+// modes, one family, P <= kSmallSvtMaxP rows, P <= J q, len * J <=
+// kSmallSvtMaxLJ, no singular-value output.  Its duals are stored
+// structure-of-arrays: element (i, c) of matrix m at D[(i * J q + c) * count + m].
+constexpr int kSmallSvtMaxP = 8;
+constexpr int kSmallSvtMaxLJ = 64;
+bool small_svt_applicable(const SvtParams& prm);
+bool launch_small_svt(const SvtParams& prm, cudaStream_t stream);
+
 // Index function shared by the kernel and shlr_cuda_lift_index_map: source
 // of element (i, c) of the p x (blocks*q) weighted lift (operators.cpp:36-56,
 // hankel.cpp:31-41): regular block b < J reads coil b at i + t; vc block

@@ -520,8 +520,10 @@ void ParamPlan::enqueue_iteration(bool record_events) {
     }
   }
   {
+    // echo lifts (P x J(L-P+1), 5 x 32 at config 4): one thread per matrix
+    // when they are that small, else the general kernel
     SvtParams sp = svt_params(false);
-    launch_hankel_svt(sp, sp.fam[0].count, stream_);
+    if (!launch_small_svt(sp, stream_)) launch_hankel_svt(sp, sp.fam[0].count, stream_);
     ++launch_count_;
   }
   if (record_events) SHLR_CUDA(cudaEventRecord(evB_, stream_));
