@@ -24,6 +24,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 
 namespace shlr_b200 {
@@ -343,6 +344,8 @@ ParamPlan::ParamPlan(const ParamConfig& cfg, const double* y, const uint8_t* mas
     vpe_ = dalloc<float2>((size_t)S * L * dp_pe_ * dp_pe_);
     vspe_ = dalloc<float2>((size_t)S * L * svt_subspace_store_dim(d) * kSubspaceKB);
     fallback_ = dalloc<int>((size_t)S * L);
+    diag_ = dalloc<int>((size_t)S * L);
+    SHLR_CUDA(cudaMemsetAsync(diag_, 0, sizeof(int) * S * L, stream_));
     SHLR_CUDA(cudaMemsetAsync(fallback_, 0, sizeof(int) * S * L, stream_));
   }
   {
@@ -392,7 +395,7 @@ ParamPlan::~ParamPlan() {
   if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
   if (graph_) cudaGraphDestroy(graph_);
   void* bufs[] = {x0_, yk_, x_, xold_, r_, p_, bk_, hpe_, ximg_, hecho_, dg_, hpe0_, hecho0_, wcN_, twN_,
-                  dpe_, decho_, vpe_, vecho_, vspe_, fallback_, halt_, have_v_, ctl_, log_};
+                  dpe_, decho_, vpe_, vecho_, vspe_, fallback_, diag_, halt_, have_v_, ctl_, log_};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (ev0_) cudaEventDestroy(ev0_);
@@ -503,6 +506,7 @@ void ParamPlan::enqueue_iteration(bool record_events) {
   // ---- Z/D updates and the next RHS adjoints: PE family, then echo family
   {
     SvtParams sp = svt_params(true);
+    sp.sweeps_out = diag_;
     if (launch_hankel_svt_subspace(sp, sp.fam[0].count, stream_)) {
       subspace_used_ = true;
       SvtParams fb = sp;
@@ -561,6 +565,19 @@ void ParamPlan::run(size_t iters) {
         float ms = 0;
         SHLR_CUDA(cudaEventElapsedTime(&ms, evA_, evB_));
         svt_ms_ += ms;
+        if (std::getenv("SHLR_RANK_DIAG")) {  // Ritz values above the threshold per PE lift
+          const int n = cfg_.S * cfg_.L;
+          std::vector<int> h(n);
+          SHLR_CUDA(cudaMemcpy(h.data(), diag_, n * sizeof(int), cudaMemcpyDeviceToHost));
+          int mx = 0;
+          double mean = 0;
+          for (int v : h) {
+            mx = std::max(mx, v / 1000);
+            mean += v / 1000;
+          }
+          std::fprintf(stderr, "param iter %d: PE rank above threshold max %d mean %.1f\n", iter_ + 1, mx,
+                       mean / n);
+        }
       }
     }
     ++iter_;

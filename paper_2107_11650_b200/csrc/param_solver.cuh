@@ -81,6 +81,7 @@ class ParamPlan {
   float2 *vpe_ = nullptr, *vecho_ = nullptr;    // full-solver eigenvector stores
   float2* vspe_ = nullptr;                      // subspace-solver block store (PE family)
   int* fallback_ = nullptr;
+  int* diag_ = nullptr;              // per-PE-lift diagnostics (sweeps_out of the SVT launch)
   int* halt_ = nullptr;              // [S] stopped || error
   int* have_v_ = nullptr;            // warm-start flag (after the first iteration)
   ParamSliceCtl* ctl_ = nullptr;     // [S]
