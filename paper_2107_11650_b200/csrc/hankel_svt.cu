@@ -1506,6 +1506,11 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
   const SvtFamily& F = family_of(prm, blockIdx.x, mat);
   if (F.halt && F.halt[mat / F.halt_div]) return;
   if (prm.only_flagged && !F.fallback[mat]) return;
+  // large-d levels (fallback flag: 0 level 1, 1 handed to level 2 by level 1
+  // in this launch, 3 stays at level 2, 2 level-2 overflow): level 1 skips
+  // the matrices that stay at level 2
+  constexpr bool LEVEL2 = BIG && KB > kSubspaceKB;
+  if (BIG && !LEVEL2 && F.fallback && F.fallback[mat] == kLevelStay2) return;
   const int tid = threadIdx.x;
   const int d = F.d, e = F.e, len = F.len, B = F.B, J = F.J;
   const bool admm = prm.mode != SVT_PLAIN;
@@ -1557,7 +1562,12 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
 
   float2* Dg = admm ? F.D + (long long)mat * e * d : nullptr;
   float2* Vsg = F.Vs + (long long)mat * DP * kSubspaceKB;  // warm-start store: kSubspaceKB columns
-  const bool warm = prm.warm && *prm.warm;
+  float2* Vsg2 = LEVEL2 && F.Vs2 ? F.Vs2 + (long long)mat * DP * KB : nullptr;  // level-2 store
+  // level 2 starts warm (from its own store) only for matrices it kept from
+  // the previous iteration; the ones level 1 just handed over start from
+  // level 1's fresh block (+ random columns)
+  const bool warm = prm.warm && *prm.warm && (!LEVEL2 || (Vsg2 && F.fallback[mat] == kLevelStay2));
+  const bool seeded = LEVEL2 && !warm && F.fallback[mat] == kLevelHanded;
   const bool stg = Dg != nullptr && !BIG;  // duals staged by cp.async (non-BIG)
 
   // ---------------------------------------------------------- spectra
@@ -1607,14 +1617,16 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
   if (warm) {
     for (int t = tid; t < DP * KB; t += NT) {
       const int k = t / KB, j = t - k * KB;
-      V[k * KS + j] = j < kSubspaceKB ? Vsg[k * kSubspaceKB + j] : make_float2(0.f, 0.f);
+      V[k * KS + j] = Vsg2 ? Vsg2[t] : (j < kSubspaceKB ? Vsg[k * kSubspaceKB + j] : make_float2(0.f, 0.f));
     }
     __syncthreads();
   } else {
     for (int t = tid; t < DP * KB; t += NT) {
       const int k = t / KB, j = t - k * KB;
       const unsigned int h = (unsigned int)(mat * 0x9E3779B1u) ^ (unsigned int)(t * 0x85EBCA77u);
-      X[k * KS + j] = k < d ? make_float2(hash_unit(h), hash_unit(h ^ 0x5bd1e995u)) : make_float2(0.f, 0.f);
+      float2 v = k < d ? make_float2(hash_unit(h), hash_unit(h ^ 0x5bd1e995u)) : make_float2(0.f, 0.f);
+      if (seeded && j < kSubspaceKB) v = Vsg[k * kSubspaceKB + j];
+      X[k * KS + j] = v;
     }
     __syncthreads();
     householder_qr<KB, KS, DP>(X, V, d, tau);
@@ -1855,11 +1867,20 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
   if (prm.sweeps_out && tid == 0) prm.sweeps_out[blockIdx.x] += 1000 * r;
   // the last level accepts Ritz pairs up to KB - kSubspaceMarginLast: pairs
   // that close to the block edge converge slowest but sit near the threshold,
-  // where the shrink factor 1 - tau / sigma is ~0
-  constexpr int kMargin = (BIG && KB > kSubspaceKB) ? kSubspaceMarginLast : kSubspaceMargin;
-  if (F.fallback) {
-    if (tid == 0) F.fallback[mat] = (r > KB - kMargin) ? 1 : 0;
+  // where the shrink factor 1 - tau / sigma is ~0.  It keeps a matrix until
+  // its rank falls well inside level 1's range (hysteresis).
+  if (F.fallback && tid == 0) {
+    if (LEVEL2)
+      F.fallback[mat] = r > KB - kSubspaceMarginLast ? kLevelOverflow
+                        : r <= kSubspaceKB - 2 * kSubspaceMargin ? 0 : kLevelStay2;
+    else
+      F.fallback[mat] = (r > KB - kSubspaceMargin) ? kLevelHanded : 0;
   }
+  if (Vsg2)
+    for (int t = tid; t < DP * KB; t += NT) {
+      const int k = t / KB, j = t - k * KB;
+      Vsg2[t] = Vf[k * KS + j];
+    }
   // warm start of the next ADMM iteration: the leading kSubspaceKB Ritz
   // vectors (sorted), stored even when this matrix is handed to a fallback
   for (int t = tid; t < DP * kSubspaceKB; t += NT) {
@@ -1870,8 +1891,7 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
   // matrix from its untouched duals (d <= 128: the full solver; d > 128: this
   // kernel with the larger block).  The last level finishes with the Ritz
   // pairs it has and the host reports the flag.
-  const bool last_level = BIG && KB > kSubspaceKB;
-  if (!last_level && r > KB - kSubspaceMargin) return;
+  if (!LEVEL2 && r > KB - kSubspaceMargin) return;
 
   // ---------------------------------------------------------- Z = (Ahat V) f V^H, duals, adjoint
   SUB_STAMP(6);

@@ -51,6 +51,8 @@ struct SvtFamily {
   float2* Vs;          // subspace solver: count x DP x KB dominant-subspace store
   int* fallback;       // subspace solver: per-matrix flag, 1 = rank above threshold too
                        // close to KB, the full solver must redo this matrix
+  float2* Vs2;         // large-d level 2: count x DP x kSubspaceKBBig store (warm start of the
+                       // matrices that stay at level 2); nullptr: level 2 always starts seeded
   const int* halt;     // optional per-group stop flags: matrix `mat` is skipped when
   int halt_div;        // halt[mat / halt_div] != 0 (independent ADMM problems batched in
                        // one launch, each with its own early stop: parammap.cpp:37-51)
@@ -94,6 +96,10 @@ constexpr int kSubspaceKB = 48;
 // block (no split-k buffer); a matrix beyond kSubspaceKBBig - kSubspaceMargin
 // there keeps its flag, which the host reports as unsupported.
 constexpr int kSubspaceKBBig = 64;
+// Per-matrix fallback flag values of the large-d levels.
+constexpr int kLevelHanded = 1;    // level 1 handed the matrix to level 2 in this launch
+constexpr int kLevelOverflow = 2;  // level 2 ran out of block: reported as unsupported
+constexpr int kLevelStay2 = 3;     // stays at level 2 (warm from its own store) next iteration
 // Padded dimension of the large-d variant for d (0 if out of range).
 inline int svt_big_padded_dim(int d) { return d <= 128 ? 0 : d <= 160 ? 160 : d <= 192 ? 192 : d <= 248 ? 248 : 0; }
 int svt_padded_dim(int d);

@@ -414,6 +414,7 @@ void ParamPlan::reset() {
                                                         cfg_.J);
   k_p_reset<<<(S + 255) / 256, 256, 0, stream_>>>(ctl_, halt_, have_v_, S);
   SHLR_CUDA(cudaMemsetAsync(log_, 0, 3 * sizeof(double) * S * std::max(cfg_.max_outer, 1), stream_));
+  SHLR_CUDA(cudaMemsetAsync(fallback_, 0, sizeof(int) * S * cfg_.L, stream_));  // solver levels
   SHLR_LAUNCH_CHECK();
   iter_ = 0;
   subspace_used_ = false;

@@ -685,6 +685,10 @@ PiPlan::PiPlan(const PiConfig& cfg, const double* y, const uint8_t* mask, size_t
   const int sdim = svt_subspace_store_dim(std::max(dr, dc));
   vsrow_ = dalloc<float2>((size_t)M * sdim * kSubspaceKB);
   vscol_ = dalloc<float2>((size_t)N * sdim * kSubspaceKB);
+  if (std::max(dr, dc) > 128) {
+    vs2row_ = dalloc<float2>((size_t)M * sdim * kSubspaceKBBig);
+    vs2col_ = dalloc<float2>((size_t)N * sdim * kSubspaceKBBig);
+  }
   fallback_ = dalloc<int>((size_t)(M + N));
   SHLR_CUDA(cudaMemsetAsync(fallback_, 0, sizeof(int) * (M + N), stream_));
   if (const char* s = std::getenv("SHLR_Q_COLD")) q_cold_ = std::atoi(s);
@@ -764,7 +768,7 @@ PiPlan::~PiPlan() {
   if (graph_) cudaGraphDestroy(graph_);
   void* bufs[] = {yk_, x_, xold_, r_, p_, ap_, bk_, tmp_, tmp2_, dg_, srow_, scol_, hrow_, hcol_,
                   hrow0_, hcol0_, drow_, dcol_, wcN_, wcM_, pmat_, twM_, twN_, sv_, partials_,
-                  ctl_, log_, x0_, vrow_, vcol_, sweeps_, vsrow_, vscol_, fallback_};
+                  ctl_, log_, x0_, vrow_, vcol_, sweeps_, vsrow_, vscol_, vs2row_, vs2col_, fallback_};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (ev0_) cudaEventDestroy(ev0_);
@@ -782,6 +786,7 @@ void PiPlan::reset() {
   k_init_h<<<grid_for(nel_), kThreads, 0, stream_>>>(hrow_, hcol_, hrow0_, hcol0_, M, N, J);
   k_reset_ctl<<<1, 1, 0, stream_>>>(ctl_);
   SHLR_CUDA(cudaMemsetAsync(log_, 0, 3 * sizeof(double) * std::max(cfg_.max_outer, 1), stream_));
+  SHLR_CUDA(cudaMemsetAsync(fallback_, 0, sizeof(int) * (M + N), stream_));  // solver levels
   SHLR_LAUNCH_CHECK();
   iter_ = 0;
   subspace_used_ = false;
@@ -925,7 +930,12 @@ void PiPlan::enqueue_iteration(int k, bool record_events) {
       if (svt_dp_ <= 128) {
         launch_hankel_svt(fb, M + N, stream_);
       } else {
-        fb.q_cold = std::max(q_cold_, 8);
+        // level 2: warm from its own store for the matrices it keeps, three
+        // QR passes from level 1's fresh block for the ones handed over
+        fb.warm = &ctl_->have_v;
+        fb.q_cold = 3;
+        fb.fam[0].Vs2 = vs2row_;
+        fb.fam[1].Vs2 = vs2col_;
         launch_hankel_svt_big_fallback(fb, M + N, stream_);
       }
       launch_count_ += 2;
@@ -1011,7 +1021,7 @@ void PiPlan::download(double* x_out, size_t* outer_iters, double* final_rel,
     std::vector<int> fl(M + N);
     SHLR_CUDA(cudaMemcpy(fl.data(), fallback_, fl.size() * sizeof(int), cudaMemcpyDeviceToHost));
     for (int f : fl)
-      if (f) *error = 3;
+      if (f == kLevelOverflow) *error = 3;
   }
   if (log_lines) {
     log_lines->clear();
@@ -1099,7 +1109,7 @@ void hankel_svt_batched_device(const float2* vecs, int batch, int nc, int n, int
         SHLR_CUDA(cudaMemcpyAsync(hf.data(), flags, nb * sizeof(int), cudaMemcpyDeviceToHost, stream));
         SHLR_CUDA(cudaStreamSynchronize(stream));
         for (int f : hf)
-          if (f)
+          if (f == kLevelOverflow)
             throw Unsupported("hankel_svt: a lifted matrix with min(m, n) > 128 has more singular values "
                               "above the threshold than the large-d subspace fallback block holds");
       }

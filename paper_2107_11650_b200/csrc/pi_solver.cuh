@@ -83,6 +83,7 @@ class PiPlan {
   float2 *drow_ = nullptr, *dcol_ = nullptr;
   float2 *vrow_ = nullptr, *vcol_ = nullptr;  // SVT eigenvector stores (warm start)
   float2 *vsrow_ = nullptr, *vscol_ = nullptr;  // subspace-solver block stores (warm start)
+  float2 *vs2row_ = nullptr, *vs2col_ = nullptr;  // large-d level-2 block stores
   int* fallback_ = nullptr;                     // per-matrix subspace -> full fallback flags
   int q_cold_ = 6, q_warm_ = 1;
   bool subspace_ = true;
