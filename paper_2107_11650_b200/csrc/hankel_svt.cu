@@ -643,7 +643,8 @@ __global__ void __maxnreg__(svt_max_regs(DP)) hankel_svt_kernel(const SvtParams 
   int mat;
   const SvtFamily& F = family_of(prm, blockIdx.x, mat);
   if (F.halt && F.halt[mat / F.halt_div]) return;
-  if (prm.only_flagged && !F.fallback[mat]) return;
+  if (prm.only_flagged && (prm.only_flag_value ? F.fallback[mat] != prm.only_flag_value : !F.fallback[mat]))
+    return;
   const int tid = threadIdx.x;
   const int d = F.d, e = F.e, len = F.len, B = F.B, J = F.J;
   const bool admm = prm.mode != SVT_PLAIN;
@@ -1488,7 +1489,7 @@ __device__ void hermitian_eig_tridiag(float2* H, float* scr, float* work, float2
 
 }  // namespace
 
-template <int DP, int KB, int R, bool BIG>
+template <int DP, int KB, int R, bool BIG, bool L2>
 __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams prm) {
   constexpr int NT = kSubNT;
   constexpr int KS = KB + 1;       // row stride of the d x KB blocks (conflict-free column walks)
@@ -1496,21 +1497,29 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
   constexpr int NC = KB / 16;      // 16-column groups
   constexpr int MR = (DP + 31) / 32;
   // the large-d fallback block (KB > 48) has no room for the split-k buffer
-  constexpr bool NOSPLIT = BIG && KB > kSubspaceKB;
+  // solver levels: level 1 (KB1 columns) for every matrix, level 2 (KB2) for
+  // the ones whose rank above the threshold came too close to KB1; d <= 128
+  // has the full solver behind level 2, d > 128 (BIG) has nothing
+  // (d <= 128 level 1 runs with kSubspaceKB1 or kSubspaceKB columns; only
+  // the former has a level 2 behind it)
+  constexpr int KB1 = BIG ? kSubspaceKB : (L2 ? kSubspaceKB1 : KB);
+  constexpr int KB2 = BIG ? kSubspaceKBBig : kSubspaceKB;
+  static_assert(L2 ? KB == KB2 : (BIG ? KB == kSubspaceKB : (KB == kSubspaceKB1 || KB == kSubspaceKB)),
+                "block size of the level");
+  constexpr bool NOSPLIT = BIG && L2;
   static_assert(KB % 16 == 0 && KB % 8 == 0, "KB must be a multiple of 16");
   static_assert(R == 32, "the thread mappings assume 32-row chunks");
-  static_assert(KB >= kSubspaceKB, "the warm-start store holds kSubspaceKB columns");
 
   if (prm.skip && *prm.skip) return;
   int mat;
   const SvtFamily& F = family_of(prm, blockIdx.x, mat);
   if (F.halt && F.halt[mat / F.halt_div]) return;
   if (prm.only_flagged && !F.fallback[mat]) return;
-  // large-d levels (fallback flag: 0 level 1, 1 handed to level 2 by level 1
-  // in this launch, 3 stays at level 2, 2 level-2 overflow): level 1 skips
-  // the matrices that stay at level 2
-  constexpr bool LEVEL2 = BIG && KB > kSubspaceKB;
-  if (BIG && !LEVEL2 && F.fallback && F.fallback[mat] == kLevelStay2) return;
+  // per-matrix level flag (fallback): 0 level 1, kLevelHanded handed to
+  // level 2 by level 1 in this launch, kLevelStay2 kept at level 2 from the
+  // previous iteration, kLevelOverflow beyond level 2; level 1 skips the
+  // matrices that are not at level 1
+  if (!L2 && F.fallback && (F.fallback[mat] == kLevelStay2 || F.fallback[mat] == kLevelOverflow)) return;
   const int tid = threadIdx.x;
   const int d = F.d, e = F.e, len = F.len, B = F.B, J = F.J;
   const bool admm = prm.mode != SVT_PLAIN;
@@ -1561,13 +1570,15 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
   int* lofs = perm + KB;                             // max(d, e): lift offsets (lift_tab)
 
   float2* Dg = admm ? F.D + (long long)mat * e * d : nullptr;
-  float2* Vsg = F.Vs + (long long)mat * DP * kSubspaceKB;  // warm-start store: kSubspaceKB columns
-  float2* Vsg2 = LEVEL2 && F.Vs2 ? F.Vs2 + (long long)mat * DP * KB : nullptr;  // level-2 store
+  float2* Vsg = F.Vs + (long long)mat * DP * KB1;  // level-1 store: KB1 columns
+  float2* Vsg2 = L2 && F.Vs2 ? F.Vs2 + (long long)mat * DP * KB : nullptr;  // level-2 store
   // level 2 starts warm (from its own store) only for matrices it kept from
   // the previous iteration; the ones level 1 just handed over start from
   // level 1's fresh block (+ random columns)
-  const bool warm = prm.warm && *prm.warm && (!LEVEL2 || (Vsg2 && F.fallback[mat] == kLevelStay2));
-  const bool seeded = LEVEL2 && !warm && F.fallback[mat] == kLevelHanded;
+  const int lvl_in = F.fallback ? F.fallback[mat] : 0;
+  const bool warm = prm.warm && *prm.warm &&
+                    (!L2 || (Vsg2 && (lvl_in == kLevelStay2 || lvl_in == kLevelOverflow)));
+  const bool seeded = L2 && !warm && lvl_in == kLevelHanded;
   const bool stg = Dg != nullptr && !BIG;  // duals staged by cp.async (non-BIG)
 
   // ---------------------------------------------------------- spectra
@@ -1617,7 +1628,7 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
   if (warm) {
     for (int t = tid; t < DP * KB; t += NT) {
       const int k = t / KB, j = t - k * KB;
-      V[k * KS + j] = Vsg2 ? Vsg2[t] : (j < kSubspaceKB ? Vsg[k * kSubspaceKB + j] : make_float2(0.f, 0.f));
+      V[k * KS + j] = Vsg2 ? Vsg2[t] : (j < KB1 ? Vsg[k * KB1 + j] : make_float2(0.f, 0.f));
     }
     __syncthreads();
   } else {
@@ -1625,7 +1636,7 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
       const int k = t / KB, j = t - k * KB;
       const unsigned int h = (unsigned int)(mat * 0x9E3779B1u) ^ (unsigned int)(t * 0x85EBCA77u);
       float2 v = k < d ? make_float2(hash_unit(h), hash_unit(h ^ 0x5bd1e995u)) : make_float2(0.f, 0.f);
-      if (seeded && j < kSubspaceKB) v = Vsg[k * kSubspaceKB + j];
+      if (seeded && j < KB1) v = Vsg[k * KB1 + j];
       X[k * KS + j] = v;
     }
     __syncthreads();
@@ -1869,10 +1880,11 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
   // that close to the block edge converge slowest but sit near the threshold,
   // where the shrink factor 1 - tau / sigma is ~0.  It keeps a matrix until
   // its rank falls well inside level 1's range (hysteresis).
+  constexpr int kMarginHere = (BIG && L2) ? kSubspaceMarginLast : kSubspaceMargin;
   if (F.fallback && tid == 0) {
-    if (LEVEL2)
-      F.fallback[mat] = r > KB - kSubspaceMarginLast ? kLevelOverflow
-                        : r <= kSubspaceKB - 2 * kSubspaceMargin ? 0 : kLevelStay2;
+    if (L2)
+      F.fallback[mat] = r > KB - kMarginHere ? kLevelOverflow
+                        : r <= KB1 - 2 * kSubspaceMargin ? 0 : kLevelStay2;
     else
       F.fallback[mat] = (r > KB - kSubspaceMargin) ? kLevelHanded : 0;
   }
@@ -1881,17 +1893,20 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
       const int k = t / KB, j = t - k * KB;
       Vsg2[t] = Vf[k * KS + j];
     }
-  // warm start of the next ADMM iteration: the leading kSubspaceKB Ritz
+  // warm start of the next ADMM iteration at level 1: the leading KB1 Ritz
   // vectors (sorted), stored even when this matrix is handed to a fallback
-  for (int t = tid; t < DP * kSubspaceKB; t += NT) {
-    const int k = t / kSubspaceKB, j = t - k * kSubspaceKB;
+  for (int t = tid; t < DP * KB1; t += NT) {
+    const int k = t / KB1, j = t - k * KB1;
     Vsg[t] = Vf[k * KS + j];
   }
   // too many singular values above the threshold: the fallback redoes this
   // matrix from its untouched duals (d <= 128: the full solver; d > 128: this
   // kernel with the larger block).  The last level finishes with the Ritz
   // pairs it has and the host reports the flag.
-  if (!LEVEL2 && r > KB - kSubspaceMargin) return;
+  // handed on: the next level redoes this matrix from its untouched duals
+  // (the last level, BIG level 2, finishes with what it has; the host
+  // reports its overflow flag)
+  if (!(BIG && L2) && r > KB - kMarginHere) return;
 
   // ---------------------------------------------------------- Z = (Ahat V) f V^H, duals, adjoint
   SUB_STAMP(6);
@@ -2025,7 +2040,7 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
 size_t svt_subspace_smem_bytes(int DP, int KB, int R, int maxB, int maxLen, int maxE, bool big) {
   const int KS = KB + 1, CS = DP + 1;
   const size_t spectra = big ? 3ull * maxLen : 2ull * maxB * maxLen;
-  const bool nosplit = big && KB > kSubspaceKB;
+  const bool nosplit = big && KB > kSubspaceKB;  // BIG level 2
   const size_t yreg = nosplit ? (size_t)std::max(R * KS, KB * KS + 3 * KB * KB / 2 - R * CS) : 2ull * R * KS;
   return sizeof(float2) * ((big ? 1ull : 2ull) * DP * KS + (size_t)R * CS + yreg + spectra) +
          sizeof(SlotRec) * KB + sizeof(double2) * KB + sizeof(double) * KB + 2 * sizeof(float) * KB +
@@ -2033,84 +2048,112 @@ size_t svt_subspace_smem_bytes(int DP, int KB, int R, int maxB, int maxLen, int 
 }
 
 namespace {
-template <int DP, int KB, bool BIG>
+template <int DP, int KB, bool BIG, bool L2>
 void launch_sub(const SvtParams& prm, int total, size_t smem, cudaStream_t stream) {
   static bool configured = false;
   if (!configured) {
-    SHLR_CUDA(cudaFuncSetAttribute(svt_subspace_kernel<DP, KB, 32, BIG>,
+    SHLR_CUDA(cudaFuncSetAttribute(svt_subspace_kernel<DP, KB, 32, BIG, L2>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     configured = true;
   }
-  svt_subspace_kernel<DP, KB, 32, BIG><<<total, kSubNT, smem, stream>>>(prm);
+  svt_subspace_kernel<DP, KB, 32, BIG, L2><<<total, kSubNT, smem, stream>>>(prm);
   SHLR_LAUNCH_CHECK();
 }
-}  // namespace
 
-bool launch_hankel_svt_subspace(const SvtParams& prm, int total, cudaStream_t stream) {
-  if (total <= 0) return true;
+struct SubGeom {
   int dmin = 1 << 30, dmax = 0, maxB = 0, maxLen = 0, maxE = 0;
-  bool all_wide = true;
+  bool all_wide = true, stores = true;
+};
+SubGeom sub_geom(const SvtParams& prm) {
+  SubGeom g;
   for (int f = 0; f < prm.nfam; ++f) {
-    dmin = std::min(dmin, prm.fam[f].d);
-    dmax = std::max(dmax, prm.fam[f].d);
-    maxB = std::max(maxB, prm.fam[f].B);
-    maxLen = std::max(maxLen, prm.fam[f].len);
-    maxE = std::max(maxE, prm.fam[f].e);
-    all_wide = all_wide && prm.fam[f].wide;
-    if (!prm.fam[f].Vs || !prm.fam[f].fallback) return false;
+    g.dmin = std::min(g.dmin, prm.fam[f].d);
+    g.dmax = std::max(g.dmax, prm.fam[f].d);
+    g.maxB = std::max(g.maxB, prm.fam[f].B);
+    g.maxLen = std::max(g.maxLen, prm.fam[f].len);
+    g.maxE = std::max(g.maxE, prm.fam[f].e);
+    g.all_wide = g.all_wide && prm.fam[f].wide;
+    g.stores = g.stores && prm.fam[f].Vs && prm.fam[f].fallback;
   }
-  // worthwhile only when the block is well below d
-  if (dmin < kSubspaceKB + 24) return false;
-  if (dmax > 128) {
-    // large-d variant (KB = kSubspaceKBBig, spectra and adjoint not resident)
-    if (!all_wide || maxLen > 0xffff) return false;
-    const int dpb = svt_big_padded_dim(dmax);
+  return g;
+}
+
+// Launches level L2 of the subspace solver (d <= 128 level 1 with KB1
+// columns); false if the geometry is out of its range (nothing launched).
+template <bool L2, int KB1 = kSubspaceKB1>
+bool launch_level(const SvtParams& prm, int total, cudaStream_t stream) {
+  const SubGeom g = sub_geom(prm);
+  if (!g.stores) return false;
+  // worthwhile only when the level-1 block is well below d
+  if (g.dmin < kSubspaceKB + 24) return false;
+  if (g.dmax > 128) {
+    // large-d variant (spectra and adjoint not resident)
+    if (!g.all_wide || g.maxLen > 0xffff) return false;
+    const int dpb = svt_big_padded_dim(g.dmax);
     if (!dpb) return false;
-    const size_t smem = svt_subspace_smem_bytes(dpb, kSubspaceKB, 32, maxB, maxLen, maxE, true);
+    constexpr int KB = L2 ? kSubspaceKBBig : kSubspaceKB;
+    const size_t smem = svt_subspace_smem_bytes(dpb, KB, 32, g.maxB, g.maxLen, g.maxE, true);
     if (smem > 227 * 1024) return false;
     switch (dpb) {
-      case 160: launch_sub<160, kSubspaceKB, true>(prm, total, smem, stream); return true;
-      case 192: launch_sub<192, kSubspaceKB, true>(prm, total, smem, stream); return true;
-      case 248: launch_sub<248, kSubspaceKB, true>(prm, total, smem, stream); return true;
+      case 160: launch_sub<160, KB, true, L2>(prm, total, smem, stream); return true;
+      case 192: launch_sub<192, KB, true, L2>(prm, total, smem, stream); return true;
+      case 248: launch_sub<248, KB, true, L2>(prm, total, smem, stream); return true;
     }
     return false;
   }
-  const int dp = svt_padded_dim(dmax);
-  const size_t smem = svt_subspace_smem_bytes(dp, kSubspaceKB, 32, maxB, maxLen, maxE, false);
+  constexpr int KB = L2 ? kSubspaceKB : KB1;
+  const int dp = svt_padded_dim(g.dmax);
+  const size_t smem = svt_subspace_smem_bytes(dp, KB, 32, g.maxB, g.maxLen, g.maxE, false);
   if (smem > 227 * 1024) return false;
   switch (dp) {
-    case 72: launch_sub<72, kSubspaceKB, false>(prm, total, smem, stream); return true;
-    case 80: launch_sub<80, kSubspaceKB, false>(prm, total, smem, stream); return true;
-    case 88: launch_sub<88, kSubspaceKB, false>(prm, total, smem, stream); return true;
-    case 96: launch_sub<96, kSubspaceKB, false>(prm, total, smem, stream); return true;
-    case 104: launch_sub<104, kSubspaceKB, false>(prm, total, smem, stream); return true;
-    case 112: launch_sub<112, kSubspaceKB, false>(prm, total, smem, stream); return true;
-    case 120: launch_sub<120, kSubspaceKB, false>(prm, total, smem, stream); return true;
-    case 128: launch_sub<128, kSubspaceKB, false>(prm, total, smem, stream); return true;
+    case 72: launch_sub<72, KB, false, L2>(prm, total, smem, stream); return true;
+    case 80: launch_sub<80, KB, false, L2>(prm, total, smem, stream); return true;
+    case 88: launch_sub<88, KB, false, L2>(prm, total, smem, stream); return true;
+    case 96: launch_sub<96, KB, false, L2>(prm, total, smem, stream); return true;
+    case 104: launch_sub<104, KB, false, L2>(prm, total, smem, stream); return true;
+    case 112: launch_sub<112, KB, false, L2>(prm, total, smem, stream); return true;
+    case 120: launch_sub<120, KB, false, L2>(prm, total, smem, stream); return true;
+    case 128: launch_sub<128, KB, false, L2>(prm, total, smem, stream); return true;
     default: return false;
   }
 }
+}  // namespace
 
-void launch_hankel_svt_big_fallback(const SvtParams& prm, int total, cudaStream_t stream) {
+bool launch_hankel_svt_subspace(const SvtParams& prm, int total, cudaStream_t stream, int kb1) {
+  if (total <= 0) return true;
+  return kb1 == kSubspaceKB1 ? launch_level<false, kSubspaceKB1>(prm, total, stream)
+                             : launch_level<false, kSubspaceKB>(prm, total, stream);
+}
+
+int launch_hankel_svt_levels(const SvtParams& sp, int total, cudaStream_t stream, int kb1) {
+  int dmax = 0;
+  for (int f = 0; f < sp.nfam; ++f) dmax = std::max(dmax, sp.fam[f].d);
+  const bool big = dmax > 128;
+  if (big) kb1 = kSubspaceKB;
+  if (!launch_hankel_svt_subspace(sp, total, stream, kb1)) return 0;
+  int n = 1;
+  if (big || kb1 == kSubspaceKB1) {
+    SvtParams l2 = sp;
+    l2.only_flagged = sp.fam[0].fallback;
+    l2.q_cold = 3;
+    launch_hankel_svt_level2(l2, total, stream);
+    ++n;
+  }
+  if (big) return n;
+  // the full solver redoes what the last subspace level handed on (cold)
+  SvtParams fs = sp;
+  fs.only_flagged = sp.fam[0].fallback;
+  fs.only_flag_value = kb1 == kSubspaceKB1 ? kLevelOverflow : kLevelHanded;
+  fs.warm = nullptr;
+  launch_hankel_svt(fs, total, stream);
+  return n + 1;
+}
+
+void launch_hankel_svt_level2(const SvtParams& prm, int total, cudaStream_t stream) {
   if (total <= 0) return;
-  int dmax = 0, maxB = 0, maxLen = 0, maxE = 0;
-  for (int f = 0; f < prm.nfam; ++f) {
-    dmax = std::max(dmax, prm.fam[f].d);
-    maxB = std::max(maxB, prm.fam[f].B);
-    maxLen = std::max(maxLen, prm.fam[f].len);
-    maxE = std::max(maxE, prm.fam[f].e);
-    if (!prm.fam[f].Vs || !prm.fam[f].fallback || !prm.fam[f].wide)
-      throw InvalidArg("hankel_svt large-d fallback: wide families with stores and flags only");
-  }
-  if (!prm.only_flagged) throw InvalidArg("hankel_svt large-d fallback: only_flagged required");
-  const int dpb = svt_big_padded_dim(dmax);
-  const size_t smem = svt_subspace_smem_bytes(dpb, kSubspaceKBBig, 32, maxB, maxLen, maxE, true);
-  if (!dpb || smem > 227 * 1024) throw Unsupported("hankel_svt: large-d fallback geometry out of range");
-  switch (dpb) {
-    case 160: return launch_sub<160, kSubspaceKBBig, true>(prm, total, smem, stream);
-    case 192: return launch_sub<192, kSubspaceKBBig, true>(prm, total, smem, stream);
-    case 248: return launch_sub<248, kSubspaceKBBig, true>(prm, total, smem, stream);
-  }
+  if (!prm.only_flagged) throw InvalidArg("hankel_svt level 2: only_flagged required");
+  if (!launch_level<true>(prm, total, stream))
+    throw Unsupported("hankel_svt: subspace level-2 geometry out of range");
 }
 
 size_t svt_smem_bytes(int DP, int R, int maxB, int maxLen, bool wl_smem) {

@@ -71,8 +71,10 @@ struct SvtParams {
   int* sweeps_out;     // optional diagnostics: Jacobi sweeps used per matrix
   int q_cold, q_warm;  // subspace solver: iterations from a random / stored start
   long long* phase_clk;  // optional diagnostics: kPhaseSlots clock64 stamps per matrix
-  const int* only_flagged;  // full solver: nonzero pointer -> process only matrices whose
-                            // fallback flag is set (fam[f].fallback)
+  const int* only_flagged;  // nonzero pointer -> process only matrices whose fallback flag is
+                            // set (fam[f].fallback); with only_flag_value != 0 (full solver):
+                            // only matrices whose flag equals it
+  int only_flag_value;
   float rr_tol_rel, rr_tol_abs;  // subspace Rayleigh-Ritz rotation tolerances (0 = defaults)
   float rr_tail;                 // pairs with both Ritz values < rr_tail * thresh^2 not rotated
   float s2_tail;                 // full solver, stage 2: same rule (0 = rotate every pair)
@@ -87,7 +89,12 @@ struct SvtParams {
 // s2_tol_abs).
 constexpr float kS2Tail = 0.25f;
 constexpr float kS2TolAbs = 1e-8f;
-// Dominant-subspace block size of the subspace SVT solver.
+// Block sizes of the subspace SVT solver's levels.  d <= 128: level 1 with
+// kSubspaceKB columns, then the full solver; or level 1 kSubspaceKB1, level 2
+// kSubspaceKB, then the full solver (low-rank families: the parameter path's
+// PE lifts).  d > 128 (large-d variant): level 1 kSubspaceKB, level 2
+// kSubspaceKBBig, then nothing.
+constexpr int kSubspaceKB1 = 32;
 constexpr int kSubspaceKB = 48;
 // Large-d variant (128 < d <= 248, wide matrices): the same block size, with
 // spectra and adjoint accumulators not resident in shared memory.  Its
@@ -122,10 +129,17 @@ constexpr int kSubspaceMarginLast = 2;
 // then Householder QR), a final Rayleigh-Ritz projection H = (Ahat V)^H
 // (Ahat V) solved by the Jacobi kernel, and the same fused Z / dual / adjoint
 // epilogue.  Returns false (no launch) when the geometry is outside its range.
-bool launch_hankel_svt_subspace(const SvtParams& prm, int total, cudaStream_t stream);
-// Large-d fallback (kSubspaceKBBig block, cold start) for the matrices the
-// large-d subspace launch flagged (prm.only_flagged = the flags).
-void launch_hankel_svt_big_fallback(const SvtParams& prm, int total, cudaStream_t stream);
+bool launch_hankel_svt_subspace(const SvtParams& prm, int total, cudaStream_t stream,
+                                int kb1 = kSubspaceKB);
+// Level 2 of the subspace solver for the matrices level 1 handed over or
+// kept at level 2 (prm.only_flagged = the flags; fam[f].Vs2 its store).
+void launch_hankel_svt_level2(const SvtParams& prm, int total, cudaStream_t stream);
+// The whole subspace pipeline: level 1, level 2 (warm from fam[f].Vs2 when
+// set), and for d <= 128 the full solver for level-2 overflow (cold).
+// Returns the number of launches; 0 = the subspace solver does not apply to
+// this geometry (nothing launched).  Matrices with d > 128 that overflow
+// level 2 keep kLevelOverflow in their flag for the host to report.
+int launch_hankel_svt_levels(const SvtParams& sp, int total, cudaStream_t stream, int kb1);
 
 // One-thread-per-matrix Hankel-SVT for tiny plain lifts (small_svt.cu): the
 // parameter-imaging echo term (5 x 32 at config 4).  Plain / plain-ADMM

@@ -343,6 +343,7 @@ ParamPlan::ParamPlan(const ParamConfig& cfg, const double* y, const uint8_t* mas
     dpe_ = dalloc<float2>(dpe_elems_);
     vpe_ = dalloc<float2>((size_t)S * L * dp_pe_ * dp_pe_);
     vspe_ = dalloc<float2>((size_t)S * L * svt_subspace_store_dim(d) * kSubspaceKB);
+    vspe2_ = dalloc<float2>((size_t)S * L * svt_subspace_store_dim(d) * (d > 128 ? kSubspaceKBBig : kSubspaceKB));
     fallback_ = dalloc<int>((size_t)S * L);
     diag_ = dalloc<int>((size_t)S * L);
     SHLR_CUDA(cudaMemsetAsync(diag_, 0, sizeof(int) * S * L, stream_));
@@ -395,7 +396,7 @@ ParamPlan::~ParamPlan() {
   if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
   if (graph_) cudaGraphDestroy(graph_);
   void* bufs[] = {x0_, yk_, x_, xold_, r_, p_, bk_, hpe_, ximg_, hecho_, dg_, hpe0_, hecho0_, wcN_, twN_,
-                  dpe_, decho_, vpe_, vecho_, vspe_, fallback_, diag_, halt_, have_v_, ctl_, log_};
+                  dpe_, decho_, vpe_, vecho_, vspe_, vspe2_, fallback_, diag_, halt_, have_v_, ctl_, log_};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (ev0_) cudaEventDestroy(ev0_);
@@ -508,16 +509,13 @@ void ParamPlan::enqueue_iteration(bool record_events) {
   {
     SvtParams sp = svt_params(true);
     sp.sweeps_out = diag_;
-    if (launch_hankel_svt_subspace(sp, sp.fam[0].count, stream_)) {
+    sp.fam[0].Vs2 = vspe2_;
+    int nl = 0;
+    // PE lifts are low rank (mean 15-17 above the threshold at config 4):
+    // a 32-column level 1, 48-column level 2, then the full solver
+    if ((nl = launch_hankel_svt_levels(sp, sp.fam[0].count, stream_, kSubspaceKB1)) > 0) {
       subspace_used_ = true;
-      SvtParams fb = sp;
-      fb.only_flagged = fallback_;
-      fb.warm = nullptr;
-      if (sp.fam[0].d <= 128)
-        launch_hankel_svt(fb, sp.fam[0].count, stream_);
-      else
-        launch_hankel_svt_big_fallback(fb, sp.fam[0].count, stream_);
-      launch_count_ += 2;
+      launch_count_ += nl;
     } else {
       if (subspace_used_) sp.warm = nullptr;
       launch_hankel_svt(sp, sp.fam[0].count, stream_);

@@ -80,6 +80,7 @@ class ParamPlan {
   float2 *dpe_ = nullptr, *decho_ = nullptr;    // duals (Ahat orientation)
   float2 *vpe_ = nullptr, *vecho_ = nullptr;    // full-solver eigenvector stores
   float2* vspe_ = nullptr;                      // subspace-solver block store (PE family)
+  float2* vspe2_ = nullptr;                     // its level-2 store
   int* fallback_ = nullptr;
   int* diag_ = nullptr;              // per-PE-lift diagnostics (sweeps_out of the SVT launch)
   int* halt_ = nullptr;              // [S] stopped || error

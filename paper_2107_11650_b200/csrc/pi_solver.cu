@@ -685,15 +685,17 @@ PiPlan::PiPlan(const PiConfig& cfg, const double* y, const uint8_t* mask, size_t
   const int sdim = svt_subspace_store_dim(std::max(dr, dc));
   vsrow_ = dalloc<float2>((size_t)M * sdim * kSubspaceKB);
   vscol_ = dalloc<float2>((size_t)N * sdim * kSubspaceKB);
-  if (std::max(dr, dc) > 128) {
-    vs2row_ = dalloc<float2>((size_t)M * sdim * kSubspaceKBBig);
-    vs2col_ = dalloc<float2>((size_t)N * sdim * kSubspaceKBBig);
+  {
+    const int kb2 = std::max(dr, dc) > 128 ? kSubspaceKBBig : kSubspaceKB;
+    vs2row_ = dalloc<float2>((size_t)M * sdim * kb2);
+    vs2col_ = dalloc<float2>((size_t)N * sdim * kb2);
   }
   fallback_ = dalloc<int>((size_t)(M + N));
   SHLR_CUDA(cudaMemsetAsync(fallback_, 0, sizeof(int) * (M + N), stream_));
   if (const char* s = std::getenv("SHLR_Q_COLD")) q_cold_ = std::atoi(s);
   if (const char* s = std::getenv("SHLR_Q_WARM")) q_warm_ = std::atoi(s);
   if (std::getenv("SHLR_FULL_SVT")) subspace_ = false;
+  if (const char* s = std::getenv("SHLR_KB1")) kb1_ = std::atoi(s) == kSubspaceKB1 ? kSubspaceKB1 : kSubspaceKB;
   if (const char* s = std::getenv("SHLR_RR_REL")) rr_tol_rel_ = (float)std::atof(s);
   if (const char* s = std::getenv("SHLR_RR_ABS")) rr_tol_abs_ = (float)std::atof(s);
   if (const char* s = std::getenv("SHLR_RR_TAIL")) rr_tail_ = (float)std::atof(s);
@@ -919,26 +921,15 @@ void PiPlan::enqueue_iteration(int k, bool record_events) {
     if (record_events) SHLR_CUDA(cudaEventRecord(evA_, stream_));
     // The debug singular-value hook needs every singular value: full solver.
     const bool want_sv = sp.fam[0].sv != nullptr;
-    if (subspace_ && !want_sv && launch_hankel_svt_subspace(sp, M + N, stream_)) {
+    sp.fam[0].Vs2 = vs2row_;
+    sp.fam[1].Vs2 = vs2col_;
+    int nl = 0;
+    if (subspace_ && !want_sv && (nl = launch_hankel_svt_levels(sp, M + N, stream_, kb1_)) > 0) {
+      // level 1 (32 / 48 columns), level 2 (48 / 64) for matrices whose rank
+      // above the threshold came too close to the block, then (d <= 128) the
+      // full solver for level-2 overflow; d > 128 overflow is checked on download
       subspace_used_ = true;
-      // matrices whose rank above the threshold came too close to the block
-      // size are redone (from their unmodified duals) by the full solver;
-      // the large-d variant (d > 128) has none: its flags are checked on download
-      SvtParams fb = sp;
-      fb.only_flagged = fallback_;
-      fb.warm = nullptr;
-      if (svt_dp_ <= 128) {
-        launch_hankel_svt(fb, M + N, stream_);
-      } else {
-        // level 2: warm from its own store for the matrices it keeps, three
-        // QR passes from level 1's fresh block for the ones handed over
-        fb.warm = &ctl_->have_v;
-        fb.q_cold = 3;
-        fb.fam[0].Vs2 = vs2row_;
-        fb.fam[1].Vs2 = vs2col_;
-        launch_hankel_svt_big_fallback(fb, M + N, stream_);
-      }
-      launch_count_ += 2;
+      launch_count_ += nl;
     } else {
       // the full solver's warm start (vrow_/vcol_) is stale when earlier
       // iterations ran the subspace solver: start it cold then
@@ -1099,12 +1090,8 @@ void hankel_svt_batched_device(const float2* vecs, int batch, int nc, int n, int
     spc.sweeps_out = sweeps_out ? sweeps_out + b0 : nullptr;
     spc.q_cold = 6;
     spc.q_warm = 3;
-    if (!sv && !std::getenv("SHLR_FULL_SVT") && launch_hankel_svt_subspace(spc, nb, stream)) {
-      spc.only_flagged = flags;
-      if (dp <= 128) {
-        launch_hankel_svt(spc, nb, stream);
-      } else {  // large-d variant: its larger-block fallback, then the flags
-        launch_hankel_svt_big_fallback(spc, nb, stream);
+    if (!sv && !std::getenv("SHLR_FULL_SVT") && launch_hankel_svt_levels(spc, nb, stream, kSubspaceKB) > 0) {
+      if (dp > 128) {  // large-d variant: nothing behind level 2
         std::vector<int> hf(nb);
         SHLR_CUDA(cudaMemcpyAsync(hf.data(), flags, nb * sizeof(int), cudaMemcpyDeviceToHost, stream));
         SHLR_CUDA(cudaStreamSynchronize(stream));

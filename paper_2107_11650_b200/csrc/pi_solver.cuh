@@ -86,6 +86,7 @@ class PiPlan {
   float2 *vs2row_ = nullptr, *vs2col_ = nullptr;  // large-d level-2 block stores
   int* fallback_ = nullptr;                     // per-matrix subspace -> full fallback flags
   int q_cold_ = 6, q_warm_ = 1;
+  int kb1_ = kSubspaceKB;  // level-1 block of the subspace SVT (d <= 128); SHLR_KB1 overrides
   bool subspace_ = true;
   float rr_tol_rel_ = 0.f, rr_tol_abs_ = 0.f;  // 0 = kernel defaults
   float rr_tail_ = 0.f;
