@@ -24,6 +24,19 @@ struct FftTwiddles {
   int logn = -1;               // >= 0 iff n is a power of two
 };
 
+// t -> (fibre f, row k) of an [n][F] tile; shifts when F is a power of two
+// (lf = log2 F, or -1).
+__device__ __forceinline__ int fib_log2(int F) { return (F & (F - 1)) == 0 ? __ffs(F) - 1 : -1; }
+__device__ __forceinline__ void tile_idx(int t, int F, int lf, int& f, int& k) {
+  if (lf >= 0) {
+    f = t & (F - 1);
+    k = t >> lf;
+  } else {
+    f = t % F;
+    k = t / F;
+  }
+}
+
 // Radix-4 butterfly on v[0..3]; forward uses w = -i.
 template <bool INV>
 __device__ __forceinline__ void dft4(float2& a, float2& b, float2& c, float2& d) {
@@ -57,15 +70,21 @@ __device__ float2* smem_fft_pow2(float2* a, float2* b, int n, int logn, int F,
                                  const float2* __restrict__ tw) {
   float2* in = a;
   float2* out = b;
-  int ns = 1;
+  // fibre counts are powers of two in every caller: index math by shifts
+  const bool fpow2 = (F & (F - 1)) == 0;
+  const int lf = fpow2 ? __ffs(F) - 1 : 0;
+  int lns = 0;  // log2 of the current span ns
   int rem = logn;
   while (rem > 0) {
+    const int ns = 1 << lns;
     if (rem >= 2) {
       const int nb = n >> 2;
+      const int sshift = logn - lns - 2;  // n / (ns * 4) = 1 << sshift
       for (int t = threadIdx.x; t < nb * F; t += blockDim.x) {
-        const int f = t % F, j = t / F;
+        const int f = fpow2 ? (t & (F - 1)) : t % F;
+        const int j = fpow2 ? (t >> lf) : t / F;
         const int k = j & (ns - 1);
-        const int step = (n / (ns * 4)) * k;
+        const int step = k << sshift;
         float2 v0 = in[(j)*F + f];
         float2 v1 = in[(j + nb) * F + f];
         float2 v2 = in[(j + 2 * nb) * F + f];
@@ -76,28 +95,30 @@ __device__ float2* smem_fft_pow2(float2* a, float2* b, int n, int logn, int F,
           v3 = cmul(v3, twiddle(tw, 3 * step, INV));
         }
         dft4<INV>(v0, v1, v2, v3);
-        const int d0 = (j / ns) * ns * 4 + k;
+        const int d0 = ((j >> lns) << (lns + 2)) + k;
         out[(d0)*F + f] = v0;
         out[(d0 + ns) * F + f] = v1;
         out[(d0 + 2 * ns) * F + f] = v2;
         out[(d0 + 3 * ns) * F + f] = v3;
       }
-      ns <<= 2;
+      lns += 2;
       rem -= 2;
     } else {
       const int nb = n >> 1;
+      const int sshift = logn - lns - 1;
       for (int t = threadIdx.x; t < nb * F; t += blockDim.x) {
-        const int f = t % F, j = t / F;
+        const int f = fpow2 ? (t & (F - 1)) : t % F;
+        const int j = fpow2 ? (t >> lf) : t / F;
         const int k = j & (ns - 1);
-        const int step = (n / (ns * 2)) * k;
+        const int step = k << sshift;
         float2 v0 = in[(j)*F + f];
         float2 v1 = in[(j + nb) * F + f];
         if (ns > 1) v1 = cmul(v1, twiddle(tw, step, INV));
-        const int d0 = (j / ns) * ns * 2 + k;
+        const int d0 = ((j >> lns) << (lns + 1)) + k;
         out[(d0)*F + f] = cadd(v0, v1);
         out[(d0 + ns) * F + f] = csub(v0, v1);
       }
-      ns <<= 1;
+      lns += 1;
       rem -= 1;
     }
     __syncthreads();
@@ -149,8 +170,10 @@ template <bool INV>
 __device__ float2* smem_centered_dft(float2* a, float2* b, const FftTwiddles& tw, int F) {
   const int n = tw.n;
   if (tw.logn >= 0) {
+    const bool fpow2 = (F & (F - 1)) == 0;
+    const int lf = fpow2 ? __ffs(F) - 1 : 0;
     for (int t = threadIdx.x; t < n * F; t += blockDim.x) {
-      const int m = t / F;
+      const int m = fpow2 ? (t >> lf) : t / F;
       if (m & 1) a[t] = make_float2(-a[t].x, -a[t].y);
     }
     __syncthreads();
@@ -179,9 +202,11 @@ __global__ void __launch_bounds__(kFftThreads) fft_axis_kernel(Op op, FftTwiddle
   float2* b = fft_smem + (size_t)n * F;
   const int o = blockIdx.y;
   const int i0 = blockIdx.x * F;
+  const int lf = fib_log2(F);
 #pragma unroll 4
   for (int t = threadIdx.x; t < n * F; t += blockDim.x) {
-    const int f = t % F, k = t / F;
+    int f, k;
+    tile_idx(t, F, lf, f, k);
     const int i = i0 + f;
     a[t] = (i < inner) ? op.load(o, k, i) : make_float2(0.f, 0.f);
   }
@@ -189,7 +214,8 @@ __global__ void __launch_bounds__(kFftThreads) fft_axis_kernel(Op op, FftTwiddle
   float2* r = smem_centered_dft<INV>(a, b, tw, F);
   const float isn = rsqrtf((float)n);
   for (int t = threadIdx.x; t < n * F; t += blockDim.x) {
-    const int f = t % F, k = t / F;
+    int f, k;
+    tile_idx(t, F, lf, f, k);
     const int i = i0 + f;
     if (i < inner) op.store(o, k, i, cscale(r[t], centered_out_scale(k, n, tw.logn, isn)));
   }

@@ -432,9 +432,11 @@ __global__ void __launch_bounds__(kFftThreads) k_spirit_cols(const float2* __res
   const int n0 = blockIdx.x * PPT;  // first pixel column of the tile
   float2* a = sm;
   float2* b = sm + (size_t)M * F;
+  const int lf = fib_log2(F);
 #pragma unroll 4
   for (int t = threadIdx.x; t < M * F; t += blockDim.x) {
-    const int f = t % F, k = t / F;
+    int f, k;
+    tile_idx(t, F, lf, f, k);
     const int n = n0 + f / J;
     a[t] = n < N ? tmp[k * NJ + (long long)n0 * J + f] : make_float2(0.f, 0.f);
   }
@@ -494,7 +496,8 @@ __global__ void __launch_bounds__(kFftThreads) k_spirit_cols(const float2* __res
   __syncthreads();
   float2* res2 = smem_centered_dft<false>(oth, res, tw, F);
   for (int t = threadIdx.x; t < M * F; t += blockDim.x) {
-    const int f = t % F, k = t / F;
+    int f, k;
+    tile_idx(t, F, lf, f, k);
     const int n = n0 + f / J;
     if (n < N) tmp2[k * NJ + (long long)n0 * J + f] = cscale(res2[t], centered_out_scale(k, M, tw.logn, isn));
   }
@@ -524,13 +527,14 @@ __global__ void __launch_bounds__(kFftThreads) k_spirit_rows_fwd(const float2* _
   float2* res = smem_centered_dft<false>(a, b, tw, F);
   const float isn = rsqrtf((float)N);
   double s = 0.0;
+  const int lf = fib_log2(F);
 #pragma unroll 4
   for (int t = threadIdx.x; t < N * F; t += blockDim.x) {
-    const int k = t / F;
+    const int k = lf >= 0 ? t >> lf : t / F;
     const long long idx = m * NJ + t;
     const float2 v = cscale(res[t], centered_out_scale(k, N, tw.logn, isn));
     const float2 pv = vec[idx];
-    const float dv = dg[idx / J];
+    const float dv = dg[(long long)m * N + k];  // F == J: element (m, k, coil) -> pixel (m, k)
     const float2 av = make_float2(fmaf(dv, pv.x, lambda1 * v.x), fmaf(dv, pv.y, lambda1 * v.y));
     ap[idx] = av;
     s += (double)pv.x * av.x + (double)pv.y * av.y;
