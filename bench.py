@@ -333,6 +333,7 @@ def gpu_arm(args, dist, rank, world, local):
     if not args.no_extra:
         extra["config4_param"] = param_workload(args, dist, world, fp32_peak)
         extra["config3_large_d"] = large_d_workload(args, dist, world, fp32_peak)
+        extra["config5_sweep"] = sweep_workload(args, fp32_peak)
 
     value = world * args.steps / (t_max_ms * 1e-3)
     out = {
@@ -478,6 +479,51 @@ def large_d_workload(args, dist, world, fp32_peak):
                       "h2d_bytes_per_step": int(y.size * 16 + bits.size), "d2h_bytes_per_step": int(y.size * 16),
                       "step": "one 30-iteration shlr_cuda_pi_reconstruct call with host buffers"}
     return out
+
+
+SWEEP_POINTS = [(128, 8, 15), (256, 1, 15), (256, 8, 7), (256, 8, 15), (256, 8, 31), (256, 32, 15),
+                (512, 8, 15)]
+
+
+def sweep_workload(args, fp32_peak):
+    """BASELINE config 5 (batched Hankel-SVT unit, slices = 1, batch = 2N) at a
+    few sweep points: device-resident complex64 vectors in and out through the
+    device-pointer C-ABI call (lift_plain -> svt -> adjoint_lift_plain, cold:
+    the unit has no warm start), CUDA events around the call on its stream."""
+    import torch
+    from paper_2107_11650_b200 import api as A
+    from paper_2107_11650_b200 import synth
+    out = []
+    for n, nc, k in SWEEP_POINTS:
+        p = n - k + 1
+        batch = 2 * n
+        v = synth.sweep_vectors(n, nc, k, batch)
+        tau = synth.sweep_tau(n, nc, k)
+        dv = torch.from_numpy(v.astype(np.complex64)).cuda()
+        do = torch.empty_like(dv)
+        st = torch.cuda.Stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        try:
+            with torch.cuda.stream(st):
+                A.hankel_svt_batched_device(dv.data_ptr(), batch, nc, n, p, tau, do.data_ptr(), 0, st.cuda_stream)
+                st.synchronize()
+                reps = 3
+                e0.record(st)
+                for _ in range(reps):
+                    A.hankel_svt_batched_device(dv.data_ptr(), batch, nc, n, p, tau, do.data_ptr(), 0,
+                                                st.cuda_stream)
+                e1.record(st)
+                st.synchronize()
+            ms = e0.elapsed_time(e1) / reps
+            e, d = max(p, nc * k), min(p, nc * k)
+            tf = batch * svt_flops(e, d) / (ms * 1e-3) / 1e12
+            out.append({"N": n, "Nc": nc, "K": k, "matrix": f"{p}x{nc * k}", "batch": batch,
+                        "matrices_per_s": batch / (ms * 1e-3), "ms": ms, "algorithmic_tflops": tf,
+                        "frac_of_fp32_peak": tf / fp32_peak})
+        except Exception as exc:  # geometry outside this build
+            out.append({"N": n, "Nc": nc, "K": k, "unsupported": str(exc)[:160]})
+    return {"workload": "config5: batched Hankel-SVT unit, CN(0,1) + rank-K/2 exponentials, tau = sqrt(m)+sqrt(n), "
+                        "batch 2N (slices 1), cold solves", "points": out}
 
 
 def reference_arm(args, dist, rank, world):

@@ -1,6 +1,9 @@
 """GPU parity of the batched Hankel-SVT unit (BASELINE config 5) against the
-oracle on the sweep's synthetic inputs, over the shapes this build supports
-(d = min(p, Nc K) <= 128), plus size-independent properties at full batch."""
+oracle on the sweep's synthetic inputs: every sweep point with d = min(p, Nc K)
+<= 128 (singular values and adjoints), every wide point with 128 < d <= 248
+(adjoints: the large-d subspace path has no exact singular-value output),
+loud NotImplementedError for the rest; plus size-independent properties at
+full batch."""
 import numpy as np
 import pytest
 
@@ -79,7 +82,32 @@ def test_full_batch_properties(gpu):
     assert lhs <= rhs * (1 + 1e-4)
 
 
-def test_unsupported_large_d_fails_loudly(gpu):
+ALL = [(n, nc, k) for n in (128, 256, 512) for nc in (1, 8, 32) for k in (7, 15, 31)]
+BIG_WIDE = [(n, nc, k) for n, nc, k in ALL if 128 < min(n - k + 1, nc * k) <= 248 and nc * k > n - k + 1]
+UNSUPPORTED = [(n, nc, k) for n, nc, k in ALL if min(n - k + 1, nc * k) > 128 and (n, nc, k) not in BIG_WIDE]
+
+
+@pytest.mark.parametrize("n,nc,k", BIG_WIDE)
+def test_sweep_point_large_d_parity(gpu, n, nc, k):
+    from paper_2107_11650_b200 import synth
+    v = synth.sweep_vectors(n, nc, k, 4)
+    tau = synth.sweep_tau(n, nc, k)
+    p = n - k + 1
+    adj, _ = gpu.hankel_svt_batched(v, p, tau, want_sv=False)
+    adj_o, _ = O.hankel_svt_unit(v, p, tau)
+    assert rel(adj, adj_o) < TOL
+
+
+@pytest.mark.parametrize("n,nc,k", UNSUPPORTED)
+def test_unsupported_sweep_points_fail_loudly(gpu, n, nc, k):
+    from paper_2107_11650_b200 import synth
+    v = synth.sweep_vectors(n, nc, k, 2)
+    with pytest.raises(NotImplementedError):
+        gpu.hankel_svt_batched(v, n - k + 1, synth.sweep_tau(n, nc, k), want_sv=False)
+
+
+def test_exact_singular_values_need_full_solver(gpu):
+    """The exact singular-value output needs the full eigen-solver (d <= 128)."""
     from paper_2107_11650_b200 import synth
     v = synth.sweep_vectors(256, 32, 15, 2)
     with pytest.raises(NotImplementedError):
