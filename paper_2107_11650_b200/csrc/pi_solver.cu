@@ -1092,9 +1092,14 @@ void hankel_svt_batched_device(const float2* vecs, int batch, int nc, int n, int
     Fc.Vs = vsub;
     Fc.fallback = flags;
     spc.sweeps_out = sweeps_out ? sweeps_out + b0 : nullptr;
-    spc.q_cold = 6;
+    // one-shot (cold) solves: a 32-column level 1 with 4 QR passes; matrices
+    // whose rank above tau comes near the block go to the 48-column level 2
+    // (3 passes from level 1's block), then the full solver
+    static const int unit_q = std::getenv("SHLR_UNIT_Q") ? std::atoi(std::getenv("SHLR_UNIT_Q")) : 4;
+    static const int unit_kb = std::getenv("SHLR_UNIT_KB1") ? std::atoi(std::getenv("SHLR_UNIT_KB1")) : kSubspaceKB1;
+    spc.q_cold = unit_q;
     spc.q_warm = 3;
-    if (!sv && !std::getenv("SHLR_FULL_SVT") && launch_hankel_svt_levels(spc, nb, stream, kSubspaceKB) > 0) {
+    if (!sv && !std::getenv("SHLR_FULL_SVT") && launch_hankel_svt_levels(spc, nb, stream, unit_kb) > 0) {
       if (dp > 128) {  // large-d variant: nothing behind level 2
         std::vector<int> hf(nb);
         SHLR_CUDA(cudaMemcpyAsync(hf.data(), flags, nb * sizeof(int), cudaMemcpyDeviceToHost, stream));
