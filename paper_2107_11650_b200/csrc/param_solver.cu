@@ -34,6 +34,7 @@ namespace {
 using util::block_sum;
 using util::block_sum_all;
 using util::dalloc;
+using util::dalloc_s;
 using util::grid_for;
 using util::kThreads;
 
@@ -318,34 +319,34 @@ ParamPlan::ParamPlan(const ParamConfig& cfg, const double* y, const uint8_t* mas
   for (int k = 0; k < N; ++k) wcNf[k] = make_float2((float)wN[2 * k], (float)wN[2 * k + 1]);
 
   // ---- device buffers
-  x0_ = dalloc<float2>(nel_);
-  yk_ = dalloc<float2>(nel_);
-  x_ = dalloc<float2>(nel_);
-  xold_ = dalloc<float2>(nel_);
-  r_ = dalloc<float2>(nel_);
-  p_ = dalloc<float2>(nel_);
-  bk_ = dalloc<float2>(nel_);
-  hpe_ = dalloc<float2>(nel_);
-  ximg_ = dalloc<float2>(nel_);
-  hecho_ = dalloc<float2>(nel_);
-  dg_ = dalloc<float>((size_t)L * N);
-  hpe0_ = dalloc<float2>(N);
-  hecho0_ = dalloc<float>(L);
-  wcN_ = dalloc<float2>(N);
-  halt_ = dalloc<int>(S);
-  have_v_ = dalloc<int>(1);
-  ctl_ = dalloc<ParamSliceCtl>(S);
-  log_ = dalloc<double>((size_t)S * std::max(cfg.max_outer, 1) * 3);
+  x0_ = dalloc_s<float2>(nel_, stream_);
+  yk_ = dalloc_s<float2>(nel_, stream_);
+  x_ = dalloc_s<float2>(nel_, stream_);
+  xold_ = dalloc_s<float2>(nel_, stream_);
+  r_ = dalloc_s<float2>(nel_, stream_);
+  p_ = dalloc_s<float2>(nel_, stream_);
+  bk_ = dalloc_s<float2>(nel_, stream_);
+  hpe_ = dalloc_s<float2>(nel_, stream_);
+  ximg_ = dalloc_s<float2>(nel_, stream_);
+  hecho_ = dalloc_s<float2>(nel_, stream_);
+  dg_ = dalloc_s<float>((size_t)L * N, stream_);
+  hpe0_ = dalloc_s<float2>(N, stream_);
+  hecho0_ = dalloc_s<float>(L, stream_);
+  wcN_ = dalloc_s<float2>(N, stream_);
+  halt_ = dalloc_s<int>(S, stream_);
+  have_v_ = dalloc_s<int>(1, stream_);
+  ctl_ = dalloc_s<ParamSliceCtl>(S, stream_);
+  log_ = dalloc_s<double>((size_t)S * std::max(cfg.max_outer, 1) * 3, stream_);
   {
     const int e = std::max(cfg.Ppe, Bpe_ * qpe_), d = std::min(cfg.Ppe, Bpe_ * qpe_);
     dpe_elems_ = (size_t)S * L * e * d;
     dp_pe_ = svt_padded_dim(d);
-    dpe_ = dalloc<float2>(dpe_elems_);
-    vpe_ = dalloc<float2>((size_t)S * L * dp_pe_ * dp_pe_);
-    vspe_ = dalloc<float2>((size_t)S * L * svt_subspace_store_dim(d) * kSubspaceKB);
-    vspe2_ = dalloc<float2>((size_t)S * L * svt_subspace_store_dim(d) * (d > 128 ? kSubspaceKBBig : kSubspaceKB));
-    fallback_ = dalloc<int>((size_t)S * L);
-    diag_ = dalloc<int>((size_t)S * L);
+    dpe_ = dalloc_s<float2>(dpe_elems_, stream_);
+    vpe_ = dalloc_s<float2>((size_t)S * L * dp_pe_ * dp_pe_, stream_);
+    vspe_ = dalloc_s<float2>((size_t)S * L * svt_subspace_store_dim(d) * kSubspaceKB, stream_);
+    vspe2_ = dalloc_s<float2>((size_t)S * L * svt_subspace_store_dim(d) * (d > 128 ? kSubspaceKBBig : kSubspaceKB), stream_);
+    fallback_ = dalloc_s<int>((size_t)S * L, stream_);
+    diag_ = dalloc_s<int>((size_t)S * L, stream_);
     SHLR_CUDA(cudaMemsetAsync(diag_, 0, sizeof(int) * S * L, stream_));
     SHLR_CUDA(cudaMemsetAsync(fallback_, 0, sizeof(int) * S * L, stream_));
   }
@@ -353,8 +354,8 @@ ParamPlan::ParamPlan(const ParamConfig& cfg, const double* y, const uint8_t* mas
     const int e = std::max(cfg.Ppar, J * qpar_), d = std::min(cfg.Ppar, J * qpar_);
     decho_elems_ = (size_t)S * N * e * d;
     dp_echo_ = svt_padded_dim(d);
-    decho_ = dalloc<float2>(decho_elems_);
-    vecho_ = dalloc<float2>((size_t)S * N * dp_echo_ * dp_echo_);
+    decho_ = dalloc_s<float2>(decho_elems_, stream_);
+    vecho_ = dalloc_s<float2>((size_t)S * N * dp_echo_ * dp_echo_, stream_);
   }
   SHLR_CUDA(cudaMemcpyAsync(dg_, dg.data(), dg.size() * sizeof(float), cudaMemcpyHostToDevice, stream_));
   SHLR_CUDA(cudaMemcpyAsync(hpe0_, hpe0.data(), N * sizeof(float2), cudaMemcpyHostToDevice, stream_));
@@ -365,8 +366,8 @@ ParamPlan::ParamPlan(const ParamConfig& cfg, const double* y, const uint8_t* mas
   // ---- data: y (fp64) -> complex64; dataset: iFFT along FE (parammap.cpp:32);
   // then the masked PE k-space x0 and lambda * x0
   {
-    double* y_d = dalloc<double>(2 * nel_);
-    uint8_t* m_d = dalloc<uint8_t>((size_t)N * L);
+    double* y_d = dalloc_s<double>(2 * nel_, stream_);
+    uint8_t* m_d = dalloc_s<uint8_t>((size_t)N * L, stream_);
     SHLR_CUDA(cudaMemcpyAsync(y_d, y, 2 * nel_ * sizeof(double), cudaMemcpyHostToDevice, stream_));
     SHLR_CUDA(cudaMemcpyAsync(m_d, mask, (size_t)N * L, cudaMemcpyHostToDevice, stream_));
     k_p_from_double<<<grid_for(nel_), kThreads, 0, stream_>>>(y_d, r_, nel_);
@@ -383,9 +384,9 @@ ParamPlan::ParamPlan(const ParamConfig& cfg, const double* y, const uint8_t* mas
     k_p_prep<<<grid_for(nel_), kThreads, 0, stream_>>>(hyb, m_d, S, N, L, J, (float)cfg.lambda, x0_, yk_);
     SHLR_LAUNCH_CHECK();
     SHLR_CUDA(cudaStreamSynchronize(stream_));
-    SHLR_CUDA(cudaFree(y_d));
-    SHLR_CUDA(cudaFree(m_d));
-    if (twM) SHLR_CUDA(cudaFree(twM));
+    SHLR_CUDA(cudaFreeAsync(y_d, stream_));
+    SHLR_CUDA(cudaFreeAsync(m_d, stream_));
+    if (twM) SHLR_CUDA(cudaFreeAsync(twM, stream_));
   }
   SHLR_CUDA(cudaFuncSetAttribute(k_p_cg, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
   reset();
@@ -398,7 +399,7 @@ ParamPlan::~ParamPlan() {
   void* bufs[] = {x0_, yk_, x_, xold_, r_, p_, bk_, hpe_, ximg_, hecho_, dg_, hpe0_, hecho0_, wcN_, twN_,
                   dpe_, decho_, vpe_, vecho_, vspe_, vspe2_, fallback_, diag_, halt_, have_v_, ctl_, log_};
   for (void* b : bufs)
-    if (b) cudaFree(b);
+    if (b) cudaFreeAsync(b, stream_);
   if (ev0_) cudaEventDestroy(ev0_);
   if (ev1_) cudaEventDestroy(ev1_);
   if (evA_) cudaEventDestroy(evA_);
@@ -595,7 +596,7 @@ void ParamPlan::download(double* x_out, std::vector<int>* outer, std::vector<dou
   const int S = cfg_.S, N = cfg_.N, L = cfg_.L, J = cfg_.J;
   ParamToImageOp op{x_, r_, N, L, J, nullptr};
   launch_fft_axis<ParamToImageOp, true>(op, tN_, S, L * J, std::min(16, L * J), stream_);
-  double* xd = dalloc<double>(2 * nel_);
+  double* xd = dalloc_s<double>(2 * nel_, stream_);
   k_p_to_double<<<grid_for(nel_), kThreads, 0, stream_>>>(r_, xd, nel_);
   SHLR_LAUNCH_CHECK();
   std::vector<ParamSliceCtl> hc(S);
@@ -605,7 +606,7 @@ void ParamPlan::download(double* x_out, std::vector<int>* outer, std::vector<dou
   SHLR_CUDA(cudaMemcpyAsync(hc.data(), ctl_, S * sizeof(ParamSliceCtl), cudaMemcpyDeviceToHost, stream_));
   SHLR_CUDA(cudaMemcpyAsync(lg.data(), log_, lg.size() * sizeof(double), cudaMemcpyDeviceToHost, stream_));
   SHLR_CUDA(cudaStreamSynchronize(stream_));
-  SHLR_CUDA(cudaFree(xd));
+  SHLR_CUDA(cudaFreeAsync(xd, stream_));
   *error = 0;
   if (outer) outer->assign(S, 0);
   if (final_rel) final_rel->assign(S, 1.0);

@@ -25,6 +25,7 @@ namespace {
 
 using util::block_sum;
 using util::dalloc;
+using util::dalloc_s;
 using util::grid_for;
 using util::kThreads;
 
@@ -605,7 +606,7 @@ FftTwiddles make_twiddles(int n, float2** dev_storage, cudaStream_t stream) {
     const double ang = -2.0 * M_PI * (double)k / (double)n;
     tw[k] = make_float2((float)std::cos(ang), (float)std::sin(ang));
   }
-  float2* d = dalloc<float2>(n);
+  float2* d = dalloc_s<float2>(n, stream);  // freed with cudaFreeAsync by the owner
   SHLR_CUDA(cudaMemcpyAsync(d, tw.data(), n * sizeof(float2), cudaMemcpyHostToDevice, stream));
   *dev_storage = d;
   FftTwiddles t;
@@ -657,44 +658,44 @@ PiPlan::PiPlan(const PiConfig& cfg, const double* y, const uint8_t* mask, size_t
   for (int k = 0; k < M; ++k) wcMf[k] = make_float2((float)wM[2 * k], (float)wM[2 * k + 1]);
 
   // ---- device buffers
-  yk_ = dalloc<float2>(nel_);
-  x_ = dalloc<float2>(nel_);
-  xold_ = dalloc<float2>(nel_);
-  r_ = dalloc<float2>(nel_);
-  p_ = dalloc<float2>(nel_);
-  bk_ = dalloc<float2>(nel_);
-  tmp_ = dalloc<float2>(nel_);
-  srow_ = dalloc<float2>(nel_);
-  scol_ = dalloc<float2>(nel_);
-  hrow_ = dalloc<float2>(nel_);
-  hcol_ = dalloc<float2>(nel_);
-  dg_ = dalloc<float>((size_t)M * N);
-  hrow0_ = dalloc<float2>(N);
-  hcol0_ = dalloc<float2>(M);
-  wcN_ = dalloc<float2>(N);
-  wcM_ = dalloc<float2>(M);
-  partials_ = dalloc<double>(4 * (size_t)std::max(red_blocks_, M));
-  ctl_ = dalloc<SolverCtl>(1);
-  log_ = dalloc<double>(3 * (size_t)std::max(cfg.max_outer, 1));
+  yk_ = dalloc_s<float2>(nel_, stream_);
+  x_ = dalloc_s<float2>(nel_, stream_);
+  xold_ = dalloc_s<float2>(nel_, stream_);
+  r_ = dalloc_s<float2>(nel_, stream_);
+  p_ = dalloc_s<float2>(nel_, stream_);
+  bk_ = dalloc_s<float2>(nel_, stream_);
+  tmp_ = dalloc_s<float2>(nel_, stream_);
+  srow_ = dalloc_s<float2>(nel_, stream_);
+  scol_ = dalloc_s<float2>(nel_, stream_);
+  hrow_ = dalloc_s<float2>(nel_, stream_);
+  hcol_ = dalloc_s<float2>(nel_, stream_);
+  dg_ = dalloc_s<float>((size_t)M * N, stream_);
+  hrow0_ = dalloc_s<float2>(N, stream_);
+  hcol0_ = dalloc_s<float2>(M, stream_);
+  wcN_ = dalloc_s<float2>(N, stream_);
+  wcM_ = dalloc_s<float2>(M, stream_);
+  partials_ = dalloc_s<double>(4 * (size_t)std::max(red_blocks_, M), stream_);
+  ctl_ = dalloc_s<SolverCtl>(1, stream_);
+  log_ = dalloc_s<double>(3 * (size_t)std::max(cfg.max_outer, 1), stream_);
   const int er = std::max(cfg.Pr, B_ * qr_), dr = std::min(cfg.Pr, B_ * qr_);
   const int ec = std::max(cfg.Pc, B_ * qc_), dc = std::min(cfg.Pc, B_ * qc_);
   d_row_elems_ = (size_t)M * er * dr;
   d_col_elems_ = (size_t)N * ec * dc;
-  drow_ = dalloc<float2>(d_row_elems_);
-  dcol_ = dalloc<float2>(d_col_elems_);
+  drow_ = dalloc_s<float2>(d_row_elems_, stream_);
+  dcol_ = dalloc_s<float2>(d_col_elems_, stream_);
   svt_dp_ = svt_padded_dim(std::max(dr, dc));
-  vrow_ = dalloc<float2>((size_t)M * svt_dp_ * svt_dp_);
-  vcol_ = dalloc<float2>((size_t)N * svt_dp_ * svt_dp_);
-  sweeps_ = dalloc<int>((size_t)(M + N));
+  vrow_ = dalloc_s<float2>((size_t)M * svt_dp_ * svt_dp_, stream_);
+  vcol_ = dalloc_s<float2>((size_t)N * svt_dp_ * svt_dp_, stream_);
+  sweeps_ = dalloc_s<int>((size_t)(M + N), stream_);
   const int sdim = svt_subspace_store_dim(std::max(dr, dc));
-  vsrow_ = dalloc<float2>((size_t)M * sdim * kSubspaceKB);
-  vscol_ = dalloc<float2>((size_t)N * sdim * kSubspaceKB);
+  vsrow_ = dalloc_s<float2>((size_t)M * sdim * kSubspaceKB, stream_);
+  vscol_ = dalloc_s<float2>((size_t)N * sdim * kSubspaceKB, stream_);
   {
     const int kb2 = std::max(dr, dc) > 128 ? kSubspaceKBBig : kSubspaceKB;
-    vs2row_ = dalloc<float2>((size_t)M * sdim * kb2);
-    vs2col_ = dalloc<float2>((size_t)N * sdim * kb2);
+    vs2row_ = dalloc_s<float2>((size_t)M * sdim * kb2, stream_);
+    vs2col_ = dalloc_s<float2>((size_t)N * sdim * kb2, stream_);
   }
-  fallback_ = dalloc<int>((size_t)(M + N));
+  fallback_ = dalloc_s<int>((size_t)(M + N), stream_);
   SHLR_CUDA(cudaMemsetAsync(fallback_, 0, sizeof(int) * (M + N), stream_));
   if (const char* s = std::getenv("SHLR_Q_COLD")) q_cold_ = std::atoi(s);
   if (const char* s = std::getenv("SHLR_Q_WARM")) q_warm_ = std::atoi(s);
@@ -704,13 +705,13 @@ PiPlan::PiPlan(const PiConfig& cfg, const double* y, const uint8_t* mask, size_t
   if (const char* s = std::getenv("SHLR_RR_ABS")) rr_tol_abs_ = (float)std::atof(s);
   if (const char* s = std::getenv("SHLR_RR_TAIL")) rr_tail_ = (float)std::atof(s);
   if (std::getenv("SHLR_PHASE_CLK")) {
-    phase_clk_ = dalloc<long long>((size_t)(M + N) * kPhaseSlots);
+    phase_clk_ = dalloc_s<long long>((size_t)(M + N) * kPhaseSlots, stream_);
     SHLR_CUDA(cudaMemsetAsync(phase_clk_, 0, sizeof(long long) * kPhaseSlots * (M + N), stream_));
   }
   if (cfg.debug_sv_iter > 0) {
     if (dr != dc) throw InvalidArg("debug singular values need equal row/column d");
     d_sv_ = dr;
-    sv_ = dalloc<float>((size_t)(M + N) * dr);
+    sv_ = dalloc_s<float>((size_t)(M + N) * dr, stream_);
   }
   SHLR_CUDA(cudaMemcpyAsync(dg_, dg.data(), dg.size() * sizeof(float), cudaMemcpyHostToDevice, stream_));
   SHLR_CUDA(cudaMemcpyAsync(hrow0_, hN.data(), N * sizeof(float2), cudaMemcpyHostToDevice, stream_));
@@ -722,28 +723,28 @@ PiPlan::PiPlan(const PiConfig& cfg, const double* y, const uint8_t* mask, size_t
 
   // data: y (fp64) -> masked complex64 x0 and lambda*y
   {
-    x0_ = dalloc<float2>(nel_);
-    double* y_d = dalloc<double>(2 * nel_);
-    uint8_t* m_d = dalloc<uint8_t>(mask_rows * (size_t)N);
+    x0_ = dalloc_s<float2>(nel_, stream_);
+    double* y_d = dalloc_s<double>(2 * nel_, stream_);
+    uint8_t* m_d = dalloc_s<uint8_t>(mask_rows * (size_t)N, stream_);
     SHLR_CUDA(cudaMemcpyAsync(y_d, y, 2 * nel_ * sizeof(double), cudaMemcpyHostToDevice, stream_));
     SHLR_CUDA(cudaMemcpyAsync(m_d, mask, mask_rows * (size_t)N, cudaMemcpyHostToDevice, stream_));
     k_init_data<<<grid_for(nel_), kThreads, 0, stream_>>>(y_d, m_d, (int)mask_rows, M, N, J,
                                                           cfg.lambda, x0_, yk_);
     SHLR_LAUNCH_CHECK();
     SHLR_CUDA(cudaStreamSynchronize(stream_));
-    SHLR_CUDA(cudaFree(y_d));
-    SHLR_CUDA(cudaFree(m_d));
+    SHLR_CUDA(cudaFreeAsync(y_d, stream_));
+    SHLR_CUDA(cudaFreeAsync(m_d, stream_));
   }
 
   if (cfg.spirit) {
     if (!spirit_w || spirit_k == 0) throw InvalidArg("spirit enabled without kernels");
     const int JJ = J * J;
     const size_t npl = (size_t)M * N * JJ;
-    double* w_d = dalloc<double>(2 * spirit_k * spirit_k * JJ);
+    double* w_d = dalloc_s<double>(2 * spirit_k * spirit_k * JJ, stream_);
     SHLR_CUDA(cudaMemcpyAsync(w_d, spirit_w, 2 * spirit_k * spirit_k * JJ * sizeof(double),
                               cudaMemcpyHostToDevice, stream_));
-    float2* conv = dalloc<float2>(npl);
-    float2* tmpc = dalloc<float2>(npl);
+    float2* conv = dalloc_s<float2>(npl, stream_);
+    float2* tmpc = dalloc_s<float2>(npl, stream_);
     k_spirit_conv<<<grid_for(npl), kThreads, 0, stream_>>>(w_d, (int)spirit_k, M, N, J, conv);
     SHLR_LAUNCH_CHECK();
     // maps = ifft2c(conv) per plane: axis 1 then axis 0 over [M][N][JJ]
@@ -753,15 +754,15 @@ PiPlan::PiPlan(const PiConfig& cfg, const double* y, const uint8_t* mask, size_t
       StridedCopyOp op0{tmpc, conv, 0, (long long)N * JJ, 1};
       launch_fft_axis<StridedCopyOp, true>(op0, tM_, 1, N * JJ, 16, stream_);
     }
-    pmat_ = dalloc<float2>(npl);
+    pmat_ = dalloc_s<float2>(npl, stream_);
     k_spirit_pmat<<<grid_for(npl), kThreads, 0, stream_>>>(conv, M * N, J, pmat_);
     SHLR_LAUNCH_CHECK();
     SHLR_CUDA(cudaStreamSynchronize(stream_));
-    SHLR_CUDA(cudaFree(conv));
-    SHLR_CUDA(cudaFree(tmpc));
-    SHLR_CUDA(cudaFree(w_d));
-    ap_ = dalloc<float2>(nel_);
-    tmp2_ = dalloc<float2>(nel_);
+    SHLR_CUDA(cudaFreeAsync(conv, stream_));
+    SHLR_CUDA(cudaFreeAsync(tmpc, stream_));
+    SHLR_CUDA(cudaFreeAsync(w_d, stream_));
+    ap_ = dalloc_s<float2>(nel_, stream_);
+    tmp2_ = dalloc_s<float2>(nel_, stream_);
   }
   SHLR_CUDA(cudaFuncSetAttribute(k_spirit_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
   SHLR_CUDA(cudaFuncSetAttribute(k_spirit_rows_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
@@ -776,7 +777,7 @@ PiPlan::~PiPlan() {
                   hrow0_, hcol0_, drow_, dcol_, wcN_, wcM_, pmat_, twM_, twN_, sv_, partials_,
                   ctl_, log_, x0_, vrow_, vcol_, sweeps_, vsrow_, vscol_, vs2row_, vs2col_, fallback_};
   for (void* b : bufs)
-    if (b) cudaFree(b);
+    if (b) cudaFreeAsync(b, stream_);
   if (ev0_) cudaEventDestroy(ev0_);
   if (ev1_) cudaEventDestroy(ev1_);
   if (evA_) cudaEventDestroy(evA_);
@@ -999,7 +1000,7 @@ void PiPlan::download(double* x_out, size_t* outer_iters, double* final_rel,
   launch_fft_axis<StridedCopyOp, true>(op1, tN_, M, J, J, stream_);
   StridedCopyOp op0{tmp_, bk_, 0, NJ, 1};
   launch_fft_axis<StridedCopyOp, true>(op0, tM_, 1, N * J, 16, stream_);
-  double* xd = dalloc<double>(2 * nel_);
+  double* xd = dalloc_s<double>(2 * nel_, stream_);
   k_to_double<<<grid_for(nel_), kThreads, 0, stream_>>>(bk_, xd, nel_);
   SHLR_LAUNCH_CHECK();
   SolverCtl hc;
@@ -1008,7 +1009,7 @@ void PiPlan::download(double* x_out, size_t* outer_iters, double* final_rel,
   SHLR_CUDA(cudaMemcpyAsync(&hc, ctl_, sizeof(SolverCtl), cudaMemcpyDeviceToHost, stream_));
   SHLR_CUDA(cudaMemcpyAsync(lg.data(), log_, lg.size() * sizeof(double), cudaMemcpyDeviceToHost, stream_));
   SHLR_CUDA(cudaStreamSynchronize(stream_));
-  SHLR_CUDA(cudaFree(xd));
+  SHLR_CUDA(cudaFreeAsync(xd, stream_));
   *outer_iters = (size_t)hc.outer;
   *final_rel = hc.outer > 0 ? hc.relchange : 1.0;
   *error = hc.error;
@@ -1165,7 +1166,8 @@ void fft_along_axis_host(double* data, const size_t* dims, int ndim, int axis, b
   cudaFree(dd);
   cudaFree(a);
   cudaFree(b);
-  cudaFree(tw_storage);
+  cudaFreeAsync(tw_storage, st);
+  cudaStreamSynchronize(st);
   cudaStreamDestroy(st);
 }
 

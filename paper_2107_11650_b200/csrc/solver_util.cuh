@@ -4,6 +4,7 @@
 #pragma once
 
 #include <algorithm>
+#include <cstdint>
 #include <cmath>
 #include <vector>
 
@@ -50,6 +51,28 @@ template <class T>
 inline T* dalloc(size_t n) {
   T* p = nullptr;
   SHLR_CUDA(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
+  return p;
+}
+
+// Stream-ordered allocation from the device's default pool, which is told to
+// keep freed memory (release threshold: unlimited), so a plan created after
+// another one was destroyed reuses its memory without cudaMalloc/cudaFree.
+inline void keep_pool_memory() {
+  static bool done = false;
+  if (done) return;
+  int dev = 0;
+  SHLR_CUDA(cudaGetDevice(&dev));
+  cudaMemPool_t pool;
+  SHLR_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+  uint64_t thr = UINT64_MAX;
+  SHLR_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  done = true;
+}
+template <class T>
+inline T* dalloc_s(size_t n, cudaStream_t s) {
+  keep_pool_memory();
+  T* p = nullptr;
+  SHLR_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), std::max<size_t>(n, 1) * sizeof(T), s));
   return p;
 }
 
