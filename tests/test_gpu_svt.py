@@ -112,3 +112,29 @@ def test_exact_singular_values_need_full_solver(gpu):
     v = synth.sweep_vectors(256, 32, 15, 2)
     with pytest.raises(NotImplementedError):
         gpu.hankel_svt_batched(v, 242, 10.0)
+
+
+def _rank_r_vectors(n, nc, r, batch, seed):
+    """nc vectors of length n: r complex exponentials (amplitude ~4) + CN(0,1)."""
+    rng = np.random.default_rng(seed)
+    t = np.arange(n)
+    v = (rng.standard_normal((batch, nc, n)) + 1j * rng.standard_normal((batch, nc, n))) / np.sqrt(2)
+    w = rng.uniform(0, 2 * np.pi, size=(batch, 1, r, 1))
+    a = 4 * (rng.standard_normal((batch, nc, r, 1)) + 1j * rng.standard_normal((batch, nc, r, 1)))
+    return v + np.sum(a * np.exp(1j * w * t), axis=2)
+
+
+@pytest.mark.parametrize("r", [10, 30, 45])
+def test_subspace_levels(gpu, r):
+    """242 x 120 lifts with r signal components: r = 10 stays at level 1 (32
+    columns), r = 30 is handed to level 2 (48 columns), r = 45 overflows level
+    2 and is redone by the full solver -- every route matches the oracle."""
+    n, nc, k = 256, 8, 15
+    p = n - k + 1
+    v = _rank_r_vectors(n, nc, r, 6, 100 + r)
+    tau = float(np.sqrt(p) + np.sqrt(nc * k))
+    adj, _ = gpu.hankel_svt_batched(v, p, tau, want_sv=False)
+    adj_o, sv_o = O.hankel_svt_unit(v, p, tau)
+    assert rel(adj, adj_o) < TOL
+    above = (sv_o > tau).sum(axis=1)
+    assert above.min() >= min(r, 40) - 2  # the route the case is meant to take
