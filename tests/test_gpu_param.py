@@ -149,3 +149,20 @@ def test_gpu_param_errors(gpu):
     xo, _ = O.shlr_param_reconstruct_slice(y, O.SamplingMask(16, 9, np.ones((16, 9), np.uint8)),
                                            O.HankelConfig(pencil=11), O.AdmmConfig(max_outer=2, tol=1e-300))
     assert rel(x, xo) < TOL
+
+
+@pytest.mark.gpu
+def test_gpu_param_nonfinite_raises_divergence(gpu):
+    """A non-finite residual in a slice's CG raises DivergenceError
+    (solvers.cpp:35-36), as the reference's slice solve throws."""
+    A = gpu
+    y = np.ones((16, 9, 2), np.complex128)
+    y[3, 2, 1] = np.nan
+    with pytest.raises(A.DivergenceError):
+        A.shlr_param_reconstruct_slice(y, A.SamplingMask(16, 9, np.ones((16, 9), np.uint8)),
+                                       A.HankelConfig(pencil=11), A.AdmmConfig(max_outer=2))
+    ds = A.ParameterDataset(np.ones((2, 16, 9, 2), np.complex128) * (1 + 1j), [10.0 * (e + 1) for e in range(9)])
+    ds.data[1, 4, 4, 0] = np.inf
+    with pytest.raises(A.DivergenceError):
+        A.recon_param_dataset(ds, A.SamplingMask(16, 9, np.ones((16, 9), np.uint8)), A.HankelConfig(pencil=11),
+                              A.AdmmConfig(max_outer=2))
