@@ -436,18 +436,18 @@ def param_workload(args, dist, world, fp32_peak):
 
 WORKLOAD3 = ("config3: 256x256x32 coils (two staggered rings), SHLR-V (virtual coils), R=6 2D random mask "
              "(mask_random2d(256,256,1/6,24): the reference's nearest generator to BASELINE's Poisson disc), "
-             "Hankel window K=11 (pencil 246, 512 lifted 246x704 matrices/iter, d=246), 30 outer iterations")
+             "Hankel window K=11 (pencil 246, 512 lifted 246x704 matrices/iter, d=246), 50 outer iterations")
 
 
 def large_d_workload(args, dist, world, fp32_peak):
-    """BASELINE config 3 on the same GPU (30 iterations; see make_c3_golden.py for
-    why 30): the large-d subspace SVT path.  Timed over iterations 1-30 as a
-    whole (the rank above the threshold, and with it the share of matrices
-    that need the 64-column fallback level, grows with the iteration)."""
+    """BASELINE config 3 on the same GPU (50 iterations, the reference default):
+    the large-d subspace SVT path.  Timed over iterations 1-50 as a whole (the
+    rank above the threshold, and with it the share of matrices at level 2
+    (64 columns) and level 3 (deflated remainder), grows with the iteration)."""
     sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
     import make_c3_golden as G
     from paper_2107_11650_b200 import api as A
-    iters = 30
+    iters = 50
     y, bits = G.make_inputs()
     mask = A.SamplingMask(256, 256, bits)
     hcfg = A.HankelConfig(pencil=246)
@@ -480,7 +480,7 @@ def large_d_workload(args, dist, world, fp32_peak):
         t_e2e = max_over_ranks(dist, time.perf_counter() - t0)
         out["e2e"] = {"value": world * st.outer_iters / t_e2e, "unit": "iterations/s",
                       "h2d_bytes_per_step": int(y.size * 16 + bits.size), "d2h_bytes_per_step": int(y.size * 16),
-                      "step": "one 30-iteration shlr_cuda_pi_reconstruct call with host buffers"}
+                      "step": "one 50-iteration shlr_cuda_pi_reconstruct call with host buffers"}
     return out
 
 

@@ -17,6 +17,8 @@
 
 #include "hankel_svt.cuh"
 
+#include <cstdlib>
+
 namespace shlr_b200 {
 
 namespace {
@@ -1489,6 +1491,33 @@ __device__ void hermitian_eig_tridiag(float2* H, float* scr, float* work, float2
 
 }  // namespace
 
+// M (d x KB in smem, row stride KS) <- (I - V1 V1^H) M, V1 = the first k1
+// columns of a global d x ld block (orthonormal), coefficients staged in
+// `coef` (k1 x KB smem).  Two barriers; called by the whole CTA.
+template <int KB, int KS>
+__device__ void project_out(float2* M, const float2* __restrict__ V1, int ld, int k1, int d, float2* coef) {
+  for (int t = threadIdx.x; t < k1 * KB; t += blockDim.x) {
+    const int i = t % k1, j = t / k1;
+    float2 a = make_float2(0.f, 0.f);
+#pragma unroll 4
+    for (int k = 0; k < d; ++k) cfmac(a, __ldg(V1 + (long long)k * ld + i), M[k * KS + j]);
+    coef[i * KB + j] = a;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < d * KB; t += blockDim.x) {
+    const int k = t / KB, j = t - k * KB;
+    float2 m = M[k * KS + j];
+#pragma unroll 4
+    for (int i = 0; i < k1; ++i) {
+      const float2 v = __ldg(V1 + (long long)k * ld + i), c = coef[i * KB + j];
+      m.x -= v.x * c.x - v.y * c.y;
+      m.y -= v.x * c.y + v.y * c.x;
+    }
+    M[k * KS + j] = m;
+  }
+  __syncthreads();
+}
+
 template <int DP, int KB, int R, bool BIG, bool L2>
 __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams prm) {
   constexpr int NT = kSubNT;
@@ -1514,12 +1543,19 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
   int mat;
   const SvtFamily& F = family_of(prm, blockIdx.x, mat);
   if (F.halt && F.halt[mat / F.halt_div]) return;
-  if (prm.only_flagged && !F.fallback[mat]) return;
+  if (prm.only_flagged && (prm.only_flag_value ? F.fallback[mat] != prm.only_flag_value : !F.fallback[mat]))
+    return;
   // per-matrix level flag (fallback): 0 level 1, kLevelHanded handed to
   // level 2 by level 1 in this launch, kLevelStay2 kept at level 2 from the
-  // previous iteration, kLevelOverflow beyond level 2; level 1 skips the
-  // matrices that are not at level 1
-  if (!L2 && F.fallback && (F.fallback[mat] == kLevelStay2 || F.fallback[mat] == kLevelOverflow)) return;
+  // previous iteration, kLevelDeflate split between level 2 and the deflated
+  // level 3, kLevelOverflow beyond that; level 1 skips the matrices that are
+  // not at level 1
+  if (!L2 && F.fallback &&
+      (F.fallback[mat] == kLevelStay2 || F.fallback[mat] == kLevelOverflow || F.fallback[mat] == kLevelDeflate))
+    return;
+  // level 3 (large d): SVT of the part of the matrix orthogonal to level 2's
+  // leading kDeflateK Ritz vectors, plus level 2's Z1 on that part
+  const bool defl3 = BIG && L2 && prm.deflate;
   const int tid = threadIdx.x;
   const int d = F.d, e = F.e, len = F.len, B = F.B, J = F.J;
   const bool admm = prm.mode != SVT_PLAIN;
@@ -1576,9 +1612,10 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
   // the previous iteration; the ones level 1 just handed over start from
   // level 1's fresh block (+ random columns)
   const int lvl_in = F.fallback ? F.fallback[mat] : 0;
-  const bool warm = prm.warm && *prm.warm &&
-                    (!L2 || (Vsg2 && (lvl_in == kLevelStay2 || lvl_in == kLevelOverflow)));
-  const bool seeded = L2 && !warm && lvl_in == kLevelHanded;
+  const bool warm = !defl3 && prm.warm && *prm.warm &&
+                    (!L2 || (Vsg2 && (lvl_in == kLevelStay2 || lvl_in == kLevelOverflow || lvl_in == kLevelDeflate)));
+  const bool seeded = L2 && !defl3 && !warm && lvl_in == kLevelHanded;
+  const float2* V1g = defl3 ? Vsg2 : nullptr;  // level 2's sorted Ritz vectors (its store)
   const bool stg = Dg != nullptr && !BIG;  // duals staged by cp.async (non-BIG)
 
   // ---------------------------------------------------------- spectra
@@ -1640,6 +1677,10 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
       X[k * KS + j] = v;
     }
     __syncthreads();
+    if (defl3) {  // start orthogonal to level 2's leading block (twice: CGS2)
+      project_out<KB, KS>(X, V1g, KB, kDeflateK, d, C);
+      project_out<KB, KS>(X, V1g, KB, kDeflateK, d, C);
+    }
     householder_qr<KB, KS, DP>(X, V, d, tau);
   }
 
@@ -1700,6 +1741,10 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
     __syncthreads();
     clk_pass += clock64() - clk_t;
     clk_t = clock64();
+    if (defl3) {
+      project_out<KB, KS>(X, V1g, KB, kDeflateK, d, C);
+      project_out<KB, KS>(X, V1g, KB, kDeflateK, d, C);
+    }
     if (warm && prm.inner_norm && it + 1 < iters) {
       // warm inner pass: X ~ V0 Lambda with V0 the previous (sorted) Ritz
       // vectors, so unit columns are already a well-conditioned basis; the
@@ -1881,21 +1926,28 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
   // where the shrink factor 1 - tau / sigma is ~0.  It keeps a matrix until
   // its rank falls well inside level 1's range (hysteresis).
   constexpr int kMarginHere = (BIG && L2) ? kSubspaceMarginLast : kSubspaceMargin;
+  // level 2 (large d) with too many values above the threshold and a Z1
+  // buffer: keep the leading kDeflateK Ritz pairs (Z1 = Ahat V1 f1 V1^H to
+  // HBM) and hand the rest to the deflated level 3
+  const bool to_defl = BIG && L2 && !defl3 && F.Z1 && F.Vs2 && r > KB - kMarginHere;
   if (F.fallback && tid == 0) {
-    if (L2)
-      F.fallback[mat] = r > KB - kMarginHere ? kLevelOverflow
+    if (defl3)
+      F.fallback[mat] = r > KB - kMarginHere ? kLevelOverflow : kLevelDeflate;
+    else if (L2)
+      F.fallback[mat] = to_defl ? kLevelDeflate
+                        : r > KB - kMarginHere ? kLevelOverflow
                         : r <= KB1 - 2 * kSubspaceMargin ? 0 : kLevelStay2;
     else
       F.fallback[mat] = (r > KB - kSubspaceMargin) ? kLevelHanded : 0;
   }
-  if (Vsg2)
+  if (Vsg2 && !defl3)
     for (int t = tid; t < DP * KB; t += NT) {
       const int k = t / KB, j = t - k * KB;
       Vsg2[t] = Vf[k * KS + j];
     }
   // warm start of the next ADMM iteration at level 1: the leading KB1 Ritz
   // vectors (sorted), stored even when this matrix is handed to a fallback
-  for (int t = tid; t < DP * KB1; t += NT) {
+  for (int t = tid; t < (defl3 ? 0 : DP * KB1); t += NT) {
     const int k = t / KB1, j = t - k * KB1;
     Vsg[t] = Vf[k * KS + j];
   }
@@ -1920,9 +1972,10 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
     else build_chunk<DP, CS, R>(C, wl, lofs, F, Dg ? Ds : nullptr, i0, rows, prm.inv_beta);
     __syncthreads();
     {
-      // only the first r (sorted) Ritz columns have f > 0
+      // only the first r (sorted) Ritz columns have f > 0 (Z1 mode: the
+      // leading kDeflateK)
       static_assert(NC <= 4, "NC > 4 needs more cases");
-      const int nb = (r + 15) >> 4;
+      const int nb = ((to_defl ? kDeflateK : r) + 15) >> 4;
       if (nb <= 1) chunk_block<CS, KS, 1, R, NOSPLIT>(C, Vf, Yc, Yc2, d, S.f);
       else if (nb == 2 || NC == 2) chunk_block<CS, KS, (NC >= 2 ? 2 : 1), R, NOSPLIT>(C, Vf, Yc, Yc2, d, S.f);
       else if (nb == 3 || NC == 3) chunk_block<CS, KS, (NC >= 3 ? 3 : 1), R, NOSPLIT>(C, Vf, Yc, Yc2, d, S.f);
@@ -1934,7 +1987,8 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
       float2 z[MZ];
 #pragma unroll
       for (int m = 0; m < MZ; ++m) z[m] = make_float2(0.f, 0.f);
-      for (int j = 0; j < r; ++j) {
+      const int rz = to_defl ? kDeflateK : r;
+      for (int j = 0; j < rz; ++j) {
         const float2 yv = Yc[yi * KS + j];
 #pragma unroll
         for (int m = 0; m < MZ; ++m) {
@@ -1946,6 +2000,15 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
       for (int m = 0; m < MZ; ++m) {
         const int k = c16 + 16 * m;
         if (yi < rows && k < d) {
+          if (to_defl) {  // Z1 only: level 3 finishes this matrix
+            F.Z1[(long long)mat * e * d + (long long)(i0 + yi) * d + k] = z[m];
+            continue;
+          }
+          if (defl3) {
+            const float2 z1 = __ldcg(F.Z1 + (long long)mat * e * d + (long long)(i0 + yi) * d + k);
+            z[m].x += z1.x;
+            z[m].y += z1.y;
+          }
           float2 tv = z[m];
           if (admm) {
             const float2 L = BIG ? lift_global(F, spg, wl, weighted, lofs[i0 + yi], k)
@@ -1964,7 +2027,9 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
     }
     __syncthreads();
     if (stg && i0 + R < e) stage_d_async(Ds, Dg, i0 + R, min(R, e - i0 - R), d);  // overlaps the adjoint
-    if (BIG) {
+    if (to_defl) {
+      // Z1 mode: no duals, no adjoint (level 3 finishes the matrix)
+    } else if (BIG) {
       // blocks b_lo..b_hi touch this chunk; a block whose rows continue into
       // the next chunk is carried (acc[par]), the one carried in from the
       // previous chunk is acc[par ^ 1]; complete blocks are weighted and
@@ -2135,11 +2200,23 @@ int launch_hankel_svt_levels(const SvtParams& sp, int total, cudaStream_t stream
   if (big || kb1 == kSubspaceKB1) {
     SvtParams l2 = sp;
     l2.only_flagged = sp.fam[0].fallback;
-    l2.q_cold = 3;
+    l2.q_cold = std::getenv("SHLR_L2_Q") ? std::atoi(std::getenv("SHLR_L2_Q")) : 5;
     launch_hankel_svt_level2(l2, total, stream);
     ++n;
   }
-  if (big) return n;
+  if (big) {
+    if (sp.fam[0].Z1) {  // level 3: the deflated remainder of level 2's overflow
+      SvtParams l3 = sp;
+      l3.only_flagged = sp.fam[0].fallback;
+      l3.only_flag_value = kLevelDeflate;
+      l3.deflate = 1;
+      l3.warm = nullptr;
+      l3.q_cold = std::getenv("SHLR_L3_Q") ? std::atoi(std::getenv("SHLR_L3_Q")) : 4;
+      launch_hankel_svt_level2(l3, total, stream);
+      ++n;
+    }
+    return n;
+  }
   // the full solver redoes what the last subspace level handed on (cold)
   SvtParams fs = sp;
   fs.only_flagged = sp.fam[0].fallback;

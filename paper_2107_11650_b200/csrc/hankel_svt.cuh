@@ -51,6 +51,7 @@ struct SvtFamily {
   float2* Vs;          // subspace solver: count x DP x KB dominant-subspace store
   int* fallback;       // subspace solver: per-matrix flag, 1 = rank above threshold too
                        // close to KB, the full solver must redo this matrix
+  float2* Z1;          // large d: count x e x d buffer for level 2's Z1 (nullptr: no level 3)
   float2* Vs2;         // large-d level 2: count x DP x kSubspaceKBBig store (warm start of the
                        // matrices that stay at level 2); nullptr: level 2 always starts seeded
   const int* halt;     // optional per-group stop flags: matrix `mat` is skipped when
@@ -75,6 +76,7 @@ struct SvtParams {
                             // set (fam[f].fallback); with only_flag_value != 0 (full solver):
                             // only matrices whose flag equals it
   int only_flag_value;
+  int deflate;         // large-d level 3 launch (SvtFamily::Z1, flags kLevelDeflate)
   float rr_tol_rel, rr_tol_abs;  // subspace Rayleigh-Ritz rotation tolerances (0 = defaults)
   float rr_tail;                 // pairs with both Ritz values < rr_tail * thresh^2 not rotated
   float s2_tail;                 // full solver, stage 2: same rule (0 = rotate every pair)
@@ -107,6 +109,10 @@ constexpr int kSubspaceKBBig = 64;
 constexpr int kLevelHanded = 1;    // level 1 handed the matrix to level 2 in this launch
 constexpr int kLevelOverflow = 2;  // level 2 ran out of block: reported as unsupported
 constexpr int kLevelStay2 = 3;     // stays at level 2 (warm from its own store) next iteration
+constexpr int kLevelDeflate = 4;   // large d: level 2 keeps its leading kDeflateK Ritz pairs (Z1),
+                                   // level 3 solves the orthogonal remainder
+// Ritz pairs level 2 hands to the deflation split (its converged head).
+constexpr int kDeflateK = kSubspaceKBBig - 8;
 // Padded dimension of the large-d variant for d (0 if out of range).
 inline int svt_big_padded_dim(int d) { return d <= 128 ? 0 : d <= 160 ? 160 : d <= 192 ? 192 : d <= 248 ? 248 : 0; }
 int svt_padded_dim(int d);

@@ -694,6 +694,10 @@ PiPlan::PiPlan(const PiConfig& cfg, const double* y, const uint8_t* mask, size_t
     const int kb2 = std::max(dr, dc) > 128 ? kSubspaceKBBig : kSubspaceKB;
     vs2row_ = dalloc_s<float2>((size_t)M * sdim * kb2, stream_);
     vs2col_ = dalloc_s<float2>((size_t)N * sdim * kb2, stream_);
+    if (std::max(dr, dc) > 128 && !std::getenv("SHLR_NO_DEFLATE")) {  // large-d level 3
+      z1row_ = dalloc_s<float2>(d_row_elems_, stream_);
+      z1col_ = dalloc_s<float2>(d_col_elems_, stream_);
+    }
   }
   fallback_ = dalloc_s<int>((size_t)(M + N), stream_);
   SHLR_CUDA(cudaMemsetAsync(fallback_, 0, sizeof(int) * (M + N), stream_));
@@ -775,7 +779,8 @@ PiPlan::~PiPlan() {
   if (graph_) cudaGraphDestroy(graph_);
   void* bufs[] = {yk_, x_, xold_, r_, p_, ap_, bk_, tmp_, tmp2_, dg_, srow_, scol_, hrow_, hcol_,
                   hrow0_, hcol0_, drow_, dcol_, wcN_, wcM_, pmat_, twM_, twN_, sv_, partials_,
-                  ctl_, log_, x0_, vrow_, vcol_, sweeps_, vsrow_, vscol_, vs2row_, vs2col_, fallback_};
+                  ctl_, log_, x0_, vrow_, vcol_, sweeps_, vsrow_, vscol_, vs2row_, vs2col_, z1row_, z1col_,
+                  fallback_};
   for (void* b : bufs)
     if (b) cudaFreeAsync(b, stream_);
   if (ev0_) cudaEventDestroy(ev0_);
@@ -928,6 +933,8 @@ void PiPlan::enqueue_iteration(int k, bool record_events) {
     const bool want_sv = sp.fam[0].sv != nullptr;
     sp.fam[0].Vs2 = vs2row_;
     sp.fam[1].Vs2 = vs2col_;
+    sp.fam[0].Z1 = z1row_;
+    sp.fam[1].Z1 = z1col_;
     int nl = 0;
     if (subspace_ && !want_sv && (nl = launch_hankel_svt_levels(sp, M + N, stream_, kb1_)) > 0) {
       // level 1 (32 / 48 columns), level 2 (48 / 64) for matrices whose rank
@@ -1081,6 +1088,13 @@ void hankel_svt_batched_device(const float2* vecs, int batch, int nc, int n, int
   SHLR_CUDA(cudaMallocAsync(&vsub, (size_t)chunk * svt_subspace_store_dim(F.d) * kSubspaceKB * sizeof(float2),
                             stream));
   SHLR_CUDA(cudaMallocAsync(&flags, (size_t)chunk * sizeof(int), stream));
+  // large d: level 2's store and the Z1 buffer of the deflated level 3
+  float2 *vs2 = nullptr, *z1 = nullptr;
+  if (F.d > 128) {
+    SHLR_CUDA(cudaMallocAsync(&vs2, (size_t)chunk * svt_subspace_store_dim(F.d) * kSubspaceKBBig * sizeof(float2),
+                              stream));
+    SHLR_CUDA(cudaMallocAsync(&z1, (size_t)chunk * F.e * F.d * sizeof(float2), stream));
+  }
   for (int b0 = 0; b0 < batch; b0 += chunk) {
     const int nb = std::min(chunk, batch - b0);
     SvtParams spc = sp;
@@ -1092,6 +1106,9 @@ void hankel_svt_batched_device(const float2* vecs, int batch, int nc, int n, int
     Fc.V = vscr;
     Fc.Vs = vsub;
     Fc.fallback = flags;
+    Fc.Vs2 = vs2;
+    Fc.Z1 = z1;
+    SHLR_CUDA(cudaMemsetAsync(flags, 0, (size_t)nb * sizeof(int), stream));
     spc.sweeps_out = sweeps_out ? sweeps_out + b0 : nullptr;
     // one-shot (cold) solves: a 32-column level 1 with 4 QR passes; matrices
     // whose rank above tau comes near the block go to the 48-column level 2
@@ -1117,6 +1134,8 @@ void hankel_svt_batched_device(const float2* vecs, int batch, int nc, int n, int
   SHLR_CUDA(cudaFreeAsync(vscr, stream));
   SHLR_CUDA(cudaFreeAsync(vsub, stream));
   SHLR_CUDA(cudaFreeAsync(flags, stream));
+  if (vs2) SHLR_CUDA(cudaFreeAsync(vs2, stream));
+  if (z1) SHLR_CUDA(cudaFreeAsync(z1, stream));
 }
 
 void PiPlan::debug_phases(long long* out, int n) {

@@ -16,7 +16,7 @@ ph = synth.pi_phantom(256, 256, 32, rings=2)
 mask = A.mask_random2d(256, 256, 1.0 / 6.0, 24, synth.SEED_MASK)
 y = np.where(mask.bits.astype(bool)[:, :, None], ph.kspace, 0)
 print(f"inputs {time.time() - t0:.1f}s", flush=True)
-plan = A.PiPlan(y, mask, None, A.HankelConfig(pencil=246), A.AdmmConfig(max_outer=30, tol=1e-300, enable_vc=True))
+plan = A.PiPlan(y, mask, None, A.HankelConfig(pencil=246), A.AdmmConfig(max_outer=int(os.environ.get('ITERS', 30)), tol=1e-300, enable_vc=True))
 plan.run(3)
 plan.sync()
 for k in range(3):
@@ -32,7 +32,7 @@ plan.sync()
 svt, tot, n = plan.timing()
 print(f"timing mode iters 1-3: {tot / 3:.3f} ms/iter, svt {svt / 3:.3f} ms/iter", flush=True)
 plan.set_timing(False)
-plan.run(27)
+plan.run(int(os.environ.get('ITERS', 30)) - 3)
 plan.sync()
 x, st = plan.download()
 print("iters", st.outer_iters, "finite", bool(np.isfinite(x).all()))

@@ -47,3 +47,25 @@ def test_gpu_svt_unit_large_d(gpu, n, nc, k):
     out, _ = A.hankel_svt_batched(v, p, tau, want_sv=False)
     ref, _ = O.hankel_svt_unit(v, p, tau)
     assert rel(out, ref) < TOL
+
+
+@pytest.mark.gpu
+def test_gpu_svt_unit_large_d_deflated_level3(gpu):
+    """242 x 480 lifts with ~90 singular values above the threshold: beyond the
+    64-column level 2, so level 2 keeps its leading 56 Ritz pairs (Z1) and the
+    deflated level 3 solves the orthogonal remainder (SVT(A) = SVT(A P1) +
+    SVT(A (I - P1)) for an invariant P1)."""
+    A = gpu
+    rng = np.random.default_rng(5)
+    n, nc, k, r = 256, 32, 15, 90
+    p = n - k + 1
+    t = np.arange(n)
+    v = (rng.standard_normal((4, nc, n)) + 1j * rng.standard_normal((4, nc, n))) / np.sqrt(2)
+    w = rng.uniform(0, 2 * np.pi, size=(4, 1, r, 1))
+    a = 4 * (rng.standard_normal((4, nc, r, 1)) + 1j * rng.standard_normal((4, nc, r, 1)))
+    v = v + np.sum(a * np.exp(1j * w * t), axis=2)
+    tau = float(np.sqrt(p) + np.sqrt(nc * k))
+    adj, _ = A.hankel_svt_batched(v, p, tau, want_sv=False)
+    adj_o, sv_o = O.hankel_svt_unit(v, p, tau)
+    assert (sv_o > tau).sum(axis=1).min() > 64
+    assert rel(adj, adj_o) < TOL
