@@ -6,10 +6,9 @@ matrices 246 x 704 (d = 246).  The Poisson-disc mask of BASELINE does not
 exist in the reference; the nearest reference generator,
 mask_random2d(256, 256, 1/6, 24, 11650), stands in (SURVEY 8 mapping table).
 Iteration count: 30.  (BASELINE leaves it open; the reference default is
-max_outer = 50, solvers.hpp:16-34.  The number of singular values above the
-threshold per lifted matrix grows with the iterations -- max 47 at
-iteration 25, 63 at 50 -- and the B200 large-d subspace path holds 62, so
-parity is pinned at 30.)
+max_outer = 50, solvers.hpp:16-34.  The unmodified single-threaded reference
+needs about 5 minutes per config-3 iteration on this host, so the fixture
+stops at 30; the B200 path runs all 50 -- bench.py's config-3 side workload.)
 
     python tests/golden/make_c3_golden.py inputs DIR     # writes DIR/y.cplx, DIR/m.cplx
     oracle/_ref/ref_driver pi y=DIR/y.cplx mask=DIR/m.cplx out=DIR/ref30 vc=1 \\
