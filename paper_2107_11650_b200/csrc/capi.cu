@@ -220,8 +220,8 @@ int shlr_cuda_pi_plan_download(shlr_pi_plan* plan, double* x_out, shlr_stats* st
     if (err == 2) return fail(SHLR_EDIVERGE, "cg_solve: operator not positive definite");
     if (err == 3)
       return fail(SHLR_EUNSUPPORTED,
-                  "hankel_svt: a lifted matrix with min(m, n) > 128 has more than 62 singular values "
-                  "above the threshold (the large-d subspace fallback block holds 64)");
+                  "hankel_svt: a lifted matrix with min(m, n) > 128 has more than 118 singular values "
+                  "above the threshold (large-d subspace levels 2 + 3 hold 56 + 62)");
     return SHLR_OK;
   });
 }
