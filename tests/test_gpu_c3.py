@@ -1,0 +1,44 @@
+"""BASELINE config 3 at full size against the reference library's own run.
+
+tests/golden/c3_ref30.npz holds the unmodified reference (oracle/_ref +
+oracle/ref_driver, see tests/golden/make_c3_golden.py) run for 30 ADMM
+iterations on 256 x 256 x 32 coils (two rings), SHLR-V (virtual coils),
+K = 11 -> 512 lifted 246 x 704 matrices per iteration (d = 246: the large-d
+subspace levels), the random-2D mask standing in for BASELINE's Poisson disc.
+The B200 path must reproduce the image within 1e-4 relative L2 (4 of the 32
+coils stored, and the root-sum-of-squares over all coils) and the log."""
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLDEN = os.path.join(ROOT, "tests", "golden", "c3_ref30.npz")
+TOL = 1e-4
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+@pytest.mark.gpu
+def test_c3_parity_vs_reference(gpu):
+    if not os.path.exists(GOLDEN):
+        pytest.fail("tests/golden/c3_ref30.npz missing (tests/golden/make_c3_golden.py)")
+    sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+    import make_c3_golden as G
+    g = np.load(GOLDEN)
+    y, bits = G.make_inputs()
+    A = gpu
+    log = []
+    x = A.shlr_pi_reconstruct(y, A.SamplingMask(256, 256, bits), None, A.HankelConfig(pencil=246),
+                              A.AdmmConfig(max_outer=30, tol=1e-300, enable_vc=True), log=log)
+    coils = [int(c) for c in g["coils"]]
+    assert rel(x[:, :, coils], g["x30_coils"]) < TOL
+    assert rel(np.sqrt((np.abs(x) ** 2).sum(axis=2)), g["rss30"]) < TOL
+    cg = [int(l.split("cg_iters=")[1].split()[0]) for l in log]
+    cg_ref = [int(str(l).split("cg_iters=")[1].split()[0]) for l in g["log"]]
+    assert cg == cg_ref
+    relc = np.array([float(l.split("relchange=")[1].split()[0]) for l in log])
+    np.testing.assert_allclose(relc[:5], g["relchange"][:5], rtol=2e-2)
