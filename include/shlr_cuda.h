@@ -226,6 +226,14 @@ size_t shlr_pencil_for_param(size_t pencil_param, size_t len);
 int shlr_spirit_calibrate(const double* acs, size_t a, size_t b, size_t j, size_t k,
                           double tikhonov, double* weights_out);
 
+/* The same calibration on the device in FP64: the
+ * augmented patch-matrix Gram in tiles, then per target coil the power
+ * iteration for s_max^2, the ridge shift and a Cholesky solve -- the
+ * restatement shlr_spirit_calibrate runs on the host.  Same arguments and
+ * result layout; SHLR_ECUDA without a device. */
+int shlr_cuda_spirit_calibrate(const double* acs, size_t a, size_t b, size_t j, size_t k,
+                               double tikhonov, double* weights_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -114,6 +114,8 @@ PROTOTYPES = {
     "shlr_pencil_for_param": (C.c_size_t, [C.c_size_t, C.c_size_t]),
     "shlr_spirit_calibrate": (C.c_int, [C.POINTER(C.c_double), C.c_size_t, C.c_size_t, C.c_size_t,
                                         C.c_size_t, C.c_double, C.POINTER(C.c_double)]),
+    "shlr_cuda_spirit_calibrate": (C.c_int, [C.POINTER(C.c_double), C.c_size_t, C.c_size_t, C.c_size_t,
+                                             C.c_size_t, C.c_double, C.POINTER(C.c_double)]),
 }
 
 

@@ -144,15 +144,19 @@ def mask_random2d(rows: int, cols: int, rate: float, center: int, seed: int) -> 
     return SamplingMask(rows, cols, bits.reshape(rows, cols), "random2d", seed, rate, center)
 
 
-def spirit_calibrate(acs: np.ndarray, kernel_size: int = 5, tikhonov: float = 1e-4) -> SpiritKernels:
-    """``shlr::spirit_calibrate`` (``spirit.hpp:62-64``) on an a x b x J ACS block."""
+def spirit_calibrate(acs: np.ndarray, kernel_size: int = 5, tikhonov: float = 1e-4,
+                     device: bool = False) -> SpiritKernels:
+    """``shlr::spirit_calibrate`` (``spirit.hpp:62-64``) on an a x b x J ACS block.
+    Setup, not the per-iteration path: FP64 on the host by default,
+    ``device=True`` runs the same FP64 restatement on the GPU
+    (``shlr_cuda_spirit_calibrate``)."""
     blk = _c128(acs)
     if blk.ndim != 3:
         raise ValueError("spirit_calibrate: expected a x b x J ACS")
     a, b, j = blk.shape
     w = np.zeros((kernel_size, kernel_size, j, j), np.complex128)
-    _check(lib.shlr_spirit_calibrate(_dptr(blk), a, b, j, kernel_size, tikhonov, _dptr(w)),
-           "spirit_calibrate")
+    fn = lib.shlr_cuda_spirit_calibrate if device else lib.shlr_spirit_calibrate
+    _check(fn(_dptr(blk), a, b, j, kernel_size, tikhonov, _dptr(w)), "spirit_calibrate")
     return SpiritKernels(kernel_size, j, w)
 
 

@@ -9,6 +9,11 @@
 #include "param_solver.cuh"
 #include "pi_solver.cuh"
 
+namespace shlr_b200 {
+bool spirit_calibrate_device(const double* acs, size_t a, size_t b, size_t j, size_t k, double tikhonov,
+                             double* weights_out);
+}
+
 namespace {
 
 thread_local std::string g_last_error;
@@ -471,6 +476,23 @@ int shlr_cuda_param_reconstruct(const shlr_param_args* args, double* x_out, shlr
   shlr_cuda_param_plan_destroy(plan);
   g_last_error = err;
   return rc;
+}
+
+int shlr_cuda_spirit_calibrate(const double* acs, size_t a, size_t b, size_t j, size_t k, double tikhonov,
+                               double* weights_out) {
+  return guarded([&] {
+    // spirit.cpp:24-38: the reference's argument checks
+    if (!acs || !weights_out || j == 0 || k == 0 || k % 2 == 0 || tikhonov < 0)
+      throw shlr_b200::InvalidArg("spirit_calibrate: invalid arguments");
+    if (a <= k || b <= k) throw shlr_b200::InvalidArg("spirit_calibrate: ACS region too small");
+    double energy = 0.0;
+    for (size_t i = 0; i < 2 * a * b * j; ++i) energy += acs[i] * acs[i];
+    if (energy == 0.0) throw shlr_b200::InvalidArg("spirit_calibrate: all-zero ACS");
+    require_device();
+    if (!shlr_b200::spirit_calibrate_device(acs, a, b, j, k, tikhonov, weights_out))
+      throw shlr_b200::InvalidArg("spirit_calibrate: normal matrix not positive definite");
+    return SHLR_OK;
+  });
 }
 
 }  // extern "C"

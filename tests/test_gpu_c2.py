@@ -65,3 +65,25 @@ def test_c2_resident_plan_parity(gpu, golden, inputs):
     x, st = plan.download()
     assert st.outer_iters == 50
     assert rel(x, golden["x50"]) < TOL
+
+
+@pytest.mark.gpu
+def test_c2_device_calibration_matches_reference(gpu, golden):
+    """SPIRiT calibration on the device (FP64, shlr_cuda_spirit_calibrate) gives
+    the kernels the reference's own config-2 run calibrated (spirit.cpp:22-94)."""
+    import time
+    import bench
+    from paper_2107_11650_b200 import synth
+    A = gpu
+    cfg = bench.CFG2
+    ph = synth.pi_phantom(cfg["M"], cfg["N"], cfg["J"])
+    mask = A.mask_gauss_cartesian(cfg["N"], cfg["rate"], cfg["acs"], synth.SEED_MASK)
+    y = np.where(mask.bits[0][None, :, None].astype(bool), ph.kspace, 0)
+    a0, a1 = A.acs_range(cfg["N"], cfg["acs"])
+    A.spirit_calibrate(y[:, a0:a1, :], cfg["kernel"], cfg["tikhonov"], device=True)  # warm-up
+    t0 = time.perf_counter()
+    g = A.spirit_calibrate(y[:, a0:a1, :], cfg["kernel"], cfg["tikhonov"], device=True)
+    dt = time.perf_counter() - t0
+    err = float(np.abs(g.weights - golden["kernels"]).max() / np.abs(golden["kernels"]).max())
+    print(f"device calibration {dt * 1e3:.1f} ms, max rel {err:.2e}")
+    assert err < 1e-9
