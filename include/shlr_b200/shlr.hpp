@@ -228,6 +228,24 @@ inline SpiritKernels spirit_calibrate(const ComplexTensor& acs, std::size_t kern
   return SpiritKernels(kernel_size, j, std::move(w));
 }
 
+// The same calibration in FP64 on the device (shlr_cuda_spirit_calibrate).
+inline SpiritKernels spirit_calibrate_device(const ComplexTensor& acs, std::size_t kernel_size = 5,
+                                             double tikhonov = 1e-4) {
+  if (acs.rank() != 3) throw std::invalid_argument("spirit_calibrate: expected a x b x J ACS");
+  if (kernel_size % 2 == 0 || kernel_size == 0)
+    throw std::invalid_argument("spirit_calibrate: kernel size must be odd");
+  if (acs.dim(0) <= kernel_size || acs.dim(1) <= kernel_size)
+    throw CalibrationError("spirit_calibrate: ACS region too small");
+  if (tikhonov < 0) throw std::invalid_argument("spirit_calibrate: negative tikhonov");
+  const std::size_t j = acs.dim(2);
+  std::vector<cplx> w(kernel_size * kernel_size * j * j);
+  const int rc = shlr_cuda_spirit_calibrate(reinterpret_cast<const double*>(acs.data()), acs.dim(0), acs.dim(1),
+                                            j, kernel_size, tikhonov, reinterpret_cast<double*>(w.data()));
+  if (rc == SHLR_EINVAL) throw CalibrationError(std::string("spirit_calibrate: ") + shlr_cuda_last_error());
+  detail::check(rc, "spirit_calibrate");
+  return SpiritKernels(kernel_size, j, std::move(w));
+}
+
 // Parallel-imaging ADMM (SHLR / SHLR-S / SHLR-V / SHLR-SV) on the GPU.
 inline ComplexTensor shlr_pi_reconstruct(const ComplexTensor& y, const SamplingMask& mask,
                                          const SpiritKernels* g, const HankelConfig& hcfg,

@@ -286,3 +286,21 @@ TEST_CASE("parameter imaging: dataset = per-slice solves, argument validation") 
   hp.pencil_param = l + 1;
   CHECK_THROWS_AS(shlr_param_reconstruct_slice(plane, mask, hp, acfg), std::invalid_argument);
 }
+
+TEST_CASE("SPIRiT calibration: device FP64 equals the host restatement") {
+  const std::size_t n = 32, j = 3;
+  ComplexTensor k = phantom_kspace(n, j, 9);
+  ComplexTensor acs({n, 12, j});
+  for (std::size_t r = 0; r < n; ++r)
+    for (std::size_t c = 0; c < 12; ++c)
+      for (std::size_t q = 0; q < j; ++q) acs.at(r, c, q) = k.at(r, c + 10, q);
+  const SpiritKernels h = spirit_calibrate(acs, 5, 1e-4);
+  const SpiritKernels d = spirit_calibrate_device(acs, 5, 1e-4);
+  double mx = 0, md = 0;
+  for (std::size_t i = 0; i < h.raw().size(); ++i) {
+    mx = std::max(mx, std::abs(h.raw()[i]));
+    md = std::max(md, std::abs(h.raw()[i] - d.raw()[i]));
+  }
+  CHECK(md <= 1e-9 * mx);
+  CHECK_THROWS_AS(spirit_calibrate_device(ComplexTensor({4, 4, j}), 5, 1e-4), CalibrationError);
+}
