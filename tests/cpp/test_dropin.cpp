@@ -301,6 +301,8 @@ TEST_CASE("SPIRiT calibration: device FP64 equals the host restatement") {
     mx = std::max(mx, std::abs(h.raw()[i]));
     md = std::max(md, std::abs(h.raw()[i] - d.raw()[i]));
   }
-  CHECK(md <= 1e-9 * mx);
+  // both solve the same ridge system in FP64 with different summation orders;
+  // cond(A^H A + mu^2 I) <= 1 / tikhonov^2 = 1e8
+  CHECK(md <= 1e-6 * mx);
   CHECK_THROWS_AS(spirit_calibrate_device(ComplexTensor({4, 4, j}), 5, 1e-4), CalibrationError);
 }
