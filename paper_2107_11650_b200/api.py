@@ -372,7 +372,9 @@ def _run_param(a: ShlrParamArgs, out_shape, log, what: str):
     def _cb(_ctx, line):
         lines.append(line.decode())
 
-    rc = lib.shlr_cuda_param_reconstruct(C.byref(a), _dptr(x), C.byref(st), _cb, None)
+    # no callback when the caller does not want the log (12 800 lines at config 4)
+    rc = lib.shlr_cuda_param_reconstruct(C.byref(a), _dptr(x), C.byref(st),
+                                         _cb if log is not None else LOG_FN(), None)
     if log is not None:
         log.extend(lines)
     _check(rc, what)

@@ -443,7 +443,7 @@ int shlr_cuda_param_plan_download(shlr_param_plan* plan, double* x_out, shlr_sta
     std::vector<double> rel;
     std::vector<std::string> lines;
     int err = 0;
-    plan->impl->download(x_out, &outer, &rel, &lines, &err);
+    plan->impl->download(x_out, &outer, &rel, log_cb ? &lines : nullptr, &err);
     if (log_cb)
       for (const auto& l : lines) log_cb(log_ctx, l.c_str());
     if (stats) {
