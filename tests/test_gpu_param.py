@@ -166,3 +166,19 @@ def test_gpu_param_nonfinite_raises_divergence(gpu):
     with pytest.raises(A.DivergenceError):
         A.recon_param_dataset(ds, A.SamplingMask(16, 9, np.ones((16, 9), np.uint8)), A.HankelConfig(pencil=11),
                               A.AdmmConfig(max_outer=2))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,l,j", [(20, 4, 1), (24, 3, 2), (18, 20, 3)])
+def test_gpu_param_small_and_long_echo_trains(gpu, n, l, j):
+    """Echo pencils 2 (L = 3, 4) up to 8 (L = 20: 8 x 13 J lifts), single coil."""
+    A = gpu
+    rng = np.random.default_rng(n * l)
+    y = rng.standard_normal((2, n, l, j)) + 1j * rng.standard_normal((2, n, l, j))
+    bits = np.stack([O.mask_gauss_cartesian(n, 0.5, 4, 30 + e).bits[0] for e in range(l)], axis=1)
+    acfg = A.AdmmConfig(max_outer=3, tol=1e-300, enable_vc=(j > 1))
+    x = A.recon_param_dataset(A.ParameterDataset(y, [10.0 * (e + 1) for e in range(l)]), A.SamplingMask(n, l, bits),
+                              A.HankelConfig(), acfg).data
+    xo, _ = O.recon_param_dataset(y, O.SamplingMask(n, l, bits), O.HankelConfig(),
+                                  O.AdmmConfig(max_outer=3, tol=1e-300, enable_vc=(j > 1)))
+    assert rel(x, xo) < TOL

@@ -173,3 +173,25 @@ def test_cpp_dropin_suite(gpu):
         subprocess.run(["make", "-C", os.path.join(ROOT, "tests", "cpp")], check=True)
     out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,n,j,vc,spirit", [(24, 32, 2, False, False), (40, 24, 3, True, False),
+                                             (20, 28, 1, True, False), (32, 24, 2, False, True)])
+def test_non_square_and_single_coil(gpu, m, n, j, vc, spirit):
+    """Rows use pencil_for(N), columns pencil_for(M) (solvers.cpp:113-114): a
+    non-square image has different row / column lift geometries; J = 1."""
+    A = gpu
+    y0 = phantom(m, n, j, seed=m + n)
+    mk = A.mask_gauss_cartesian(n, 0.5, 6, 3)
+    y = np.where(mk.bits[0][None, :, None].astype(bool), y0, 0)
+    kern, kern_o = None, None
+    if spirit:
+        a0, a1 = A.acs_range(n, 6)
+        kern = A.spirit_calibrate(y[:, a0:a1, :], 3)
+        kern_o = O.SpiritKernels(3, j, kern.weights)
+    acfg = A.AdmmConfig(max_outer=3, tol=1e-300, enable_vc=vc, enable_spirit=spirit)
+    x = A.shlr_pi_reconstruct(y, mk, kern, A.HankelConfig(), acfg)
+    xo, _ = O.shlr_pi_reconstruct(y, O.SamplingMask(1, n, mk.bits), kern_o, O.HankelConfig(),
+                                  O.AdmmConfig(max_outer=3, tol=1e-300, enable_vc=vc, enable_spirit=spirit))
+    assert rel(x, xo) < TOL
