@@ -347,6 +347,8 @@ def gpu_arm(args, dist, rank, world, local):
     extra = {}
     if not args.no_extra:
         extra["config4_param"] = param_workload(args, dist, world, fp32_peak)
+        if rank == 0 and not args.no_cpu:
+            extra["config4_param"]["cpu_baseline"] = param_cpu_baseline()
         extra["config3_large_d"] = large_d_workload(args, dist, world, fp32_peak)
         extra["config5_sweep"] = sweep_workload(args, fp32_peak)
 
@@ -444,6 +446,33 @@ def param_workload(args, dist, world, fp32_peak):
                       "step": "one 50-iteration recon_param_dataset call (host complex128 M x N x L x J in/out, "
                               "FE iFFT and plan setup inside)", "slice_iterations": tot[0]}
     return out
+
+
+def param_cpu_baseline(iters: int = 3):
+    """The reference (oracle/_ref/ref_driver = proj/src unmodified) on the centre
+    FE slice of config 4 for a few iterations, one core; a dataset iteration is
+    256 independent slice iterations (parammap.cpp:37-51)."""
+    if not os.path.exists(REF_DRIVER):
+        return None
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import shlr_oracle as O
+    from paper_2107_11650_b200.cplx_io import write_cplx, write_mask
+    ds, mask, _, _ = make_param_inputs()
+    hybrid = O.fft_along_axis(ds.data[:, :, :, :], 0, True)
+    tmp = tempfile.mkdtemp(prefix="shlr_ref4_")
+    try:
+        write_cplx(hybrid[128], os.path.join(tmp, "s.cplx"))
+        write_mask(mask.bits, os.path.join(tmp, "m.cplx"))
+        out = subprocess.run([REF_DRIVER, "param", "y=s.cplx", "mask=m.cplx", "out=r", "vc=1",
+                              f"pencil={CFG4['N'] - CFG4['K'] + 1}", f"max_outer={iters}", "tol=1e-300",
+                              "time=1"], cwd=tmp, capture_output=True, text=True, timeout=600).stdout
+    finally:
+        shutil.rmtree(tmp, ignore_errors=True)
+    secs = float(out.split("param seconds=")[1].split()[0])
+    per_slice_iter = secs / iters
+    return {"value": 1.0 / (CFG4["M"] * per_slice_iter), "unit": "iterations/s", "cores": 1, "kind": "reference",
+            "sample": f"reference shlr_param_reconstruct_slice on the centre FE slice, {iters} iterations "
+                      f"({per_slice_iter:.3f} s per slice-iteration), times 256 slices per dataset iteration"}
 
 
 WORKLOAD3 = ("config3: 256x256x32 coils (two staggered rings), SHLR-V (virtual coils), R=6 2D random mask "
