@@ -4,8 +4,6 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
-#include <cstdlib>
-#include <utility>
 #include <cstdio>
 #include <stdexcept>
 #include <string>
@@ -75,38 +73,6 @@ __device__ __forceinline__ void cfmac(float2& acc, float2 a, float2 b) {
 __host__ __device__ __forceinline__ int dagger_src(int i, int n) {
   // virtual_coil_dagger (proj/src/hankel.cpp:99-113): out[i] = conj(v[(2 floor(n/2) + n - i) mod n])
   return (2 * (n / 2) + n - i) % n;
-}
-
-// Programmatic dependent launch: a kernel launched with launch_pdl may start
-// while its predecessor drains; it must call pdl_wait() before touching any
-// global memory the predecessor reads or writes.  (A no-op without a
-// programmatic dependency.)
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-
-inline bool pdl_enabled() {
-  static const bool on = std::getenv("SHLR_NO_PDL") == nullptr;
-  return on;
-}
-
-template <class... KArgs, class... Args>
-inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
-                       Args&&... args) {
-  if (!pdl_enabled()) {
-    kernel<<<grid, block, smem, stream>>>(std::forward<Args>(args)...);
-    SHLR_LAUNCH_CHECK();
-    return;
-  }
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  SHLR_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
 }
 
 inline int num_sms() {

@@ -196,7 +196,6 @@ template <class Op, bool INV>
 __global__ void __launch_bounds__(kFftThreads) fft_axis_kernel(Op op, FftTwiddles tw, int outer,
                                                        int inner, int F) {
   extern __shared__ float2 fft_smem[];
-  pdl_wait();
   if (op.skip()) return;
   const int n = tw.n;
   float2* a = fft_smem;
@@ -237,7 +236,7 @@ FftTwiddles make_twiddles(int n, float2** dev_storage, cudaStream_t stream);
 
 template <class Op, bool INV>
 void launch_fft_axis(const Op& op, const FftTwiddles& tw, int outer, int inner, int F,
-                     cudaStream_t stream, bool pdl = false) {
+                     cudaStream_t stream) {
   const size_t smem = 2 * (size_t)tw.n * F * sizeof(float2);
   static bool configured = false;
   if (!configured) {
@@ -246,10 +245,6 @@ void launch_fft_axis(const Op& op, const FftTwiddles& tw, int outer, int inner, 
     configured = true;
   }
   dim3 grid((inner + F - 1) / F, outer);
-  if (pdl) {
-    launch_pdl(fft_axis_kernel<Op, INV>, grid, dim3(kFftThreads), smem, stream, op, tw, outer, inner, F);
-    return;
-  }
   fft_axis_kernel<Op, INV><<<grid, kFftThreads, smem, stream>>>(op, tw, outer, inner, F);
   SHLR_LAUNCH_CHECK();
 }

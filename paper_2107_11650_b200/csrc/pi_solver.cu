@@ -273,7 +273,6 @@ __global__ void k_cg_a_diag(const float2* __restrict__ r, float2* __restrict__ p
                             const float* __restrict__ dg, size_t nel, int J, SolverCtl* ctl,
                             double* partials) {
   __shared__ double sh[32];
-  pdl_wait();
   if (halted(ctl) || ctl->cg.done) return;
   const bool first = ctl->cg.it == 0;
   const float g = (float)ctl->cg.gamma;
@@ -321,7 +320,6 @@ __global__ void k_cg_b(float2* __restrict__ x, float2* __restrict__ r, const flo
                        const float2* __restrict__ ap, const float* __restrict__ dg, size_t nel,
                        int J, SolverCtl* ctl, double* partials, int cg_max, double cg_tol) {
   __shared__ double sh[32];
-  pdl_wait();
   if (halted(ctl) || ctl->cg.done) return;
   const float a = (float)ctl->cg.alpha;
   double s = 0.0;
@@ -428,7 +426,6 @@ __global__ void __launch_bounds__(kFftThreads) k_spirit_cols(const float2* __res
                                                      int N, int J, int PPT, const SolverCtl* ctl,
                                                      int for_x) {
   extern __shared__ float2 sm[];
-  pdl_wait();
   if (halted(ctl) || (!for_x && ctl->cg.done)) return;
   const int M = tw.n;
   const int F = PPT * J;
@@ -518,7 +515,6 @@ __global__ void __launch_bounds__(kFftThreads) k_spirit_rows_fwd(const float2* _
                                                          double* partials, int mode) {
   extern __shared__ float2 sm[];
   __shared__ double sh[32];
-  pdl_wait();
   if (halted(ctl) || (mode == 0 && ctl->cg.done)) return;
   const int N = tw.n;
   const int F = J;
@@ -813,20 +809,21 @@ void PiPlan::cg_apply_spirit(float2* in_vec, float2* out_ap, bool init) {
   const long long NJ = (long long)N * J;
   // stage 1: row iFFT (with p update)
   SpiritRowInvOp op1{r_, p_, init ? in_vec : nullptr, tmp_, NJ, J, ctl_};
-  launch_fft_axis<SpiritRowInvOp, true>(op1, tN_, M, J, J, stream_, /*pdl=*/!init);
+  launch_fft_axis<SpiritRowInvOp, true>(op1, tN_, M, J, J, stream_);
   ++launch_count_;
   // stage 2: columns
   static const int ppt_env = std::getenv("SHLR_SPIRIT_PPT") ? std::atoi(std::getenv("SHLR_SPIRIT_PPT")) : 0;
   const int ppt = ppt_env > 0 ? ppt_env : std::max(1, 8 / J);
   const size_t smem2 = 2 * (size_t)M * ppt * J * sizeof(float2);
-  launch_pdl(k_spirit_cols, dim3((N + ppt - 1) / ppt), dim3(kFftThreads), smem2, stream_, (const float2*)tmp_,
-             tmp2_, (const float2*)pmat_, tM_, N, J, ppt, (const SolverCtl*)ctl_, init ? 1 : 0);
+  k_spirit_cols<<<(N + ppt - 1) / ppt, kFftThreads, smem2, stream_>>>(tmp_, tmp2_, pmat_, tM_, N, J, ppt,
+                                                                   ctl_, init ? 1 : 0);
+  SHLR_LAUNCH_CHECK();
   ++launch_count_;
   // stage 3: row FFT + combine (+ alpha)
   const size_t smem3 = 2 * (size_t)N * J * sizeof(float2);
-  launch_pdl(k_spirit_rows_fwd, dim3(M), dim3(kFftThreads), smem3, stream_, (const float2*)tmp2_,
-             (const float2*)(init ? in_vec : p_), (const float*)dg_, out_ap, tN_, J, (float)cfg_.lambda1, ctl_,
-             partials_, init ? 1 : 0);
+  k_spirit_rows_fwd<<<M, kFftThreads, smem3, stream_>>>(tmp2_, init ? in_vec : p_, dg_, out_ap, tN_, J,
+                                                     (float)cfg_.lambda1, ctl_, partials_, init ? 1 : 0);
+  SHLR_LAUNCH_CHECK();
   ++launch_count_;
 }
 
@@ -849,10 +846,9 @@ void PiPlan::enqueue_iteration(int k, bool record_events) {
     k_cg_zero_x<<<g, kThreads, 0, stream_>>>(x_, nel_, ctl_);
     launch_count_ += 2;
     for (int it = 0; it < cfg_.cg_max; ++it) {
-      launch_pdl(k_cg_a_diag, dim3(g), dim3(kThreads), 0, stream_, (const float2*)r_, p_, (const float*)dg_,
-                 nel_, J, ctl_, partials_);
-      launch_pdl(k_cg_b, dim3(g), dim3(kThreads), 0, stream_, x_, r_, (const float2*)p_, (const float2*)nullptr,
-                 (const float*)dg_, nel_, J, ctl_, partials_, (int)cfg_.cg_max, cfg_.cg_tol);
+      k_cg_a_diag<<<g, kThreads, 0, stream_>>>(r_, p_, dg_, nel_, J, ctl_, partials_);
+      k_cg_b<<<g, kThreads, 0, stream_>>>(x_, r_, p_, nullptr, dg_, nel_, J, ctl_, partials_,
+                                         cfg_.cg_max, cfg_.cg_tol);
       launch_count_ += 2;
     }
   } else {
@@ -863,8 +859,8 @@ void PiPlan::enqueue_iteration(int k, bool record_events) {
     launch_count_ += 2;
     for (int it = 0; it < cfg_.cg_max; ++it) {
       cg_apply_spirit(p_, ap_, false);
-      launch_pdl(k_cg_b, dim3(g), dim3(kThreads), 0, stream_, x_, r_, (const float2*)p_, (const float2*)ap_,
-                 (const float*)dg_, nel_, J, ctl_, partials_, (int)cfg_.cg_max, cfg_.cg_tol);
+      k_cg_b<<<g, kThreads, 0, stream_>>>(x_, r_, p_, ap_, dg_, nel_, J, ctl_, partials_, cfg_.cg_max,
+                                         cfg_.cg_tol);
       launch_count_ += 1;
     }
   }
