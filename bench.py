@@ -351,6 +351,7 @@ def gpu_arm(args, dist, rank, world, local):
             extra["config4_param"]["cpu_baseline"] = param_cpu_baseline()
         extra["config3_large_d"] = large_d_workload(args, dist, world, fp32_peak)
         extra["config5_sweep"] = sweep_workload(args, fp32_peak)
+        extra["config1_small"] = small_workload(args, dist, world, rank, fp32_peak)
 
     value = world * args.steps / (t_max_ms * 1e-3)
     out = {
@@ -522,6 +523,58 @@ def large_d_workload(args, dist, world, fp32_peak):
         out["e2e"] = {"value": world * st.outer_iters / t_e2e, "unit": "iterations/s",
                       "h2d_bytes_per_step": int(y.size * 16 + bits.size), "d2h_bytes_per_step": int(y.size * 16),
                       "step": "one 50-iteration shlr_cuda_pi_reconstruct call with host buffers"}
+    return out
+
+
+def small_workload(args, dist, world, rank, fp32_peak):
+    """BASELINE config 1 (the reference's CPU-runnable case): 128^2 x 8 coils,
+    SHLR (no SPIRiT, no vc), R = 4 Gaussian Cartesian with 16 ACS lines,
+    K = 9 -> 256 lifted 120 x 72 matrices per iteration, 30 iterations."""
+    from paper_2107_11650_b200 import api as A
+    from paper_2107_11650_b200 import synth
+    ph = synth.pi_phantom(128, 128, 8)
+    mask = A.mask_gauss_cartesian(128, 0.25, 16, synth.SEED_MASK)
+    y = np.where(mask.bits[0][None, :, None].astype(bool), ph.kspace, 0)
+    hcfg = A.HankelConfig(pencil=120)
+    acfg = A.AdmmConfig(max_outer=max(30, args.warmup + args.steps), tol=1e-300)
+    plan = A.PiPlan(y, mask, None, hcfg, acfg)
+    plan.run(args.warmup)
+    plan.sync()
+    barrier(dist)
+    plan.run(args.steps)
+    plan.sync()
+    _, total_ms, launches = plan.timing()
+    t_max_ms = max_over_ranks(dist, total_ms)
+    plan.close()
+    out = {"workload": "config1: 128x128x8 coils, SHLR, R=4 Gaussian Cartesian + 16 ACS lines, K=9 "
+                       "(pencil 120, 256 lifted 120x72 matrices/iter), 30 outer iterations",
+           "value": world * args.steps / (t_max_ms * 1e-3), "unit": "iterations/s",
+           "ms_per_step": t_max_ms / args.steps, "gpu_launches_per_step": launches}
+    if not args.no_e2e:
+        acfg.max_outer = 30
+        A.shlr_pi_reconstruct(y, mask, None, hcfg, A.AdmmConfig(max_outer=1))
+        t0 = time.perf_counter()
+        A.shlr_pi_reconstruct(y, mask, None, hcfg, acfg)
+        t_e2e = max_over_ranks(dist, time.perf_counter() - t0)
+        out["e2e"] = {"value": world * 30 / t_e2e, "unit": "iterations/s",
+                      "h2d_bytes_per_step": int(y.size * 16 + mask.bits.size), "d2h_bytes_per_step": int(y.size * 16),
+                      "step": "one 30-iteration shlr_cuda_pi_reconstruct call with host buffers"}
+    if rank == 0 and not args.no_cpu and os.path.exists(REF_DRIVER):
+        tmp = tempfile.mkdtemp(prefix="shlr_ref1_")
+        try:
+            from paper_2107_11650_b200.cplx_io import write_cplx, write_mask
+            write_cplx(y, os.path.join(tmp, "y.cplx"))
+            write_mask(mask.bits, os.path.join(tmp, "m.cplx"))
+            res = subprocess.run([REF_DRIVER, "pi", "y=y.cplx", "mask=m.cplx", "out=r", "pencil=120", "max_outer=2",
+                                  "tol=1e-300", "replay=1", "time=1"], cwd=tmp, capture_output=True, text=True,
+                                 timeout=600).stdout
+        finally:
+            shutil.rmtree(tmp, ignore_errors=True)
+        its = [float(ln.split("=")[1]) for ln in res.splitlines() if ln.startswith("iter_seconds=")]
+        if its:
+            out["cpu_baseline"] = {"value": 1.0 / statistics.mean(its), "unit": "iterations/s", "cores": 1,
+                                   "kind": "reference",
+                                   "sample": f"oracle/_ref/ref_driver, {len(its)} config-1 iterations, one core"}
     return out
 
 
