@@ -195,3 +195,20 @@ def test_non_square_and_single_coil(gpu, m, n, j, vc, spirit):
     xo, _ = O.shlr_pi_reconstruct(y, O.SamplingMask(1, n, mk.bits), kern_o, O.HankelConfig(),
                                   O.AdmmConfig(max_outer=3, tol=1e-300, enable_vc=vc, enable_spirit=spirit))
     assert rel(x, xo) < TOL
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,n,pencil", [(5, 5, 5), (6, 7, 1), (9, 9, 0)])
+def test_tiny_images_and_extreme_pencils(gpu, m, n, pencil):
+    """Tiny images; pencil = N (q = 1), pencil = 1 (one-row lifts), default rule."""
+    A = gpu
+    y0 = phantom(m, n, 2, seed=m * n)
+    mk = A.mask_gauss_cartesian(n, 0.6, 2, 4)
+    y = np.where(mk.bits[0][None, :, None].astype(bool), y0, 0)
+    if pencil > min(m, n):
+        pytest.skip("pencil longer than a dimension")
+    x = A.shlr_pi_reconstruct(y, mk, None, A.HankelConfig(pencil=pencil),
+                              A.AdmmConfig(max_outer=3, tol=1e-300, enable_vc=True))
+    xo, _ = O.shlr_pi_reconstruct(y, O.SamplingMask(1, n, mk.bits), None, O.HankelConfig(pencil=pencil),
+                                  O.AdmmConfig(max_outer=3, tol=1e-300, enable_vc=True))
+    assert rel(x, xo) < TOL

@@ -138,3 +138,17 @@ def test_subspace_levels(gpu, r):
     assert rel(adj, adj_o) < TOL
     above = (sv_o > tau).sum(axis=1)
     assert above.min() >= min(r, 40) - 2  # the route the case is meant to take
+
+
+def test_empty_batch_and_degenerate_pencils(gpu):
+    """Empty batch; pencil = N (one column per coil block) and pencil = 1
+    (one row), against the oracle."""
+    v = np.zeros((0, 3, 20), np.complex128)
+    out, sv = gpu.hankel_svt_batched(v, 5, 1.0)
+    assert out.shape == (0, 3, 20) and sv.shape[0] == 0
+    rng = np.random.default_rng(3)
+    v = rng.standard_normal((3, 2, 9)) + 1j * rng.standard_normal((3, 2, 9))
+    for p in (9, 1):
+        adj, s = gpu.hankel_svt_batched(v, p, 0.5)
+        adj_o, s_o = O.hankel_svt_unit(v, p, 0.5)
+        assert rel(adj, adj_o) < TOL and rel(s, s_o) < TOL
