@@ -386,6 +386,32 @@ inline ParameterDataset recon_param_dataset(const ParameterDataset& y, const Sam
   return out;
 }
 
+// FE slices [begin, end) of recon_param_dataset only (the slices are
+// independent: parammap.cpp:37-51) -- the unit of work of one rank in a
+// multi-GPU job.  Returns the end - begin reconstructed slices.
+inline ParameterDataset recon_param_dataset_shard(const ParameterDataset& y, const SamplingMask& mask,
+                                                  const HankelConfig& hcfg, const AdmmConfig& acfg,
+                                                  std::size_t begin, std::size_t end, std::ostream* log = nullptr,
+                                                  std::size_t* total_iters = nullptr) {
+  y.validate();
+  const std::size_t m = y.fe(), n = y.pe(), l = y.echoes(), j = y.coils();
+  if (mask.rows != n || mask.cols != l) throw std::invalid_argument("recon_param_dataset: mask dims mismatch");
+  if (begin >= end || end > m) throw std::invalid_argument("recon_param_dataset: slice range outside the dataset");
+  acfg.validate();
+  shlr_param_args a = detail::param_args(y.data, m, n, l, j, mask, hcfg, acfg);
+  a.slice_begin = begin;
+  a.slice_end = end;
+  ParameterDataset out;
+  out.tes_ms = y.tes_ms;
+  out.data = ComplexTensor({end - begin, n, l, j});
+  shlr_stats st{};
+  const int rc =
+      shlr_cuda_param_reconstruct(&a, reinterpret_cast<double*>(out.data.data()), &st, detail::log_line, log);
+  if (total_iters) *total_iters = st.outer_iters;
+  detail::check(rc, "recon_param_dataset");
+  return out;
+}
+
 // Centred unitary FFT along one axis (fft.hpp:11-30), on the device.
 inline ComplexTensor fft_along_axis(const ComplexTensor& x, std::size_t axis, bool inverse) {
   ComplexTensor out = x;

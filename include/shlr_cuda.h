@@ -146,6 +146,12 @@ typedef struct shlr_param_args {
   double lambda, lambda2, beta, tau, tol, cg_tol;
   size_t max_outer, cg_max;
   int enable_vc;
+  /* Dataset mode only: solve FE slices [slice_begin, slice_end) of the M
+   * (the FE transform still runs over all M lines); x_out then holds
+   * slice_end - slice_begin slices.  0, 0 = all.  The slices are independent
+   * problems (parammap.cpp:37-51): ranks of a multi-GPU job each take a range,
+   * with no collective. */
+  size_t slice_begin, slice_end;
 } shlr_param_args;
 
 /* Full parameter reconstruction, host buffers in and out.  x_out: (m ? m : 1)

@@ -51,6 +51,7 @@ class ShlrParamArgs(C.Structure):
         ("tau", C.c_double), ("tol", C.c_double), ("cg_tol", C.c_double),
         ("max_outer", C.c_size_t), ("cg_max", C.c_size_t),
         ("enable_vc", C.c_int),
+        ("slice_begin", C.c_size_t), ("slice_end", C.c_size_t),
     ]
 
 

@@ -332,8 +332,16 @@ class ParameterDataset:
                 raise ValueError("ParameterDataset: TEs must be positive and strictly increasing")
 
 
+def shard_range(m: int, world: int, rank: int) -> Tuple[int, int]:
+    """Contiguous, balanced FE-slice range of `rank` among `world` ranks (the
+    slices of recon_param_dataset are independent: parammap.cpp:37-51)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("shard_range: invalid rank / world")
+    return rank * m // world, (rank + 1) * m // world
+
+
 def _param_args(y: np.ndarray, dataset: bool, mask: SamplingMask, hcfg: HankelConfig,
-                acfg: AdmmConfig, keep: list) -> ShlrParamArgs:
+                acfg: AdmmConfig, keep: list, slices: Optional[Tuple[int, int]] = None) -> ShlrParamArgs:
     acfg.validate()
     if dataset:
         m, n, l, j = y.shape
@@ -360,6 +368,8 @@ def _param_args(y: np.ndarray, dataset: bool, mask: SamplingMask, hcfg: HankelCo
     a.tol, a.cg_tol = acfg.tol, acfg.cg_tol
     a.max_outer, a.cg_max = acfg.max_outer, acfg.cg_max
     a.enable_vc = int(acfg.enable_vc)
+    if slices is not None:
+        a.slice_begin, a.slice_end = int(slices[0]), int(slices[1])
     return a
 
 
@@ -397,18 +407,22 @@ def shlr_param_reconstruct_slice(y_m: np.ndarray, mask: SamplingMask, hcfg: Hank
 
 def recon_param_dataset(y: ParameterDataset, mask: SamplingMask, hcfg: HankelConfig,
                         acfg: AdmmConfig, log: Optional[List[str]] = None,
-                        total_iters: Optional[List[int]] = None) -> ParameterDataset:
+                        total_iters: Optional[List[int]] = None,
+                        slices: Optional[Tuple[int, int]] = None) -> ParameterDataset:
     """``shlr::recon_param_dataset`` (``parammap.hpp:35-40``): iFFT along FE, then
     every FE slice's ADMM (each with its own early stop) -- all slices batched
     on the device.  ``total_iters`` (a list) receives the summed outer
-    iterations, the reference's ``*total_iters``."""
+    iterations, the reference's ``*total_iters``.  ``slices=(begin, end)``
+    (extension for multi-GPU jobs, see ``shard_range``) solves only those FE
+    slices; the result then holds end - begin slices."""
     y.validate()
     keep: list = []
     data = np.asarray(y.data)
     if mask.rows != data.shape[1] or mask.cols != data.shape[2]:
         raise ValueError("recon_param_dataset: mask dims mismatch")
-    a = _param_args(data, True, mask, hcfg, acfg, keep)
-    x, st = _run_param(a, data.shape, log, "recon_param_dataset")
+    a = _param_args(data, True, mask, hcfg, acfg, keep, slices)
+    shape = data.shape if slices is None else (slices[1] - slices[0],) + data.shape[1:]
+    x, st = _run_param(a, shape, log, "recon_param_dataset")
     if total_iters is not None:
         total_iters.append(int(st.outer_iters))
     return ParameterDataset(x, list(y.tes_ms))
@@ -417,11 +431,11 @@ def recon_param_dataset(y: ParameterDataset, mask: SamplingMask, hcfg: HankelCon
 class ParamPlan:
     """Resident plan of the parameter path (``shlr_cuda_param_plan_*``)."""
 
-    def __init__(self, y, mask, hcfg, acfg, dataset: bool = True):
+    def __init__(self, y, mask, hcfg, acfg, dataset: bool = True, slices: Optional[Tuple[int, int]] = None):
         self._keep: list = []
         y = np.asarray(y)
-        self._args = _param_args(y, dataset, mask, hcfg, acfg, self._keep)
-        self.shape = y.shape
+        self._args = _param_args(y, dataset, mask, hcfg, acfg, self._keep, slices)
+        self.shape = y.shape if slices is None else (slices[1] - slices[0],) + y.shape[1:]
         self._h = C.c_void_p()
         _check(lib.shlr_cuda_param_plan_create(C.byref(self._args), C.byref(self._h)), "plan_create")
 

@@ -109,12 +109,20 @@ void validate_param(const shlr_param_args* a) {
     throw InvalidArg("HankelConfig: parameter pencil exceeds signal length");
   if (!a->taps || a->ntaps == 0 || a->ntaps > a->n)
     throw InvalidArg("weights_from_filter: taps invalid");
+  if (a->slice_end != 0 || a->slice_begin != 0) {
+    if (a->m == 0) throw InvalidArg("recon_param_dataset: a slice range needs a dataset");
+    if (a->slice_begin >= a->slice_end || a->slice_end > a->m)
+      throw InvalidArg("recon_param_dataset: slice range outside the dataset");
+  }
 }
 
 shlr_b200::ParamConfig param_config_of(const shlr_param_args* a) {
   shlr_b200::ParamConfig c{};
-  c.S = a->m ? (int)a->m : 1;
+  const bool shard = a->slice_end > a->slice_begin;
+  c.S = a->m ? (shard ? (int)(a->slice_end - a->slice_begin) : (int)a->m) : 1;
   c.dataset = a->m != 0;
+  c.M_full = (int)a->m;
+  c.s0 = shard ? (int)a->slice_begin : 0;
   c.N = (int)a->n;
   c.L = (int)a->l;
   c.J = (int)a->j;

@@ -365,28 +365,36 @@ ParamPlan::ParamPlan(const ParamConfig& cfg, const double* y, const uint8_t* mas
 
   // ---- data: y (fp64) -> complex64; dataset: iFFT along FE (parammap.cpp:32);
   // then the masked PE k-space x0 and lambda * x0
+  // (a dataset plan may own only FE slices [s0, s0 + S) of the M_full in y:
+  // the FE transform mixes every line, so it runs over all of them)
   {
-    double* y_d = dalloc_s<double>(2 * nel_, stream_);
+    const int Mf = cfg.dataset ? std::max(cfg.M_full, S) : S;
+    const size_t nel_in = (size_t)Mf * L * N * J;
+    double* y_d = dalloc_s<double>(2 * nel_in, stream_);
+    float2* a_d = dalloc_s<float2>(nel_in, stream_);
+    float2* b_d = cfg.dataset ? dalloc_s<float2>(nel_in, stream_) : nullptr;
     uint8_t* m_d = dalloc_s<uint8_t>((size_t)N * L, stream_);
-    SHLR_CUDA(cudaMemcpyAsync(y_d, y, 2 * nel_ * sizeof(double), cudaMemcpyHostToDevice, stream_));
+    SHLR_CUDA(cudaMemcpyAsync(y_d, y, 2 * nel_in * sizeof(double), cudaMemcpyHostToDevice, stream_));
     SHLR_CUDA(cudaMemcpyAsync(m_d, mask, (size_t)N * L, cudaMemcpyHostToDevice, stream_));
-    k_p_from_double<<<grid_for(nel_), kThreads, 0, stream_>>>(y_d, r_, nel_);
+    k_p_from_double<<<grid_for(nel_in), kThreads, 0, stream_>>>(y_d, a_d, nel_in);
     SHLR_LAUNCH_CHECK();
-    const float2* hyb = r_;
+    const float2* hyb = a_d;
     float2* twM = nullptr;
     if (cfg.dataset) {
-      FftTwiddles tM = make_twiddles(S, &twM, stream_);
+      FftTwiddles tM = make_twiddles(Mf, &twM, stream_);
       const long long inner = (long long)N * L * J;
-      StridedCopyOp op{r_, p_, 0, inner, 1};
+      StridedCopyOp op{a_d, b_d, 0, inner, 1};
       launch_fft_axis<StridedCopyOp, true>(op, tM, 1, (int)inner, 16, stream_);
-      hyb = p_;
+      hyb = b_d + (size_t)cfg.s0 * N * L * J;
     }
     k_p_prep<<<grid_for(nel_), kThreads, 0, stream_>>>(hyb, m_d, S, N, L, J, (float)cfg.lambda, x0_, yk_);
     SHLR_LAUNCH_CHECK();
-    SHLR_CUDA(cudaStreamSynchronize(stream_));
     SHLR_CUDA(cudaFreeAsync(y_d, stream_));
+    SHLR_CUDA(cudaFreeAsync(a_d, stream_));
+    if (b_d) SHLR_CUDA(cudaFreeAsync(b_d, stream_));
     SHLR_CUDA(cudaFreeAsync(m_d, stream_));
     if (twM) SHLR_CUDA(cudaFreeAsync(twM, stream_));
+    SHLR_CUDA(cudaStreamSynchronize(stream_));
   }
   SHLR_CUDA(cudaFuncSetAttribute(k_p_cg, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
   reset();

@@ -30,6 +30,8 @@ struct ParamConfig {
   int Ppe, Ppar;         // pencil_for(N), pencil_for_param(L) (hankel.cpp:10-29)
   bool vc;
   bool dataset;          // y is M x N x L x J k-space: iFFT along FE first (parammap.cpp:32)
+  int M_full;            // dataset: FE lines of y (the plan solves slices [s0, s0 + S))
+  int s0;
   double lambda, lambda2, beta, tau, tol, cg_tol;
   int max_outer, cg_max;
 };

@@ -212,3 +212,23 @@ def test_gpu_param_config4_vs_reference_slices(gpu, c4_inputs):
         # the stop-rule trace follows the reference's while it is above the
         # FP32 resolution of the iterates (the first ten iterations)
         assert all(abs(a[1] - b[1]) <= 1e-2 * abs(b[1]) for a, b in zip(got[:10], want[:10]))
+
+
+@pytest.mark.gpu
+def test_gpu_param_slice_ranges_compose(gpu):
+    """Solving FE slices [0, 3) and [3, 5) separately (the multi-GPU sharding
+    of recon_param_dataset) gives the full run's slices bitwise."""
+    A = gpu
+    rng = np.random.default_rng(9)
+    y = rng.standard_normal((5, 20, 9, 2)) + 1j * rng.standard_normal((5, 20, 9, 2))
+    bits = np.stack([O.mask_gauss_cartesian(20, 0.5, 4, 60 + e).bits[0] for e in range(9)], axis=1)
+    ds = A.ParameterDataset(y, [10.0 * (e + 1) for e in range(9)])
+    mk = A.SamplingMask(20, 9, bits)
+    acfg = A.AdmmConfig(max_outer=3, tol=1e-300, enable_vc=True)
+    full = A.recon_param_dataset(ds, mk, A.HankelConfig(pencil=14), acfg).data
+    a = A.recon_param_dataset(ds, mk, A.HankelConfig(pencil=14), acfg, slices=(0, 3)).data
+    b = A.recon_param_dataset(ds, mk, A.HankelConfig(pencil=14), acfg, slices=(3, 5)).data
+    assert a.shape == (3, 20, 9, 2) and b.shape == (2, 20, 9, 2)
+    assert np.array_equal(np.concatenate([a, b]), full)
+    with pytest.raises(ValueError):
+        A.recon_param_dataset(ds, mk, A.HankelConfig(pencil=14), acfg, slices=(4, 7))

@@ -59,3 +59,41 @@ def test_gpu_arm_fails_loudly_without_device():
         pytest.skip("host has a GPU")
     assert r.returncode != 0
     assert "no CUDA device" in (r.stderr + r.stdout)
+
+
+def _shard_worker(rank, world, port, m, q):
+    os.environ.update(RANK=str(rank), WORLD_SIZE=str(world), LOCAL_RANK=str(rank),
+                      MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    sys.path.insert(0, ROOT)
+    import torch
+    import bench
+    from paper_2107_11650_b200 import api as A
+    dist, r, w, _ = bench.dist_setup()
+    b, e = A.shard_range(m, w, r)
+    got = [torch.zeros(2, dtype=torch.int64) for _ in range(w)]
+    dist.all_gather(got, torch.tensor([b, e], dtype=torch.int64))
+    dist.destroy_process_group()
+    q.put((rank, [tuple(int(v) for v in g) for g in got]))
+
+
+@pytest.mark.parametrize("m", [256, 7])
+def test_parameter_slices_shard_over_ranks(m):
+    """Parameter imaging shards its independent FE slices over the ranks
+    (bench.py config-4 workload): with world size 2 over
+    gloo the ranks' ranges are contiguous, disjoint and cover all M slices."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_shard_worker, args=(r, 2, port, m, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    res = sorted(q.get(timeout=10) for _ in range(2))
+    ranges = res[0][1]
+    assert ranges == res[1][1]
+    assert ranges[0][0] == 0 and ranges[-1][1] == m
+    assert all(ranges[i][1] == ranges[i + 1][0] for i in range(len(ranges) - 1))
+    assert all(e > b for b, e in ranges)
