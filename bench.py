@@ -584,7 +584,7 @@ def small_workload(args, dist, world, rank, fp32_peak):
 
 
 SWEEP_POINTS = [(128, 8, 15), (256, 1, 15), (256, 8, 7), (256, 8, 15), (256, 8, 31), (256, 32, 15),
-                (512, 8, 15)]
+                (256, 32, 7), (512, 8, 15), (512, 8, 31), (512, 32, 7)]
 
 
 def sweep_workload(args, fp32_peak):

@@ -208,7 +208,8 @@ __device__ __forceinline__ void build_chunk_big(float2* dst, const SvtFamily& F,
     const int r = t / DP, u = t - r * DP;
     float2 v = make_float2(0.f, 0.f);
     if (r < rows && u < d) {
-      v = lift_global(F, sp, wcs, weighted, lofs[i0 + r], u);
+      v = F.wide ? lift_global(F, sp, wcs, weighted, lofs[i0 + r], u)
+                 : cconj(lift_global(F, sp, wcs, weighted, lofs[u], i0 + r));  // tall: Ahat = A
       if (Dg) {  // duals straight from HBM/L2 (coalesced rows)
         const float2 dd = __ldcg(Dg + (long long)(i0 + r) * d + u);
         v.x = fmaf(dd.x, inv_beta, v.x);
@@ -1623,9 +1624,19 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
   if (BIG) {
     for (int t = tid; t < len; t += NT) wl[t] = weighted ? F.wc[t] : make_float2(1.f, 0.f);
     for (int t = tid; t < 2 * len; t += NT) acc[t] = make_float2(0.f, 0.f);
-    for (int t = tid; t < e; t += NT) {
+    // block/shift of the lifted index: rows of Ahat (wide) or its columns (tall)
+    for (int t = tid; t < (F.wide ? e : d); t += NT) {
       const int b = t / F.q;
       lofs[t] = (b << 16) | (t - b * F.q);
+    }
+    // tall (plain modes only): the adjoint accumulates into this matrix's
+    // own output region across chunks (every chunk touches every block)
+    if (!F.wide) {
+      float2* op = F.out + (long long)mat * F.o_mat;
+      for (int t = tid; t < J * len; t += NT) {
+        const int j = t / len, n = t - j * len;
+        op[(long long)n * F.o_n + (long long)j * F.o_j] = make_float2(0.f, 0.f);
+      }
     }
     if (tid < 4) S.flags[tid] = 0;
     if (tid == 0) *cnt = 0;
@@ -2011,7 +2022,8 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
           }
           float2 tv = z[m];
           if (admm) {
-            const float2 L = BIG ? lift_global(F, spg, wl, weighted, lofs[i0 + yi], k)
+            const float2 L = BIG ? (F.wide ? lift_global(F, spg, wl, weighted, lofs[i0 + yi], k)
+                                           : cconj(lift_global(F, spg, wl, weighted, lofs[k], i0 + yi)))
                                  : lift_tab(wl, lofs, F.wide, i0 + yi, k);
             const long long gi = (long long)(i0 + yi) * d + k;
             float2 dn = BIG ? __ldcg(Dg + gi) : Ds[yi * d + k];
@@ -2029,6 +2041,22 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
     if (stg && i0 + R < e) stage_d_async(Ds, Dg, i0 + R, min(R, e - i0 - R), d);  // overlaps the adjoint
     if (to_defl) {
       // Z1 mode: no duals, no adjoint (level 3 finishes the matrix)
+    } else if (BIG && !F.wide) {
+      // tall, plain modes: out_b[n] += sum_i T[i][b q + n - i] over this
+      // chunk's rows, read-modify-write of the CTA's own output region
+      const int q = F.q;
+      float2* op = F.out + (long long)mat * F.o_mat;
+      const int nlo = i0, nhi = min(len - 1, i0 + rows - 1 + q - 1);
+      const int span = nhi - nlo + 1;
+      for (int o = tid; o < B * span; o += NT) {
+        const int b = o / span, n = nlo + o % span;
+        const int ilo = max(i0, n - q + 1), ihi = min(i0 + rows - 1, n);
+        float2 sacc = make_float2(0.f, 0.f);
+        for (int i = ilo; i <= ihi; ++i) sacc = cadd(sacc, C[(i - i0) * CS + b * q + (n - i)]);
+        float2* dst = op + (long long)n * F.o_n + (long long)b * F.o_j;
+        *dst = cadd(*dst, sacc);
+      }
+      __syncthreads();
     } else if (BIG) {
       // blocks b_lo..b_hi touch this chunk; a block whose rows continue into
       // the next chunk is carried (acc[par]), the one carried in from the
@@ -2153,7 +2181,9 @@ bool launch_level(const SvtParams& prm, int total, cudaStream_t stream) {
   if (g.dmin < kSubspaceKB + 24) return false;
   if (g.dmax > 128) {
     // large-d variant (spectra and adjoint not resident)
-    if (!g.all_wide || g.maxLen > 0xffff) return false;
+    // tall large-d lifts: plain modes only (the adjoint accumulates in the
+    // output without the weighting / virtual-coil combination)
+    if ((!g.all_wide && prm.mode == SVT_ADMM_WEIGHTED) || g.maxLen > 0xffff) return false;
     const int dpb = svt_big_padded_dim(g.dmax);
     if (!dpb) return false;
     constexpr int KB = L2 ? kSubspaceKBBig : kSubspaceKB;

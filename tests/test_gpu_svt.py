@@ -1,8 +1,8 @@
 """GPU parity of the batched Hankel-SVT unit (BASELINE config 5) against the
 oracle on the sweep's synthetic inputs: every sweep point with d = min(p, Nc K)
-<= 128 (singular values and adjoints), every wide point with 128 < d <= 248
+<= 128 (singular values and adjoints), every point with 128 < d <= 248
 (adjoints: the large-d subspace path has no exact singular-value output),
-loud NotImplementedError for the rest; plus size-independent properties at
+loud NotImplementedError for d > 248; plus size-independent properties at
 full batch."""
 import numpy as np
 import pytest
@@ -83,11 +83,11 @@ def test_full_batch_properties(gpu):
 
 
 ALL = [(n, nc, k) for n in (128, 256, 512) for nc in (1, 8, 32) for k in (7, 15, 31)]
-BIG_WIDE = [(n, nc, k) for n, nc, k in ALL if 128 < min(n - k + 1, nc * k) <= 248 and nc * k > n - k + 1]
-UNSUPPORTED = [(n, nc, k) for n, nc, k in ALL if min(n - k + 1, nc * k) > 128 and (n, nc, k) not in BIG_WIDE]
+BIG = [(n, nc, k) for n, nc, k in ALL if 128 < min(n - k + 1, nc * k) <= 248]
+UNSUPPORTED = [(n, nc, k) for n, nc, k in ALL if min(n - k + 1, nc * k) > 248]
 
 
-@pytest.mark.parametrize("n,nc,k", BIG_WIDE)
+@pytest.mark.parametrize("n,nc,k", BIG)
 def test_sweep_point_large_d_parity(gpu, n, nc, k):
     from paper_2107_11650_b200 import synth
     v = synth.sweep_vectors(n, nc, k, 4)
