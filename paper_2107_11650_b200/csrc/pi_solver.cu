@@ -433,12 +433,12 @@ __global__ void __launch_bounds__(kFftThreads) k_spirit_cols(const float2* __res
   const int n0 = blockIdx.x * PPT;  // first pixel column of the tile
   float2* a = sm;
   float2* b = sm + (size_t)M * F;
-  const int lf = fib_log2(F);
+  const int lf = fib_log2(F), lj = fib_log2(J);
 #pragma unroll 4
   for (int t = threadIdx.x; t < M * F; t += blockDim.x) {
     int f, k;
     tile_idx(t, F, lf, f, k);
-    const int n = n0 + f / J;
+    const int n = n0 + (lj >= 0 ? f >> lj : f / J);
     a[t] = n < N ? tmp[k * NJ + (long long)n0 * J + f] : make_float2(0.f, 0.f);
   }
   __syncthreads();
@@ -499,7 +499,7 @@ __global__ void __launch_bounds__(kFftThreads) k_spirit_cols(const float2* __res
   for (int t = threadIdx.x; t < M * F; t += blockDim.x) {
     int f, k;
     tile_idx(t, F, lf, f, k);
-    const int n = n0 + f / J;
+    const int n = n0 + (lj >= 0 ? f >> lj : f / J);
     if (n < N) tmp2[k * NJ + (long long)n0 * J + f] = cscale(res2[t], centered_out_scale(k, M, tw.logn, isn));
   }
 }
