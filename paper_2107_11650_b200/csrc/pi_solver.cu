@@ -524,18 +524,35 @@ __global__ void __launch_bounds__(kFftThreads) k_spirit_rows_fwd(const float2* _
   float2* b = sm + (size_t)N * F;
 #pragma unroll 4
   for (int t = threadIdx.x; t < N * F; t += blockDim.x) a[t] = tmp2[m * NJ + t];
+  const int lf = fib_log2(F);
+  // the combine's operands (p and the diagonal) are loaded before the FFT so
+  // their L2 latency hides under it (up to 4 elements per thread)
+  constexpr int kPre = 4;
+  const bool pre = N * F <= kPre * (int)blockDim.x;
+  float2 pv_pre[kPre];
+  float dv_pre[kPre];
+  if (pre) {
+#pragma unroll
+    for (int u = 0; u < kPre; ++u) {
+      const int t = threadIdx.x + u * blockDim.x;
+      if (t < N * F) {
+        const int k = lf >= 0 ? t >> lf : t / F;
+        pv_pre[u] = vec[m * NJ + t];
+        dv_pre[u] = dg[(long long)m * N + k];
+      }
+    }
+  }
   __syncthreads();
   float2* res = smem_centered_dft<false>(a, b, tw, F);
   const float isn = rsqrtf((float)N);
   double s = 0.0;
-  const int lf = fib_log2(F);
 #pragma unroll 4
-  for (int t = threadIdx.x; t < N * F; t += blockDim.x) {
+  for (int t = threadIdx.x, u = 0; t < N * F; t += blockDim.x, ++u) {
     const int k = lf >= 0 ? t >> lf : t / F;
     const long long idx = m * NJ + t;
     const float2 v = cscale(res[t], centered_out_scale(k, N, tw.logn, isn));
-    const float2 pv = vec[idx];
-    const float dv = dg[(long long)m * N + k];  // F == J: element (m, k, coil) -> pixel (m, k)
+    const float2 pv = pre ? pv_pre[u & (kPre - 1)] : vec[idx];
+    const float dv = pre ? dv_pre[u & (kPre - 1)] : dg[(long long)m * N + k];  // F == J: element (m, k, coil) -> pixel (m, k)
     const float2 av = make_float2(fmaf(dv, pv.x, lambda1 * v.x), fmaf(dv, pv.y, lambda1 * v.y));
     ap[idx] = av;
     s += (double)pv.x * av.x + (double)pv.y * av.y;
