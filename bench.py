@@ -181,42 +181,59 @@ def barrier(dist):
 
 
 # ---------------------------------------------------------------- CPU leg
-def write_ref_inputs(tmp: str, y, mask, g) -> None:
-    from paper_2107_11650_b200.cplx_io import write_cplx, write_mask
-    write_cplx(y, os.path.join(tmp, "y.cplx"))
-    write_mask(mask.bits, os.path.join(tmp, "m.cplx"),
-               dict(generator="gauss_cartesian", seed=mask.seed, rate=mask.rate, acs=mask.acs))
-    if g is not None:
-        write_cplx(g.weights, os.path.join(tmp, "k.cplx"))
+# The reference legs never import the product API (nor load its .so): the
+# image comes from the harness generator (numpy only), the mask from the
+# reference's own generator (`ref_driver mask`), the SPIRiT kernels from the
+# reference's own spirit_calibrate inside `ref_driver pi` (no kernels=).
+def write_ref_inputs(tmp: str, cfg=CFG2) -> None:
+    from paper_2107_11650_b200 import synth  # numpy-only harness generator
+    from paper_2107_11650_b200.cplx_io import write_cplx
+    ph = synth.pi_phantom(cfg["M"], cfg["N"], cfg["J"])
+    write_cplx(ph.kspace, os.path.join(tmp, "y.cplx"))
+    subprocess.run([REF_DRIVER, "mask", "kind=gauss", f"n={cfg['N']}", f"rate={cfg['rate']}",
+                    f"acs={cfg['acs']}", f"seed={synth.SEED_MASK}", "out=m.cplx"], cwd=tmp, check=True)
+
+
+def ref_pi_cmd(cfg, iters: int):
+    """The stock shlr_pi_reconstruct (proj/src/solvers.cpp:95-191) through
+    ref_driver, timed per iteration through its own log lines (time=1)."""
+    cmd = [REF_DRIVER, "pi", "y=y.cplx", "mask=m.cplx", f"pencil={cfg['N'] - cfg['K'] + 1}",
+           f"max_outer={iters}", "tol=1e-300", "time=1", f"lambda={cfg['lam']}", f"beta={cfg['beta']}",
+           f"tau={cfg['tau']}", f"cg_max={cfg['cg_max']}", f"cg_tol={cfg['cg_tol']}"]
+    if cfg.get("spirit"):
+        cmd += ["spirit=1", f"acs={cfg['acs']}", f"kernel={cfg['kernel']}", f"tikhonov={cfg['tikhonov']}",
+                f"lambda1={cfg['lambda1']}"]
+    return cmd
 
 
 def run_reference(tmp: str, procs: int, iters: int, budget_s: float, cfg=CFG2):
-    """Runs `procs` concurrent reference processes (oracle/_ref/ref_driver,
-    the reference's own solvers.cpp through the instrumented replay that is
-    bitwise equal to shlr_pi_reconstruct) for up to `iters` outer iterations
-    each, stopping at `budget_s`.  Returns per-process lists of per-iteration
-    seconds (setup excluded)."""
-    cmd = [REF_DRIVER, "pi", "y=y.cplx", "mask=m.cplx", "kernels=k.cplx", "spirit=1",
-           f"pencil={cfg['N'] - cfg['K'] + 1}", f"max_outer={iters}", "tol=1e-300", "replay=1",
-           "time=1"]
+    """Runs `procs` concurrent reference processes, each the stock
+    shlr_pi_reconstruct for up to `iters` outer iterations, stopping at
+    `budget_s` once every process has timed an iteration.  Returns per-process
+    lists of per-iteration seconds: iterations 2.. (setup excluded) when a
+    process got that far, else its first iteration (setup included)."""
+    cmd = ref_pi_cmd(cfg, iters)
     ps = []
     for i in range(procs):
         ps.append(subprocess.Popen(cmd + [f"out=ref{i}"], cwd=tmp, stdout=subprocess.PIPE,
                                    stderr=subprocess.DEVNULL, text=True,
                                    env=dict(os.environ, OMP_NUM_THREADS="1")))
-    results = [[] for _ in ps]
+    later = [[] for _ in ps]
+    first = [[] for _ in ps]
 
     def reader(i, p):
         for line in p.stdout:
             if line.startswith("iter_seconds="):
-                results[i].append(float(line.split("=")[1]))
+                later[i].append(float(line.split("=")[1]))
+            elif line.startswith("first_iter_seconds="):
+                first[i].append(float(line.split("=")[1]))
 
     threads = [threading.Thread(target=reader, args=(i, p), daemon=True) for i, p in enumerate(ps)]
     for t in threads:
         t.start()
     t0 = time.time()
     while any(p.poll() is None for p in ps):
-        if time.time() - t0 > budget_s and all(len(r) >= 1 for r in results):
+        if time.time() - t0 > budget_s and all(len(f) >= 1 for f in first):
             break
         time.sleep(0.5)
     for p in ps:
@@ -224,16 +241,16 @@ def run_reference(tmp: str, procs: int, iters: int, budget_s: float, cfg=CFG2):
             p.kill()
     for t in threads:
         t.join(timeout=5)
-    return results
+    return [lt if lt else f for lt, f in zip(later, first)]
 
 
-def cpu_baseline(y, mask, g, procs: int, iters: int, budget_s: float):
+def cpu_baseline(procs: int, iters: int, budget_s: float, cfg=CFG2):
     if not os.path.exists(REF_DRIVER):
         return None
     tmp = tempfile.mkdtemp(prefix="shlr_ref_")
     try:
-        write_ref_inputs(tmp, y, mask, g)
-        res = run_reference(tmp, procs, iters, budget_s)
+        write_ref_inputs(tmp, cfg)
+        res = run_reference(tmp, procs, iters, budget_s, cfg)
     finally:
         shutil.rmtree(tmp, ignore_errors=True)
     per_proc = [statistics.mean(r) for r in res if r]
@@ -243,10 +260,20 @@ def cpu_baseline(y, mask, g, procs: int, iters: int, budget_s: float):
     # throughput of `procs` concurrent single-threaded reference processes
     value = sum(1.0 / s for s in per_proc)
     return {"value": value, "unit": "iterations/s", "cores": len(per_proc), "kind": "reference",
-            "sample": (f"{len(per_proc)} concurrent single-threaded reference processes "
-                       f"(oracle/_ref/ref_driver: proj/src/*.cpp unmodified + builder Eigen subset), "
-                       f"{done} outer iterations of config 2 in total, setup excluded; "
-                       f"mean {statistics.mean(per_proc):.2f} s per iteration per process")}
+            "sample": (f"{len(per_proc)} concurrent single-threaded processes of the stock "
+                       f"shlr_pi_reconstruct (oracle/_ref/ref_driver: proj/src/*.cpp unmodified + builder "
+                       f"Eigen subset; reference-generated mask, reference SPIRiT calibration), "
+                       f"{done} outer iterations of config 2 timed through the solver's log lines "
+                       f"(iterations 2.., setup excluded); mean {statistics.mean(per_proc):.2f} s per "
+                       f"iteration per process")}
+
+
+def bench_config(world: int) -> dict:
+    """The `config` object of both arms (same workload, same keys)."""
+    m, n, j, k = CFG2["M"], CFG2["N"], CFG2["J"], CFG2["K"]
+    return {"workload": WORKLOAD, "parallelism": f"replicas x{world}",
+            "l2": "inputs larger than L2: 119 MB duals + 33.5 MB SPIRiT P streamed per step",
+            "lifted_matrix": f"{n - k + 1}x{j * k}", "matrices_per_step": m + n}
 
 
 # ---------------------------------------------------------------- GPU arm
@@ -342,7 +369,7 @@ def gpu_arm(args, dist, rank, world, local):
 
     cpu = None
     if rank == 0 and not args.no_cpu:
-        cpu = cpu_baseline(y, mask, g, procs=1, iters=1, budget_s=args.cpu_budget)
+        cpu = cpu_baseline(procs=1, iters=2, budget_s=args.cpu_budget)
 
     extra = {}
     if not args.no_extra:
@@ -368,9 +395,7 @@ def gpu_arm(args, dist, rank, world, local):
         "dtype": "c64 (fp32 complex; fp64 reductions and setup)",
         "data": "synthetic: seeded BASELINE phantom (10 ellipses, smooth phase, 8 Gaussian coils, 40 dB)",
         "impl": "b200",
-        "config": {"workload": WORKLOAD, "parallelism": f"replicas x{world}",
-                   "l2": "inputs larger than L2: 119 MB duals + 33.5 MB SPIRiT P streamed per step",
-                   "lifted_matrix": f"{p}x{j * k}", "matrices_per_step": m + n},
+        "config": bench_config(world),
         "hankel_svt": {"matrices_per_s": (m + n) / (svt_ms * 1e-3), "kernel_ms": svt_ms,
                        "share_of_step": svt_ms / (t_max_ms / args.steps),
                        "solver": "subspace iteration (block 48; 1 pass per ADMM iteration warm, 6 cold) + Rayleigh-Ritz by tridiagonalisation/multisection, "
@@ -629,19 +654,22 @@ def sweep_workload(args, fp32_peak):
 
 
 def reference_arm(args, dist, rank, world):
+    """The reference's own CPU implementation (stock shlr_pi_reconstruct, the
+    unmodified proj/src compiled by oracle/Makefile) on the host cores: up to
+    --ref-procs concurrent single-threaded processes (the reference has no
+    threading; concurrent calls are safe).  Rank 0 only."""
     if rank != 0:
         return
     if not os.path.exists(REF_DRIVER):
         print(json.dumps({"impl": "reference", "unavailable":
                           "oracle/_ref/ref_driver not built (run __graft_entry__.build())"}))
         return
-    y, mask, g, _ = make_inputs(CFG2)
     procs = max(1, min(os.cpu_count() or 1, args.ref_procs))
     tmp = tempfile.mkdtemp(prefix="shlr_ref_")
     try:
-        write_ref_inputs(tmp, y, mask, g)
-        iters = max(1, min(args.steps, 50))
-        res = run_reference(tmp, procs, iters, args.cpu_budget)
+        write_ref_inputs(tmp, CFG2)
+        iters = max(2, min(args.steps, 50))
+        res = run_reference(tmp, procs, iters, args.cpu_budget, CFG2)
     finally:
         shutil.rmtree(tmp, ignore_errors=True)
     per_proc = [statistics.mean(r) for r in res if r]
@@ -652,15 +680,29 @@ def reference_arm(args, dist, rank, world):
         "value": value, "unit": "iterations/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 / value if value else None,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128 (fp64)",
-        "data": "synthetic: seeded BASELINE phantom", "impl": "reference",
-        "config": {"workload": WORKLOAD, "parallelism": f"{len(per_proc)} host processes"},
+        "data": "synthetic: seeded BASELINE phantom (10 ellipses, smooth phase, 8 Gaussian coils, 40 dB)",
+        "impl": "reference",
+        "config": bench_config(world),
         "cpu_baseline": {"value": value, "unit": "iterations/s", "cores": len(per_proc),
                          "kind": "reference",
-                         "sample": f"{len(per_proc)} concurrent single-threaded reference processes, "
-                                   f"{done} outer iterations timed (setup excluded), budget {args.cpu_budget:.0f} s"},
+                         "sample": f"{len(per_proc)} concurrent single-threaded processes of the stock "
+                                   f"shlr_pi_reconstruct, {done} outer iterations timed through its log "
+                                   f"lines (iterations 2.., setup excluded), budget {args.cpu_budget:.0f} s"},
         "e2e": {"value": value, "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out))
+
+
+def relaunch_distributed(n: int) -> int:
+    """`bench.py --gpus N` (N > 1) outside torchrun: launch N ranks on this
+    node with torch.distributed.run (127.0.0.1 rendezvous) and wait."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -677,7 +719,11 @@ def main():
     args = ap.parse_args()
     if args.warmup < 1 or args.steps < 1:
         raise SystemExit("need --steps >= 1 and --warmup >= 1")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(relaunch_distributed(args.gpus))
     dist, rank, world, local = dist_setup()
+    if world != args.gpus and rank == 0:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; timing {world} rank(s)", file=sys.stderr)
     try:
         if args.impl == "reference":
             reference_arm(args, dist, rank, world)

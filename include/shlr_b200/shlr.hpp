@@ -342,7 +342,8 @@ inline ComplexTensor shlr_param_reconstruct_slice(const ComplexTensor& y_m, cons
   const shlr_param_args a = detail::param_args(y_m, 0, n, l, j, mask, hcfg, acfg);
   ComplexTensor x({n, l, j});
   shlr_stats st{};
-  const int rc = shlr_cuda_param_reconstruct(&a, reinterpret_cast<double*>(x.data()), &st, detail::log_line, log);
+  const int rc = shlr_cuda_param_reconstruct(&a, reinterpret_cast<double*>(x.data()), &st,
+                                             log ? detail::log_line : nullptr, log);
   if (stats) *stats = {st.outer_iters, st.final_rel_change};
   detail::check(rc, "shlr_param_reconstruct_slice");
   return x;
@@ -380,7 +381,8 @@ inline ParameterDataset recon_param_dataset(const ParameterDataset& y, const Sam
   out.data = ComplexTensor({m, n, l, j});
   shlr_stats st{};
   const int rc =
-      shlr_cuda_param_reconstruct(&a, reinterpret_cast<double*>(out.data.data()), &st, detail::log_line, log);
+      shlr_cuda_param_reconstruct(&a, reinterpret_cast<double*>(out.data.data()), &st,
+                                  log ? detail::log_line : nullptr, log);
   if (total_iters) *total_iters = st.outer_iters;
   detail::check(rc, "recon_param_dataset");
   return out;
@@ -396,8 +398,16 @@ inline ParameterDataset recon_param_dataset_shard(const ParameterDataset& y, con
   y.validate();
   const std::size_t m = y.fe(), n = y.pe(), l = y.echoes(), j = y.coils();
   if (mask.rows != n || mask.cols != l) throw std::invalid_argument("recon_param_dataset: mask dims mismatch");
-  if (begin >= end || end > m) throw std::invalid_argument("recon_param_dataset: slice range outside the dataset");
+  if (begin > end || end > m) throw std::invalid_argument("recon_param_dataset: slice range outside the dataset");
   acfg.validate();
+  if (begin == end) {  // empty shard (more ranks than FE slices): nothing to solve; the
+                       // C-ABI reads slice range (0, 0) as "all slices", so it is not called
+    if (total_iters) *total_iters = 0;
+    ParameterDataset empty;
+    empty.tes_ms = y.tes_ms;
+    empty.data = ComplexTensor({0, n, l, j});
+    return empty;
+  }
   shlr_param_args a = detail::param_args(y.data, m, n, l, j, mask, hcfg, acfg);
   a.slice_begin = begin;
   a.slice_end = end;
@@ -406,7 +416,8 @@ inline ParameterDataset recon_param_dataset_shard(const ParameterDataset& y, con
   out.data = ComplexTensor({end - begin, n, l, j});
   shlr_stats st{};
   const int rc =
-      shlr_cuda_param_reconstruct(&a, reinterpret_cast<double*>(out.data.data()), &st, detail::log_line, log);
+      shlr_cuda_param_reconstruct(&a, reinterpret_cast<double*>(out.data.data()), &st,
+                                  log ? detail::log_line : nullptr, log);
   if (total_iters) *total_iters = st.outer_iters;
   detail::check(rc, "recon_param_dataset");
   return out;

@@ -181,7 +181,9 @@ void shlr_cuda_param_plan_destroy(shlr_param_plan* plan);
  * pencil p, svt with threshold tau (solvers.cpp:11-21), adjoint_lift_plain
  * (operators.cpp:105-119).  All pointers are DEVICE pointers to complex64
  * (float2) data: vecs and out are batch x nc x n; sv_out (nullable) is
- * batch x d floats, descending.  stream is a cudaStream_t (NULL = default). */
+ * batch x d floats, descending.  stream is a cudaStream_t (NULL = default).
+ * out must not overlap vecs (SHLR_EINVAL): tall large-d lifts accumulate the
+ * adjoint in the zeroed output while the lift source is still being read. */
 int shlr_cuda_hankel_svt_batched(const void* vecs, int batch, int nc, int n, int p,
                                  float tau, void* out, float* sv_out, void* stream);
 /* Same, host complex128 buffers in and out (the e2e path). */

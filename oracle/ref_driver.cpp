@@ -11,7 +11,10 @@
 //          [lambda1=1e2] [beta=1] [tau=1] [cg_max=15] [cg_tol=1e-8]
 //          [sv_iters=] (comma list of 1-based iterations whose singular values
 //          of L + D/beta are dumped; uses the instrumented replay below)
-//          [replay=0] [time=0]
+//          [x_iters=] (comma list of 1-based iterations whose image x is
+//          dumped to out.x<k>.cplx; also uses the replay)
+//          [replay=0] [time=0]  (time=1 without the replay: the stock
+//          shlr_pi_reconstruct timed per iteration through its log lines)
 //   param  y= mask= out= [vc=0] [pencil=0] [pencil_param=0] ...admm keys
 //          (y is N x L x J -> shlr_param_reconstruct_slice, or M x N x L x J
 //          -> recon_param_dataset)
@@ -146,7 +149,8 @@ ComplexTensor pi_replay(const ComplexTensor& y, const SamplingMask& mask,
                         const SpiritKernels* g, const HankelConfig& hcfg,
                         const AdmmConfig& acfg, std::ostream* log, SolveStats* stats,
                         const std::vector<std::size_t>& sv_iters,
-                        const std::string& sv_prefix, bool print_times = false) {
+                        const std::string& sv_prefix, bool print_times = false,
+                        const std::vector<std::size_t>& x_iters = {}) {
   acfg.validate();
   const std::size_t m = y.dim(0), n = y.dim(1), j = y.dim(2);
   HankelConfig cfg = hcfg;
@@ -213,6 +217,8 @@ ComplexTensor pi_replay(const ComplexTensor& y, const SamplingMask& mask,
       d_col[c] += acfg.tau * (lifted - z_col[c]);
     }
     if (dump) write_sv(svs, sv_prefix + ".sv" + std::to_string(k + 1) + ".cplx");
+    if (std::find(x_iters.begin(), x_iters.end(), k + 1) != x_iters.end())
+      write_cplx(x_new, sv_prefix + ".x" + std::to_string(k + 1) + ".cplx");
     // rel_change_sq (solvers.cpp:80-87)
     double num = 0.0, den = 0.0;
     for (std::size_t i = 0; i < x_new.size(); ++i) {
@@ -236,6 +242,36 @@ ComplexTensor pi_replay(const ComplexTensor& y, const SamplingMask& mask,
   if (stats) *stats = {iters, relchange};
   return x;
 }
+
+// Log sink that stamps every line the STOCK shlr_pi_reconstruct writes
+// (solvers.cpp:71-78, one line per outer iteration): prints
+// first_iter_seconds= (call start -> first line, includes the solver's setup)
+// and then iter_seconds= per further iteration, so the unmodified library
+// call is timed per iteration without replaying its loop.
+class StampBuf : public std::streambuf {
+ public:
+  StampBuf(std::streambuf* sink, double t0) : sink_(sink), last_(t0) {}
+
+ protected:
+  int overflow(int c) override {
+    if (c == traits_type::eof()) return traits_type::not_eof(c);
+    if (sink_->sputc(static_cast<char>(c)) == traits_type::eof()) return traits_type::eof();
+    if (c == '\n') {
+      const double t = now_s();
+      std::printf("%s=%.6f\n", first_ ? "first_iter_seconds" : "iter_seconds", t - last_);
+      std::fflush(stdout);
+      first_ = false;
+      last_ = t;
+    }
+    return c;
+  }
+  int sync() override { return sink_->pubsync(); }
+
+ private:
+  std::streambuf* sink_;
+  double last_;
+  bool first_ = true;
+};
 
 std::vector<std::size_t> parse_list(const std::string& s) {
   std::vector<std::size_t> out;
@@ -271,16 +307,22 @@ int cmd_pi(const Args& a) {
     }
   }
   const auto sv_iters = parse_list(get(a, "sv_iters"));
+  const auto x_iters = parse_list(get(a, "x_iters"));
   std::ofstream log(out + ".log");
   SolveStats st;
   const double t0 = now_s();
   g_t0 = t0;
+  const bool replay = !sv_iters.empty() || !x_iters.empty() || getu(a, "replay", 0);
+  // stock call timed per iteration through its own log lines (time=1)
+  StampBuf stamp(log.rdbuf(), t0);
+  std::ostream stamped(&stamp);
+  std::ostream* log_out = (!replay && getu(a, "time", 0)) ? &stamped : &log;
   ComplexTensor x =
-      (!sv_iters.empty() || getu(a, "replay", 0))
-          ? pi_replay(ym, mask, acfg.enable_spirit ? &g : nullptr, hcfg, acfg, &log, &st,
-                      sv_iters, out, getu(a, "time", 0) != 0)
-          : shlr_pi_reconstruct(ym, mask, acfg.enable_spirit ? &g : nullptr, hcfg, acfg,
-                                &log, &st);
+      replay ? pi_replay(ym, mask, acfg.enable_spirit ? &g : nullptr, hcfg, acfg, &log, &st,
+                         sv_iters, out, getu(a, "time", 0) != 0, x_iters)
+             : shlr_pi_reconstruct(ym, mask, acfg.enable_spirit ? &g : nullptr, hcfg, acfg,
+                                   log_out, &st);
+  log_out->flush();
   const double secs = now_s() - t0;
   write_cplx(x, out + ".x.cplx");
   write_stats(out + ".stats", st, secs);

@@ -369,8 +369,23 @@ def _param_args(y: np.ndarray, dataset: bool, mask: SamplingMask, hcfg: HankelCo
     a.max_outer, a.cg_max = acfg.max_outer, acfg.cg_max
     a.enable_vc = int(acfg.enable_vc)
     if slices is not None:
-        a.slice_begin, a.slice_end = int(slices[0]), int(slices[1])
+        b, e = _check_slices(slices, m, dataset)
+        if b == e:
+            raise ValueError("recon_param_dataset: empty slice range")
+        a.slice_begin, a.slice_end = b, e
     return a
+
+
+def _check_slices(slices, m: int, dataset: bool = True) -> Tuple[int, int]:
+    """Validated FE-slice range [begin, end) of a dataset of m slices (an
+    empty range is valid: a rank with no slices).  The C-ABI reads (0, 0) as
+    "all slices", so an empty range must never reach it."""
+    if not dataset:
+        raise ValueError("recon_param_dataset: a slice range needs a dataset")
+    b, e = int(slices[0]), int(slices[1])
+    if not 0 <= b <= e <= m:
+        raise ValueError("recon_param_dataset: slice range outside the dataset")
+    return b, e
 
 
 def _run_param(a: ShlrParamArgs, out_shape, log, what: str):
@@ -420,6 +435,11 @@ def recon_param_dataset(y: ParameterDataset, mask: SamplingMask, hcfg: HankelCon
     data = np.asarray(y.data)
     if mask.rows != data.shape[1] or mask.cols != data.shape[2]:
         raise ValueError("recon_param_dataset: mask dims mismatch")
+    if slices is not None and _check_slices(slices, data.shape[0])[0] == slices[1]:
+        # empty shard (more ranks than FE slices): nothing to solve
+        if total_iters is not None:
+            total_iters.append(0)
+        return ParameterDataset(np.empty((0,) + data.shape[1:], np.complex128), list(y.tes_ms))
     a = _param_args(data, True, mask, hcfg, acfg, keep, slices)
     shape = data.shape if slices is None else (slices[1] - slices[0],) + data.shape[1:]
     x, st = _run_param(a, shape, log, "recon_param_dataset")
@@ -493,7 +513,8 @@ def hankel_svt_batched(vecs: np.ndarray, p: int, tau: float, want_sv: bool = Tru
     """Config-5 unit on host complex128 arrays: vecs (B, Nc, N) ->
     (adjoint vectors (B, Nc, N), singular values (B, d) descending, or None
     with want_sv=False -- the exact singular values need the full eigen-solver,
-    which covers d <= 128; without them d up to 248 runs (wide matrices))."""
+    which covers d <= 128; without them the subspace levels run any d up to
+    248, tall or wide)."""
     v = _c128(vecs)
     b, nc, n = v.shape
     q = n - p + 1

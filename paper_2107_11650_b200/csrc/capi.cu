@@ -312,6 +312,13 @@ int shlr_cuda_hankel_svt_batched(const void* vecs, int batch, int nc, int n, int
   return guarded([&] {
     if (batch < 0 || nc < 1 || n < 1 || p < 1 || p > n || tau < 0 || !vecs || !out)
       throw shlr_b200::InvalidArg("hankel_svt_batched: invalid arguments");
+    {
+      const size_t bytes = (size_t)batch * nc * n * sizeof(float2);
+      const char* a = static_cast<const char*>(vecs);
+      const char* b = static_cast<const char*>(out);
+      if (bytes && a < b + bytes && b < a + bytes)
+        throw shlr_b200::InvalidArg("hankel_svt_batched: out overlaps vecs");
+    }
     require_device();
     shlr_b200::hankel_svt_batched_device(static_cast<const float2*>(vecs), batch, nc, n, p, tau,
                                          static_cast<float2*>(out), sv_out,
@@ -462,6 +469,10 @@ int shlr_cuda_param_plan_download(shlr_param_plan* plan, double* x_out, shlr_sta
     }
     if (err == 1) return fail(SHLR_EDIVERGE, "cg_solve: non-finite residual");
     if (err == 2) return fail(SHLR_EDIVERGE, "cg_solve: operator not positive definite");
+    if (err == 3)
+      return fail(SHLR_EUNSUPPORTED,
+                  "shlr_param_reconstruct_slice: more singular values above the threshold than the "
+                  "large-d subspace levels hold");
     return SHLR_OK;
   });
 }

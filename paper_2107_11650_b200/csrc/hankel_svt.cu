@@ -1629,8 +1629,9 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
       const int b = t / F.q;
       lofs[t] = (b << 16) | (t - b * F.q);
     }
-    // tall (plain modes only): the adjoint accumulates into this matrix's
-    // own output region across chunks (every chunk touches every block)
+    // tall: the adjoint accumulates into this matrix's own output region
+    // across chunks (every chunk touches every block); the output must not
+    // alias the spectra (read again in every pass)
     if (!F.wide) {
       float2* op = F.out + (long long)mat * F.o_mat;
       for (int t = tid; t < J * len; t += NT) {
@@ -2042,21 +2043,39 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
     if (to_defl) {
       // Z1 mode: no duals, no adjoint (level 3 finishes the matrix)
     } else if (BIG && !F.wide) {
-      // tall, plain modes: out_b[n] += sum_i T[i][b q + n - i] over this
-      // chunk's rows, read-modify-write of the CTA's own output region
+      // tall: out_b[n] += sum_i T[i][b q + n - i] over this chunk's rows,
+      // read-modify-write of the CTA's own output region.  Weighted lifts
+      // apply the adjoint weighting to the chunk's partial sums (it is linear
+      // per n): regular block b adds conj(wc[n]) s at (n, coil b); after a
+      // barrier, virtual-coil block b adds wc[n] conj(s) at (dagger(n), coil
+      // b - J), the same output slots (adjoint_lift_weighted,
+      // operators.cpp:60-91)
       const int q = F.q;
       float2* op = F.out + (long long)mat * F.o_mat;
       const int nlo = i0, nhi = min(len - 1, i0 + rows - 1 + q - 1);
       const int span = nhi - nlo + 1;
-      for (int o = tid; o < B * span; o += NT) {
-        const int b = o / span, n = nlo + o % span;
-        const int ilo = max(i0, n - q + 1), ihi = min(i0 + rows - 1, n);
-        float2 sacc = make_float2(0.f, 0.f);
-        for (int i = ilo; i <= ihi; ++i) sacc = cadd(sacc, C[(i - i0) * CS + b * q + (n - i)]);
-        float2* dst = op + (long long)n * F.o_n + (long long)b * F.o_j;
-        *dst = cadd(*dst, sacc);
+      const int npass = (weighted && F.vc) ? 2 : 1;
+      for (int pass = 0; pass < npass; ++pass) {
+        for (int o = tid; o < B * span; o += NT) {
+          const int b = o / span, n = nlo + o % span;
+          const bool vcb = weighted && F.vc && b >= J;
+          if (vcb != (pass == 1)) continue;
+          const int ilo = max(i0, n - q + 1), ihi = min(i0 + rows - 1, n);
+          float2 sacc = make_float2(0.f, 0.f);
+          for (int i = ilo; i <= ihi; ++i) sacc = cadd(sacc, C[(i - i0) * CS + b * q + (n - i)]);
+          if (!weighted) {
+            float2* dst = op + (long long)n * F.o_n + (long long)b * F.o_j;
+            *dst = cadd(*dst, sacc);
+          } else if (!vcb) {
+            float2* dst = op + (long long)n * F.o_n + (long long)b * F.o_j;
+            *dst = cadd(*dst, cmulc(wl[n], sacc));
+          } else {
+            float2* dst = op + (long long)dagger_src(n, len) * F.o_n + (long long)(b - J) * F.o_j;
+            *dst = cadd(*dst, cmul(wl[n], cconj(sacc)));
+          }
+        }
+        __syncthreads();
       }
-      __syncthreads();
     } else if (BIG) {
       // blocks b_lo..b_hi touch this chunk; a block whose rows continue into
       // the next chunk is carried (acc[par]), the one carried in from the
@@ -2181,9 +2200,11 @@ bool launch_level(const SvtParams& prm, int total, cudaStream_t stream) {
   if (g.dmin < kSubspaceKB + 24) return false;
   if (g.dmax > 128) {
     // large-d variant (spectra and adjoint not resident)
-    // tall large-d lifts: plain modes only (the adjoint accumulates in the
-    // output without the weighting / virtual-coil combination)
-    if ((!g.all_wide && prm.mode == SVT_ADMM_WEIGHTED) || g.maxLen > 0xffff) return false;
+    // (tall lifts accumulate the adjoint in the zeroed output, weighted and
+    // virtual-coil blocks included; plain lifts have no virtual coils)
+    if (g.maxLen > 0xffff) return false;
+    for (int f = 0; f < prm.nfam; ++f)
+      if (prm.fam[f].vc && prm.mode != SVT_ADMM_WEIGHTED) return false;
     const int dpb = svt_big_padded_dim(g.dmax);
     if (!dpb) return false;
     constexpr int KB = L2 ? kSubspaceKBBig : kSubspaceKB;

@@ -345,6 +345,7 @@ ParamPlan::ParamPlan(const ParamConfig& cfg, const double* y, const uint8_t* mas
     vpe_ = dalloc_s<float2>((size_t)S * L * dp_pe_ * dp_pe_, stream_);
     vspe_ = dalloc_s<float2>((size_t)S * L * svt_subspace_store_dim(d) * kSubspaceKB, stream_);
     vspe2_ = dalloc_s<float2>((size_t)S * L * svt_subspace_store_dim(d) * (d > 128 ? kSubspaceKBBig : kSubspaceKB), stream_);
+    if (d > 128) z1pe_ = dalloc_s<float2>(dpe_elems_, stream_);  // large-d level 3
     fallback_ = dalloc_s<int>((size_t)S * L, stream_);
     diag_ = dalloc_s<int>((size_t)S * L, stream_);
     SHLR_CUDA(cudaMemsetAsync(diag_, 0, sizeof(int) * S * L, stream_));
@@ -405,7 +406,7 @@ ParamPlan::~ParamPlan() {
   if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
   if (graph_) cudaGraphDestroy(graph_);
   void* bufs[] = {x0_, yk_, x_, xold_, r_, p_, bk_, hpe_, ximg_, hecho_, dg_, hpe0_, hecho0_, wcN_, twN_,
-                  dpe_, decho_, vpe_, vecho_, vspe_, vspe2_, fallback_, diag_, halt_, have_v_, ctl_, log_};
+                  dpe_, decho_, vpe_, vecho_, vspe_, vspe2_, z1pe_, fallback_, diag_, halt_, have_v_, ctl_, log_};
   for (void* b : bufs)
     if (b) cudaFreeAsync(b, stream_);
   if (ev0_) cudaEventDestroy(ev0_);
@@ -519,6 +520,7 @@ void ParamPlan::enqueue_iteration(bool record_events) {
     SvtParams sp = svt_params(true);
     sp.sweeps_out = diag_;
     sp.fam[0].Vs2 = vspe2_;
+    sp.fam[0].Z1 = z1pe_;
     int nl = 0;
     // PE lifts are low rank (mean 15-17 above the threshold at config 4):
     // a 32-column level 1, 48-column level 2, then the full solver
@@ -631,6 +633,14 @@ void ParamPlan::download(double* x_out, std::vector<int>* outer, std::vector<dou
                       (int)l[1], l[2]);
         log_lines->push_back(buf);
       }
+  }
+  if (!*error && dp_pe_ > 128 && subspace_used_) {
+    // large-d PE lifts: a matrix left with more singular values above the
+    // threshold than the subspace levels hold is reported (as PiPlan does)
+    std::vector<int> fl((size_t)S * L);
+    SHLR_CUDA(cudaMemcpy(fl.data(), fallback_, fl.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    for (int f : fl)
+      if (f == kLevelOverflow) *error = 3;
   }
 }
 

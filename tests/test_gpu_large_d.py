@@ -69,3 +69,61 @@ def test_gpu_svt_unit_large_d_deflated_level3(gpu):
     adj_o, sv_o = O.hankel_svt_unit(v, p, tau)
     assert (sv_o > tau).sum(axis=1).min() > 64
     assert rel(adj, adj_o) < TOL
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,j,pencil,vc,spirit,iters", [
+    (160, 8, 144, False, False, 10),   # plain SHLR, K = 17: 144 x 136 (tall, d = 136)
+    (180, 4, 162, True, False, 10),    # SHLR-V: 162 x 152 (tall, d = 152)
+    (180, 4, 162, True, True, 8),      # SHLR-SV: SPIRiT + virtual coils, tall d = 152
+])
+def test_gpu_pi_tall_weighted_large_d_vs_oracle(gpu, m, j, pencil, vc, spirit, iters):
+    """Tall weighted lifts with 128 < d <= 248 (p > B q: SHLR-V / SHLR-SV at
+    256^2 x 8 with K = 15 lift to 242 x 240, plain SHLR with K = 17..28 to
+    240..229 x 136..224): the large-d subspace levels with the adjoint
+    weighting conj(wc) and the virtual-coil dagger applied to each chunk's
+    partial anti-diagonal sums (adjoint_lift_weighted, operators.cpp:60-91)."""
+    from paper_2107_11650_b200 import synth
+    A = gpu
+    q = m - pencil + 1
+    blocks = j * (2 if vc else 1)
+    assert pencil > blocks * q > 128  # tall, large d
+    ph = synth.pi_phantom(m, m, j)
+    mask = A.mask_gauss_cartesian(m, 0.3, 16, 11650)
+    y = np.where(mask.bits[0][None, :, None].astype(bool), ph.kspace, 0)
+    g = None
+    if spirit:
+        a0, a1 = A.acs_range(m, 16)
+        g = A.spirit_calibrate(y[:, a0:a1, :], 5)
+    acfg = A.AdmmConfig(max_outer=iters, tol=1e-300, enable_vc=vc, enable_spirit=spirit)
+    log = []
+    x = A.shlr_pi_reconstruct(y, mask, g, A.HankelConfig(pencil=pencil), acfg, log=log)
+    xo, st = O.shlr_pi_reconstruct(
+        y, O.SamplingMask(1, m, mask.bits), O.SpiritKernels(5, j, g.weights) if spirit else None,
+        O.HankelConfig(pencil=pencil),
+        O.AdmmConfig(max_outer=iters, tol=1e-300, enable_vc=vc, enable_spirit=spirit))
+    assert rel(x, xo) < TOL
+    assert [l.split()[2] for l in log] == [l.split()[2] for l in st.log]  # cg_iters
+
+
+@pytest.mark.gpu
+def test_gpu_param_tall_weighted_large_d_pe_lift(gpu):
+    """Parameter path with PE lifts 180 x 168 (N = 200, 4 coils + virtual
+    coils, pencil 180: tall weighted, d = 168 > 128): the large-d levels with a
+    Z1 buffer (deflated level 3) behind them, against the oracle."""
+    A = gpu
+    rng = np.random.default_rng(3)
+    m, n, l, j, pencil = 2, 200, 12, 4, 180
+    t = np.arange(n)[:, None, None]
+    sig = sum(rng.standard_normal((1, l, j)) * np.exp(1j * rng.uniform(0, 2 * np.pi) * t) for _ in range(6))
+    y = np.stack([sig + 0.05 * (rng.standard_normal((n, l, j)) + 1j * rng.standard_normal((n, l, j)))
+                  for _ in range(m)])
+    bits = np.stack([O.mask_gauss_cartesian(n, 0.4, 16, 40 + e).bits[0] for e in range(l)], axis=1)
+    y = y * bits[None, :, :, None]
+    acfg = dict(max_outer=4, tol=1e-300, enable_vc=True)
+    x = A.recon_param_dataset(A.ParameterDataset(y, [10.0 * (e + 1) for e in range(l)]),
+                              A.SamplingMask(n, l, bits), A.HankelConfig(pencil=pencil),
+                              A.AdmmConfig(**acfg)).data
+    xo, _ = O.recon_param_dataset(y, O.SamplingMask(n, l, bits), O.HankelConfig(pencil=pencil),
+                                  O.AdmmConfig(**acfg))
+    assert rel(x, xo) < TOL

@@ -7,6 +7,7 @@ import socket
 import subprocess
 import sys
 
+import numpy as np
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -97,3 +98,25 @@ def test_parameter_slices_shard_over_ranks(m):
     assert ranges[0][0] == 0 and ranges[-1][1] == m
     assert all(ranges[i][1] == ranges[i + 1][0] for i in range(len(ranges) - 1))
     assert all(e > b for b, e in ranges)
+
+
+def test_empty_shard_never_reaches_the_device(api):
+    """More ranks than FE slices: shard_range gives some ranks an empty range.
+    The C-ABI reads slice range (0, 0) as "all slices", so the host mirror
+    returns an empty dataset without calling it (no device, no D2H copy into a
+    0-slice buffer); inverted or out-of-range shards are rejected."""
+    A = api
+    m = 1
+    assert A.shard_range(m, 2, 0) == (0, 0)
+    y = np.zeros((m, 8, 3, 2), np.complex128)
+    ds = A.ParameterDataset(y, [10.0, 20.0, 30.0])
+    mask = A.SamplingMask(8, 3, np.ones((8, 3), np.uint8))
+    tot = []
+    out = A.recon_param_dataset(ds, mask, A.HankelConfig(), A.AdmmConfig(max_outer=1), total_iters=tot,
+                                slices=A.shard_range(m, 2, 0))
+    assert out.data.shape == (0, 8, 3, 2) and tot == [0]
+    for bad in [(1, 0), (0, 2), (-1, 1)]:
+        with pytest.raises(ValueError):
+            A.recon_param_dataset(ds, mask, A.HankelConfig(), A.AdmmConfig(max_outer=1), slices=bad)
+    with pytest.raises(ValueError):
+        A.ParamPlan(y, mask, A.HankelConfig(), A.AdmmConfig(max_outer=1), slices=(0, 0))
