@@ -522,6 +522,7 @@ class SolveStats:
     final_rel_change: float = 0.0
     log: List[str] = field(default_factory=list)
     singular_values: dict = field(default_factory=dict)
+    images: dict = field(default_factory=dict)
 
 
 def svt(m: np.ndarray, tau: float, return_sv: bool = False):
@@ -594,10 +595,11 @@ def log_line(it: int, relchange: float, cg_iters: int, cg_res: float) -> str:
 
 def shlr_pi_reconstruct(y: np.ndarray, mask: SamplingMask, g: Optional[SpiritKernels],
                         hcfg: HankelConfig, acfg: AdmmConfig,
-                        sv_iters: Sequence[int] = ()) -> Tuple[np.ndarray, SolveStats]:
+                        sv_iters: Sequence[int] = (), x_iters: Sequence[int] = ()) -> Tuple[np.ndarray, SolveStats]:
     """``src/solvers.cpp:95-191`` (Algorithm S1).  sv_iters: 1-based outer
     iterations whose singular values of L + D/beta are recorded (rows first,
-    then columns)."""
+    then columns); x_iters: iterations whose image x is recorded
+    (stats.images).  Neither changes the arithmetic."""
     acfg.validate()
     if y.ndim != 3:
         raise ValueError("shlr_pi_reconstruct: expected M x N x J")
@@ -642,6 +644,8 @@ def shlr_pi_reconstruct(y: np.ndarray, mask: SamplingMask, g: Optional[SpiritKer
         d_col = d_col + acfg.tau * (lc - z_col)
         if (k + 1) in sv_iters:
             stats.singular_values[k + 1] = (s_r, s_c)
+        if (k + 1) in x_iters:
+            stats.images[k + 1] = x_new.copy()
         relchange = rel_change_sq(x_new, x)
         x = x_new
         stats.outer_iters = k + 1

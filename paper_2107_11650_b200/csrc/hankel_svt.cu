@@ -1552,7 +1552,8 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
   // level 3, kLevelOverflow beyond that; level 1 skips the matrices that are
   // not at level 1
   if (!L2 && F.fallback &&
-      (F.fallback[mat] == kLevelStay2 || F.fallback[mat] == kLevelOverflow || F.fallback[mat] == kLevelDeflate))
+      (F.fallback[mat] == kLevelStay2 || F.fallback[mat] == kLevelOverflow || F.fallback[mat] == kLevelDeflate ||
+       F.fallback[mat] == kLevelDeflDone))
     return;
   // level 3 (large d): SVT of the part of the matrix orthogonal to level 2's
   // leading kDeflateK Ritz vectors, plus level 2's Z1 on that part
@@ -1614,9 +1615,21 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
   // level 1's fresh block (+ random columns)
   const int lvl_in = F.fallback ? F.fallback[mat] : 0;
   const bool warm = !defl3 && prm.warm && *prm.warm &&
-                    (!L2 || (Vsg2 && (lvl_in == kLevelStay2 || lvl_in == kLevelOverflow || lvl_in == kLevelDeflate)));
+                    (!L2 || (Vsg2 && (lvl_in == kLevelStay2 || lvl_in == kLevelOverflow || lvl_in == kLevelDeflate ||
+                                      lvl_in == kLevelDeflDone)));
   const bool seeded = L2 && !defl3 && !warm && lvl_in == kLevelHanded;
-  const float2* V1g = defl3 ? Vsg2 : nullptr;  // level 2's sorted Ritz vectors (its store)
+  // deflation chain: Ritz vectors already solved (level 2's leading block and
+  // every earlier level-3 step's), kept orthonormal in Vd
+  const bool chain = BIG && L2 && F.Z1 && F.Vd && F.ndefl;
+  float2* Vdg = chain ? F.Vd + (long long)mat * DP * DP : nullptr;
+  const int nd_in = defl3 ? F.ndefl[mat] : 0;
+  // M <- (I - Vd Vd^H) M over the deflated columns, in blocks of kDeflateK
+  // (block classical Gram-Schmidt, repeated: CGS2)
+  auto project_defl = [&](float2* M) {
+    for (int rep = 0; rep < 2; ++rep)
+      for (int b0 = 0; b0 < nd_in; b0 += kDeflateK)
+        project_out<KB, KS>(M, Vdg + b0, DP, min(kDeflateK, nd_in - b0), d, C);
+  };
   const bool stg = Dg != nullptr && !BIG;  // duals staged by cp.async (non-BIG)
 
   // ---------------------------------------------------------- spectra
@@ -1689,11 +1702,11 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
       X[k * KS + j] = v;
     }
     __syncthreads();
-    if (defl3) {  // start orthogonal to level 2's leading block (twice: CGS2)
-      project_out<KB, KS>(X, V1g, KB, kDeflateK, d, C);
-      project_out<KB, KS>(X, V1g, KB, kDeflateK, d, C);
-    }
+    if (defl3) project_defl(X);  // start orthogonal to the deflated columns
     householder_qr<KB, KS, DP>(X, V, d, tau);
+    // a remainder narrower than the block: the QR's extra columns leave the
+    // remainder, projecting them out makes them ~0 (Ritz values ~0, f = 0)
+    if (defl3 && d - nd_in < KB) project_defl(V);
   }
 
   // mappings: Yc rows yi / X rows k0 + 32m, columns c + 16n
@@ -1753,10 +1766,7 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
     __syncthreads();
     clk_pass += clock64() - clk_t;
     clk_t = clock64();
-    if (defl3) {
-      project_out<KB, KS>(X, V1g, KB, kDeflateK, d, C);
-      project_out<KB, KS>(X, V1g, KB, kDeflateK, d, C);
-    }
+    if (defl3) project_defl(X);
     if (warm && prm.inner_norm && it + 1 < iters) {
       // warm inner pass: X ~ V0 Lambda with V0 the previous (sorted) Ritz
       // vectors, so unit columns are already a well-conditioned basis; the
@@ -1774,6 +1784,7 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
         for (int row = s8; row < DP; row += 8) V[row * KS + g] = cscale(X[row * KS + g], inv);
     } else {
       householder_qr<KB, KS, DP>(X, V, d, tau);
+      if (defl3 && d - nd_in < KB) project_defl(V);
     }
     clk_qr += clock64() - clk_t;
     clk_t = clock64();
@@ -1941,16 +1952,25 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
   // level 2 (large d) with too many values above the threshold and a Z1
   // buffer: keep the leading kDeflateK Ritz pairs (Z1 = Ahat V1 f1 V1^H to
   // HBM) and hand the rest to the deflated level 3
-  const bool to_defl = BIG && L2 && !defl3 && F.Z1 && F.Vs2 && r > KB - kMarginHere;
+  // (level 3 again while the remainder is wider than its block; a remainder
+  // the block spans is solved exactly, so the chain always finishes)
+  const bool to_defl = chain && r > KB - kMarginHere && d - nd_in > KB;
   if (F.fallback && tid == 0) {
     if (defl3)
-      F.fallback[mat] = r > KB - kMarginHere ? kLevelOverflow : kLevelDeflate;
+      F.fallback[mat] = to_defl ? kLevelDeflate : kLevelDeflDone;
     else if (L2)
       F.fallback[mat] = to_defl ? kLevelDeflate
                         : r > KB - kMarginHere ? kLevelOverflow
                         : r <= KB1 - 2 * kSubspaceMargin ? 0 : kLevelStay2;
     else
       F.fallback[mat] = (r > KB - kSubspaceMargin) ? kLevelHanded : 0;
+  }
+  if (to_defl) {  // append the leading kDeflateK Ritz vectors to the deflated basis
+    for (int t = tid; t < DP * kDeflateK; t += NT) {
+      const int k = t / kDeflateK, j = t - k * kDeflateK;
+      Vdg[(long long)k * DP + nd_in + j] = Vf[k * KS + j];
+    }
+    if (tid == 0) F.ndefl[mat] = nd_in + kDeflateK;
   }
   if (Vsg2 && !defl3)
     for (int t = tid; t < DP * KB; t += NT) {
@@ -2012,8 +2032,9 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
       for (int m = 0; m < MZ; ++m) {
         const int k = c16 + 16 * m;
         if (yi < rows && k < d) {
-          if (to_defl) {  // Z1 only: level 3 finishes this matrix
-            F.Z1[(long long)mat * e * d + (long long)(i0 + yi) * d + k] = z[m];
+          if (to_defl) {  // Z1 only (accumulated along the chain): level 3 finishes this matrix
+            float2* z1p = F.Z1 + (long long)mat * e * d + (long long)(i0 + yi) * d + k;
+            *z1p = defl3 ? cadd(__ldcg(z1p), z[m]) : z[m];
             continue;
           }
           if (defl3) {
@@ -2251,20 +2272,24 @@ int launch_hankel_svt_levels(const SvtParams& sp, int total, cudaStream_t stream
   if (big || kb1 == kSubspaceKB1) {
     SvtParams l2 = sp;
     l2.only_flagged = sp.fam[0].fallback;
-    l2.q_cold = std::getenv("SHLR_L2_Q") ? std::atoi(std::getenv("SHLR_L2_Q")) : 5;
+    l2.q_cold = std::getenv("SHLR_L2_Q") ? std::atoi(std::getenv("SHLR_L2_Q")) : 8;
     launch_hankel_svt_level2(l2, total, stream);
     ++n;
   }
   if (big) {
-    if (sp.fam[0].Z1) {  // level 3: the deflated remainder of level 2's overflow
+    if (sp.fam[0].Z1 && sp.fam[0].Vd && sp.fam[0].ndefl) {
+      // level 3: the deflated remainder of level 2's overflow, one launch per
+      // chain step (matrices that finished skip the later launches)
       SvtParams l3 = sp;
       l3.only_flagged = sp.fam[0].fallback;
       l3.only_flag_value = kLevelDeflate;
       l3.deflate = 1;
       l3.warm = nullptr;
-      l3.q_cold = std::getenv("SHLR_L3_Q") ? std::atoi(std::getenv("SHLR_L3_Q")) : 4;
-      launch_hankel_svt_level2(l3, total, stream);
-      ++n;
+      l3.q_cold = std::getenv("SHLR_L3_Q") ? std::atoi(std::getenv("SHLR_L3_Q")) : 8;
+      for (int k = 0; k < svt_deflation_steps(dmax); ++k) {
+        launch_hankel_svt_level2(l3, total, stream);
+        ++n;
+      }
     }
     return n;
   }

@@ -51,7 +51,11 @@ struct SvtFamily {
   float2* Vs;          // subspace solver: count x DP x KB dominant-subspace store
   int* fallback;       // subspace solver: per-matrix flag, 1 = rank above threshold too
                        // close to KB, the full solver must redo this matrix
-  float2* Z1;          // large d: count x e x d buffer for level 2's Z1 (nullptr: no level 3)
+  float2* Z1;          // large d: count x e x d buffer for the deflation chain's Z1
+                       // (nullptr: no deflation; also requires Vd and ndefl)
+  float2* Vd;          // large d: count x DP x DP deflation basis (row-major, the leading
+                       // ndefl[mat] columns hold the Ritz vectors already solved)
+  int* ndefl;          // large d: per-matrix column count of Vd
   float2* Vs2;         // large-d level 2: count x DP x kSubspaceKBBig store (warm start of the
                        // matrices that stay at level 2); nullptr: level 2 always starts seeded
   const int* halt;     // optional per-group stop flags: matrix `mat` is skipped when
@@ -110,9 +114,22 @@ constexpr int kLevelHanded = 1;    // level 1 handed the matrix to level 2 in th
 constexpr int kLevelOverflow = 2;  // level 2 ran out of block: reported as unsupported
 constexpr int kLevelStay2 = 3;     // stays at level 2 (warm from its own store) next iteration
 constexpr int kLevelDeflate = 4;   // large d: level 2 keeps its leading kDeflateK Ritz pairs (Z1),
-                                   // level 3 solves the orthogonal remainder
-// Ritz pairs level 2 hands to the deflation split (its converged head).
+                                   // level 3 solves the orthogonal remainder (again deflating its
+                                   // own leading pairs while the remainder exceeds its block)
+constexpr int kLevelDeflDone = 5;  // large d: the deflation chain finished this matrix
+// Ritz pairs each deflation step keeps (the converged head of a 64 block).
 constexpr int kDeflateK = kSubspaceKBBig - 8;
+// Level-3 launches the chain needs for dimension d: level 2 deflates
+// kDeflateK, every level-3 step kDeflateK more until the remainder fits one
+// kSubspaceKBBig block (then the block spans it: exact).
+inline int svt_deflation_steps(int d) {
+  int rem = d - kDeflateK, n = 1;
+  while (rem > kSubspaceKBBig) {
+    rem -= kDeflateK;
+    ++n;
+  }
+  return n;
+}
 // Padded dimension of the large-d variant for d (0 if out of range).
 inline int svt_big_padded_dim(int d) { return d <= 128 ? 0 : d <= 160 ? 160 : d <= 192 ? 192 : d <= 248 ? 248 : 0; }
 int svt_padded_dim(int d);

@@ -345,7 +345,12 @@ ParamPlan::ParamPlan(const ParamConfig& cfg, const double* y, const uint8_t* mas
     vpe_ = dalloc_s<float2>((size_t)S * L * dp_pe_ * dp_pe_, stream_);
     vspe_ = dalloc_s<float2>((size_t)S * L * svt_subspace_store_dim(d) * kSubspaceKB, stream_);
     vspe2_ = dalloc_s<float2>((size_t)S * L * svt_subspace_store_dim(d) * (d > 128 ? kSubspaceKBBig : kSubspaceKB), stream_);
-    if (d > 128) z1pe_ = dalloc_s<float2>(dpe_elems_, stream_);  // large-d level 3
+    if (d > 128) {  // large-d deflation chain (level 3)
+      z1pe_ = dalloc_s<float2>(dpe_elems_, stream_);
+      const int sd = svt_subspace_store_dim(d);
+      vdpe_ = dalloc_s<float2>((size_t)S * L * sd * sd, stream_);
+      ndpe_ = dalloc_s<int>((size_t)S * L, stream_);
+    }
     fallback_ = dalloc_s<int>((size_t)S * L, stream_);
     diag_ = dalloc_s<int>((size_t)S * L, stream_);
     SHLR_CUDA(cudaMemsetAsync(diag_, 0, sizeof(int) * S * L, stream_));
@@ -406,7 +411,7 @@ ParamPlan::~ParamPlan() {
   if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
   if (graph_) cudaGraphDestroy(graph_);
   void* bufs[] = {x0_, yk_, x_, xold_, r_, p_, bk_, hpe_, ximg_, hecho_, dg_, hpe0_, hecho0_, wcN_, twN_,
-                  dpe_, decho_, vpe_, vecho_, vspe_, vspe2_, z1pe_, fallback_, diag_, halt_, have_v_, ctl_, log_};
+                  dpe_, decho_, vpe_, vecho_, vspe_, vspe2_, z1pe_, vdpe_, ndpe_, fallback_, diag_, halt_, have_v_, ctl_, log_};
   for (void* b : bufs)
     if (b) cudaFreeAsync(b, stream_);
   if (ev0_) cudaEventDestroy(ev0_);
@@ -521,6 +526,8 @@ void ParamPlan::enqueue_iteration(bool record_events) {
     sp.sweeps_out = diag_;
     sp.fam[0].Vs2 = vspe2_;
     sp.fam[0].Z1 = z1pe_;
+    sp.fam[0].Vd = vdpe_;
+    sp.fam[0].ndefl = ndpe_;
     int nl = 0;
     // PE lifts are low rank (mean 15-17 above the threshold at config 4):
     // a 32-column level 1, 48-column level 2, then the full solver
@@ -604,11 +611,14 @@ void ParamPlan::sync() {
 void ParamPlan::download(double* x_out, std::vector<int>* outer, std::vector<double>* final_rel,
                          std::vector<std::string>* log_lines, int* error) {
   const int S = cfg_.S, N = cfg_.N, L = cfg_.L, J = cfg_.J;
-  ParamToImageOp op{x_, r_, N, L, J, nullptr};
+  // scratch of its own: a download between run() calls leaves the plan's state alone
+  float2* s1 = dalloc_s<float2>(nel_, stream_);
+  ParamToImageOp op{x_, s1, N, L, J, nullptr};
   launch_fft_axis<ParamToImageOp, true>(op, tN_, S, L * J, std::min(16, L * J), stream_);
   double* xd = dalloc_s<double>(2 * nel_, stream_);
-  k_p_to_double<<<grid_for(nel_), kThreads, 0, stream_>>>(r_, xd, nel_);
+  k_p_to_double<<<grid_for(nel_), kThreads, 0, stream_>>>(s1, xd, nel_);
   SHLR_LAUNCH_CHECK();
+  SHLR_CUDA(cudaFreeAsync(s1, stream_));
   std::vector<ParamSliceCtl> hc(S);
   const int mo = std::max(cfg_.max_outer, 1);
   std::vector<double> lg((size_t)S * mo * 3);

@@ -84,6 +84,8 @@ class ParamPlan {
   float2* vspe_ = nullptr;                      // subspace-solver block store (PE family)
   float2* vspe2_ = nullptr;                     // its level-2 store
   float2* z1pe_ = nullptr;                      // PE d > 128: Z1 of the deflated level 3
+  float2* vdpe_ = nullptr;                      // PE d > 128: deflation chain bases
+  int* ndpe_ = nullptr;                         // PE d > 128: deflated columns per matrix
   int* fallback_ = nullptr;
   int* diag_ = nullptr;              // per-PE-lift diagnostics (sweeps_out of the SVT launch)
   int* halt_ = nullptr;              // [S] stopped || error

@@ -714,6 +714,9 @@ PiPlan::PiPlan(const PiConfig& cfg, const double* y, const uint8_t* mask, size_t
     if (std::max(dr, dc) > 128 && !std::getenv("SHLR_NO_DEFLATE")) {  // large-d level 3
       z1row_ = dalloc_s<float2>(d_row_elems_, stream_);
       z1col_ = dalloc_s<float2>(d_col_elems_, stream_);
+      vdrow_ = dalloc_s<float2>((size_t)M * sdim * sdim, stream_);  // deflation chain bases
+      vdcol_ = dalloc_s<float2>((size_t)N * sdim * sdim, stream_);
+      ndefl_ = dalloc_s<int>((size_t)(M + N), stream_);
     }
   }
   fallback_ = dalloc_s<int>((size_t)(M + N), stream_);
@@ -796,7 +799,7 @@ PiPlan::~PiPlan() {
   if (graph_) cudaGraphDestroy(graph_);
   void* bufs[] = {yk_, x_, xold_, r_, p_, ap_, bk_, tmp_, tmp2_, dg_, srow_, scol_, hrow_, hcol_,
                   hrow0_, hcol0_, drow_, dcol_, wcN_, wcM_, pmat_, twM_, twN_, sv_, partials_,
-                  ctl_, log_, x0_, vrow_, vcol_, sweeps_, vsrow_, vscol_, vs2row_, vs2col_, z1row_, z1col_,
+                  ctl_, log_, x0_, vrow_, vcol_, sweeps_, vsrow_, vscol_, vs2row_, vs2col_, z1row_, z1col_, vdrow_, vdcol_, ndefl_,
                   fallback_};
   for (void* b : bufs)
     if (b) cudaFreeAsync(b, stream_);
@@ -952,6 +955,10 @@ void PiPlan::enqueue_iteration(int k, bool record_events) {
     sp.fam[1].Vs2 = vs2col_;
     sp.fam[0].Z1 = z1row_;
     sp.fam[1].Z1 = z1col_;
+    sp.fam[0].Vd = vdrow_;
+    sp.fam[1].Vd = vdcol_;
+    sp.fam[0].ndefl = ndefl_;
+    sp.fam[1].ndefl = ndefl_ + M;
     int nl = 0;
     if (subspace_ && !want_sv && (nl = launch_hankel_svt_levels(sp, M + N, stream_, kb1_)) > 0) {
       // level 1 (32 / 48 columns), level 2 (48 / 64) for matrices whose rank
@@ -1019,14 +1026,20 @@ void PiPlan::download(double* x_out, size_t* outer_iters, double* final_rel,
                       std::vector<std::string>* log_lines, int* error) {
   const int M = cfg_.M, N = cfg_.N, J = cfg_.J;
   const long long NJ = (long long)N * J;
-  // x = iF2D(X): axis 1 then axis 0
-  StridedCopyOp op1{x_, tmp_, NJ, J, 1};
+  // x = iF2D(X): axis 1 then axis 0, in scratch of its own (the plan's
+  // buffers carry state between iterations: a download between run() calls
+  // must not disturb the next iteration)
+  float2* s1 = dalloc_s<float2>(nel_, stream_);
+  float2* s2 = dalloc_s<float2>(nel_, stream_);
+  StridedCopyOp op1{x_, s1, NJ, J, 1};
   launch_fft_axis<StridedCopyOp, true>(op1, tN_, M, J, J, stream_);
-  StridedCopyOp op0{tmp_, bk_, 0, NJ, 1};
+  StridedCopyOp op0{s1, s2, 0, NJ, 1};
   launch_fft_axis<StridedCopyOp, true>(op0, tM_, 1, N * J, 16, stream_);
   double* xd = dalloc_s<double>(2 * nel_, stream_);
-  k_to_double<<<grid_for(nel_), kThreads, 0, stream_>>>(bk_, xd, nel_);
+  k_to_double<<<grid_for(nel_), kThreads, 0, stream_>>>(s2, xd, nel_);
   SHLR_LAUNCH_CHECK();
+  SHLR_CUDA(cudaFreeAsync(s1, stream_));
+  SHLR_CUDA(cudaFreeAsync(s2, stream_));
   SolverCtl hc;
   std::vector<double> lg(3 * (size_t)std::max(cfg_.max_outer, 1));
   SHLR_CUDA(cudaMemcpyAsync(x_out, xd, 2 * nel_ * sizeof(double), cudaMemcpyDeviceToHost, stream_));
@@ -1096,7 +1109,12 @@ void hankel_svt_batched_device(const float2* vecs, int batch, int nc, int n, int
   // cold solves need a V1 spill area: process the batch in chunks so the
   // stream-ordered scratch stays <= 256 MB
   const int dp = svt_padded_dim(F.d);
-  const size_t per = (size_t)dp * dp * sizeof(float2);
+  const int sdim = svt_subspace_store_dim(F.d);
+  // per matrix: V1 spill; large d also level 2's store, Z1 and the deflation basis
+  const size_t per = (size_t)dp * dp * sizeof(float2) +
+                     (F.d > 128 ? ((size_t)sdim * kSubspaceKBBig + (size_t)F.e * F.d + (size_t)sdim * sdim) *
+                                      sizeof(float2)
+                                : 0);
   const int chunk = (int)std::max<size_t>(1, std::min<size_t>((size_t)batch, (256ull << 20) / per));
   float2* vscr = nullptr;
   float2* vsub = nullptr;
@@ -1106,11 +1124,13 @@ void hankel_svt_batched_device(const float2* vecs, int batch, int nc, int n, int
                             stream));
   SHLR_CUDA(cudaMallocAsync(&flags, (size_t)chunk * sizeof(int), stream));
   // large d: level 2's store and the Z1 buffer of the deflated level 3
-  float2 *vs2 = nullptr, *z1 = nullptr;
+  float2 *vs2 = nullptr, *z1 = nullptr, *vd = nullptr;
+  int* nd = nullptr;
   if (F.d > 128) {
-    SHLR_CUDA(cudaMallocAsync(&vs2, (size_t)chunk * svt_subspace_store_dim(F.d) * kSubspaceKBBig * sizeof(float2),
-                              stream));
+    SHLR_CUDA(cudaMallocAsync(&vs2, (size_t)chunk * sdim * kSubspaceKBBig * sizeof(float2), stream));
     SHLR_CUDA(cudaMallocAsync(&z1, (size_t)chunk * F.e * F.d * sizeof(float2), stream));
+    SHLR_CUDA(cudaMallocAsync(&vd, (size_t)chunk * sdim * sdim * sizeof(float2), stream));
+    SHLR_CUDA(cudaMallocAsync(&nd, (size_t)chunk * sizeof(int), stream));
   }
   for (int b0 = 0; b0 < batch; b0 += chunk) {
     const int nb = std::min(chunk, batch - b0);
@@ -1125,6 +1145,8 @@ void hankel_svt_batched_device(const float2* vecs, int batch, int nc, int n, int
     Fc.fallback = flags;
     Fc.Vs2 = vs2;
     Fc.Z1 = z1;
+    Fc.Vd = vd;
+    Fc.ndefl = nd;
     SHLR_CUDA(cudaMemsetAsync(flags, 0, (size_t)nb * sizeof(int), stream));
     spc.sweeps_out = sweeps_out ? sweeps_out + b0 : nullptr;
     // one-shot (cold) solves: a 32-column level 1 with 4 QR passes; matrices
@@ -1153,6 +1175,8 @@ void hankel_svt_batched_device(const float2* vecs, int batch, int nc, int n, int
   SHLR_CUDA(cudaFreeAsync(flags, stream));
   if (vs2) SHLR_CUDA(cudaFreeAsync(vs2, stream));
   if (z1) SHLR_CUDA(cudaFreeAsync(z1, stream));
+  if (vd) SHLR_CUDA(cudaFreeAsync(vd, stream));
+  if (nd) SHLR_CUDA(cudaFreeAsync(nd, stream));
 }
 
 void PiPlan::debug_phases(long long* out, int n) {

@@ -50,14 +50,17 @@ def test_gpu_svt_unit_large_d(gpu, n, nc, k):
 
 
 @pytest.mark.gpu
-def test_gpu_svt_unit_large_d_deflated_level3(gpu):
-    """242 x 480 lifts with ~90 singular values above the threshold: beyond the
-    64-column level 2, so level 2 keeps its leading 56 Ritz pairs (Z1) and the
-    deflated level 3 solves the orthogonal remainder (SVT(A) = SVT(A P1) +
-    SVT(A (I - P1)) for an invariant P1)."""
+@pytest.mark.parametrize("r,minrank", [(90, 64), (170, 125), (240, 180)])
+def test_gpu_svt_unit_large_d_deflated_level3(gpu, r, minrank):
+    """242 x 480 lifts with ~90 / ~160 / ~230 singular values above the
+    threshold: beyond the 64-column level 2, so level 2 keeps its leading 56
+    Ritz pairs (Z1) and the deflated level 3 solves the orthogonal remainder
+    (SVT(A) = SVT(A P1) + SVT(A (I - P1)) for an invariant P1), deflating its
+    own leading 56 again (the chain) while the remainder is wider than its
+    block: no rank limit."""
     A = gpu
     rng = np.random.default_rng(5)
-    n, nc, k, r = 256, 32, 15, 90
+    n, nc, k = 256, 32, 15
     p = n - k + 1
     t = np.arange(n)
     v = (rng.standard_normal((4, nc, n)) + 1j * rng.standard_normal((4, nc, n))) / np.sqrt(2)
@@ -67,7 +70,7 @@ def test_gpu_svt_unit_large_d_deflated_level3(gpu):
     tau = float(np.sqrt(p) + np.sqrt(nc * k))
     adj, _ = A.hankel_svt_batched(v, p, tau, want_sv=False)
     adj_o, sv_o = O.hankel_svt_unit(v, p, tau)
-    assert (sv_o > tau).sum(axis=1).min() > 64
+    assert (sv_o > tau).sum(axis=1).min() > minrank
     assert rel(adj, adj_o) < TOL
 
 
@@ -75,14 +78,21 @@ def test_gpu_svt_unit_large_d_deflated_level3(gpu):
 @pytest.mark.parametrize("m,j,pencil,vc,spirit,iters", [
     (160, 8, 144, False, False, 10),   # plain SHLR, K = 17: 144 x 136 (tall, d = 136)
     (180, 4, 162, True, False, 10),    # SHLR-V: 162 x 152 (tall, d = 152)
-    (180, 4, 162, True, True, 8),      # SHLR-SV: SPIRiT + virtual coils, tall d = 152
+    (180, 4, 162, True, True, 16),     # SHLR-SV: SPIRiT + virtual coils, tall d = 152
 ])
 def test_gpu_pi_tall_weighted_large_d_vs_oracle(gpu, m, j, pencil, vc, spirit, iters):
     """Tall weighted lifts with 128 < d <= 248 (p > B q: SHLR-V / SHLR-SV at
     256^2 x 8 with K = 15 lift to 242 x 240, plain SHLR with K = 17..28 to
     240..229 x 136..224): the large-d subspace levels with the adjoint
     weighting conj(wc) and the virtual-coil dagger applied to each chunk's
-    partial anti-diagonal sums (adjoint_lift_weighted, operators.cpp:60-91)."""
+    partial anti-diagonal sums (adjoint_lift_weighted, operators.cpp:60-91).
+
+    Parity point: these non-power-of-two geometries without the SPIRiT
+    term's conditioning are sensitive to FP32 perturbations in the first
+    ADMM iterations (the 15-step capped CG is not linear in its right-hand
+    side): scripts/defl_probe.py measures up to ~2e-3 at iterations 2-4 --
+    the FP32 full Jacobi solver alone gives 2.5e-4 at iteration 3 of a
+    256 x 8 case -- damped below 1e-4 by iteration ~10 (SPIRiT: ~14)."""
     from paper_2107_11650_b200 import synth
     A = gpu
     q = m - pencil + 1
@@ -107,23 +117,22 @@ def test_gpu_pi_tall_weighted_large_d_vs_oracle(gpu, m, j, pencil, vc, spirit, i
 
 
 @pytest.mark.gpu
-def test_gpu_param_tall_weighted_large_d_pe_lift(gpu):
+@pytest.mark.parametrize("fe", [100, 120])
+def test_gpu_param_tall_weighted_large_d_pe_lift(gpu, fe):
     """Parameter path with PE lifts 180 x 168 (N = 200, 4 coils + virtual
-    coils, pencil 180: tall weighted, d = 168 > 128): the large-d levels with a
-    Z1 buffer (deflated level 3) behind them, against the oracle."""
+    coils, pencil 180: tall weighted, d = 168 > 128): the large-d levels with
+    the deflation chain behind them.  One FE slice of a seeded T2 phantom
+    (shlr_param_reconstruct_slice, solvers.cpp:193-298) against the oracle."""
+    from paper_2107_11650_b200 import synth
     A = gpu
-    rng = np.random.default_rng(3)
-    m, n, l, j, pencil = 2, 200, 12, 4, 180
-    t = np.arange(n)[:, None, None]
-    sig = sum(rng.standard_normal((1, l, j)) * np.exp(1j * rng.uniform(0, 2 * np.pi) * t) for _ in range(6))
-    y = np.stack([sig + 0.05 * (rng.standard_normal((n, l, j)) + 1j * rng.standard_normal((n, l, j)))
-                  for _ in range(m)])
-    bits = np.stack([O.mask_gauss_cartesian(n, 0.4, 16, 40 + e).bits[0] for e in range(l)], axis=1)
-    y = y * bits[None, :, :, None]
-    acfg = dict(max_outer=4, tol=1e-300, enable_vc=True)
-    x = A.recon_param_dataset(A.ParameterDataset(y, [10.0 * (e + 1) for e in range(l)]),
-                              A.SamplingMask(n, l, bits), A.HankelConfig(pencil=pencil),
-                              A.AdmmConfig(**acfg)).data
-    xo, _ = O.recon_param_dataset(y, O.SamplingMask(n, l, bits), O.HankelConfig(pencil=pencil),
-                                  O.AdmmConfig(**acfg))
+    n, l, j, pencil = 200, 12, 4, 180
+    _, k, _, _ = synth.t2_phantom(n, n, j, l)
+    hybrid = O.fft_along_axis(k, 0, True)[fe]                       # N x L x J plane at one FE line
+    bits = np.stack([O.mask_gauss_cartesian(n, 0.25, 16, 40 + e).bits[0] for e in range(l)], axis=1)
+    y = hybrid * bits[:, :, None]
+    acfg = dict(max_outer=20, tol=1e-300, enable_vc=True)
+    x = A.shlr_param_reconstruct_slice(y, A.SamplingMask(n, l, bits), A.HankelConfig(pencil=pencil),
+                                       A.AdmmConfig(**acfg))
+    xo, _ = O.shlr_param_reconstruct_slice(y, O.SamplingMask(n, l, bits), O.HankelConfig(pencil=pencil),
+                                           O.AdmmConfig(**acfg))
     assert rel(x, xo) < TOL
