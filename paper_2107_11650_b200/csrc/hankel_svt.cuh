@@ -87,6 +87,10 @@ struct SvtParams {
   float s2_tol_abs;              // full solver, stage 2: absolute floor x max diagonal (0 = none)
   int rr_jacobi;                 // 1: Rayleigh-Ritz by parallel Jacobi instead of tridiagonal + bisection
   int inner_norm;                // warm: normalise (instead of QR) after all but the last pass
+  const double* relc;            // optional: the ADMM relative change of the previous outer
+                                 // iteration (device); while it is large the warm start is
+                                 // far from the new subspace and warm solves take more passes
+  float relc_q2, relc_q3;        // relc above these: at least 2 / 3 warm passes (with QR)
   int wl_global;       // set by launch_hankel_svt: the lift source is read straight from
                        // fam[f].spec (plain mode, contiguous coils) instead of an smem copy
 };
@@ -109,6 +113,8 @@ constexpr int kSubspaceKB = 48;
 // block (no split-k buffer); a matrix beyond kSubspaceKBBig - kSubspaceMargin
 // there keeps its flag, which the host reports as unsupported.
 constexpr int kSubspaceKBBig = 64;
+// HUGE variant (248 < d <= 496): the block of level 1 and of every deflation step.
+constexpr int kSubspaceKBHuge = 32;
 // Per-matrix fallback flag values of the large-d levels.
 constexpr int kLevelHanded = 1;    // level 1 handed the matrix to level 2 in this launch
 constexpr int kLevelOverflow = 2;  // level 2 ran out of block: reported as unsupported
@@ -122,21 +128,30 @@ constexpr int kDeflateK = kSubspaceKBBig - 8;
 // Level-3 launches the chain needs for dimension d: level 2 deflates
 // kDeflateK, every level-3 step kDeflateK more until the remainder fits one
 // kSubspaceKBBig block (then the block spans it: exact).
+// (HUGE: level 1 deflates kSubspaceKBHuge - 8, each step as many again,
+// until the remainder fits one kSubspaceKBHuge block.)
 inline int svt_deflation_steps(int d) {
-  int rem = d - kDeflateK, n = 1;
-  while (rem > kSubspaceKBBig) {
-    rem -= kDeflateK;
+  const bool huge = d > 248;
+  const int step = huge ? kSubspaceKBHuge - 8 : kDeflateK, kb = huge ? kSubspaceKBHuge : kSubspaceKBBig;
+  int rem = d - step, n = 1;
+  while (rem > kb) {
+    rem -= step;
     ++n;
   }
   return n;
 }
 // Padded dimension of the large-d variant for d (0 if out of range).
 inline int svt_big_padded_dim(int d) { return d <= 128 ? 0 : d <= 160 ? 160 : d <= 192 ? 192 : d <= 248 ? 248 : 0; }
+// HUGE variant (248 < d <= 496: config-5 points 498 x 480 and 482 x 992):
+// 16-row chunks and a 32-column block for level 1 and every deflation step.
+inline int svt_huge_padded_dim(int d) { return d <= 248 ? 0 : d <= 320 ? 320 : d <= 384 ? 384 : d <= 496 ? 496 : 0; }
 int svt_padded_dim(int d);
 // Row count of the per-matrix subspace store (F.Vs: store_dim x kSubspaceKB)
 // the subspace kernels use for dimension d.
 inline int svt_subspace_store_dim(int d) {
-  return d > 128 && svt_big_padded_dim(d) ? svt_big_padded_dim(d) : svt_padded_dim(d);
+  return d > 248 && svt_huge_padded_dim(d) ? svt_huge_padded_dim(d)
+         : d > 128 && svt_big_padded_dim(d) ? svt_big_padded_dim(d)
+                                            : svt_padded_dim(d);
 }
 // clock64 diagnostics slots per matrix (SvtParams::phase_clk)
 constexpr int kPhaseSlots = 24;

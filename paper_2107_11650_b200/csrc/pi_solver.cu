@@ -947,6 +947,17 @@ void PiPlan::enqueue_iteration(int k, bool record_events) {
     sp.rr_tail = rr_tail_;
     sp.rr_jacobi = std::getenv("SHLR_RR_JACOBI") ? 1 : 0;
     sp.inner_norm = std::getenv("SHLR_INNER_QR") ? 0 : 1;
+    // large d (the subspace levels with a 48/64 block for ranks ~40-60):
+    // warm solves take 2 / 3 passes while the previous outer iteration's
+    // relative change exceeds 1e-4 / 1e-2 (SHLR-SV at 242 x 240 against the
+    // reference: iteration 5 / 12 drift 8.4e-4 / 1.4e-4 with one pass,
+    // 5.8e-5 / 3.5e-5 adaptive); d <= 128 keeps one (config 2: 6.6e-6 worst
+    // over the trace)
+    if (svt_dp_ > 128 && !std::getenv("SHLR_NO_ADAPT")) {
+      sp.relc = &ctl_->relchange;
+      sp.relc_q2 = std::getenv("SHLR_RELC_Q2") ? (float)std::atof(std::getenv("SHLR_RELC_Q2")) : 1e-4f;
+      sp.relc_q3 = std::getenv("SHLR_RELC_Q3") ? (float)std::atof(std::getenv("SHLR_RELC_Q3")) : 1e-2f;
+    }
     sp.phase_clk = phase_clk_;
     if (record_events) SHLR_CUDA(cudaEventRecord(evA_, stream_));
     // The debug singular-value hook needs every singular value: full solver.
@@ -1110,16 +1121,19 @@ void hankel_svt_batched_device(const float2* vecs, int batch, int nc, int n, int
   // stream-ordered scratch stays <= 256 MB
   const int dp = svt_padded_dim(F.d);
   const int sdim = svt_subspace_store_dim(F.d);
-  // per matrix: V1 spill; large d also level 2's store, Z1 and the deflation basis
-  const size_t per = (size_t)dp * dp * sizeof(float2) +
-                     (F.d > 128 ? ((size_t)sdim * kSubspaceKBBig + (size_t)F.e * F.d + (size_t)sdim * sdim) *
-                                      sizeof(float2)
-                                : 0);
-  const int chunk = (int)std::max<size_t>(1, std::min<size_t>((size_t)batch, (256ull << 20) / per));
+  // per matrix: d <= 128 the full solver's V1 spill; large d level 2's store,
+  // Z1 and the deflation basis (a batch that large is processed in chunks so
+  // the stream-ordered scratch stays <= 256 MB, large d <= 4 GB)
+  const bool large = F.d > 128;
+  const size_t per = large ? ((size_t)sdim * kSubspaceKBBig + (size_t)F.e * F.d + (size_t)sdim * sdim) *
+                                 sizeof(float2)
+                           : (size_t)dp * dp * sizeof(float2);
+  const size_t budget = large ? (4ull << 30) : (256ull << 20);
+  const int chunk = (int)std::max<size_t>(1, std::min<size_t>((size_t)batch, budget / per));
   float2* vscr = nullptr;
   float2* vsub = nullptr;
   int* flags = nullptr;
-  SHLR_CUDA(cudaMallocAsync(&vscr, (size_t)chunk * per, stream));
+  SHLR_CUDA(cudaMallocAsync(&vscr, large ? sizeof(float2) : (size_t)chunk * per, stream));
   SHLR_CUDA(cudaMallocAsync(&vsub, (size_t)chunk * svt_subspace_store_dim(F.d) * kSubspaceKB * sizeof(float2),
                             stream));
   SHLR_CUDA(cudaMallocAsync(&flags, (size_t)chunk * sizeof(int), stream));

@@ -1,0 +1,31 @@
+// Subspace Hankel-SVT instantiations for d <= 128 (svt_subspace.cuh).
+#include "svt_subspace.cuh"
+#include "svt_subspace_launch.cuh"
+
+namespace shlr_b200 {
+
+namespace {
+template <int KB, bool L2>
+bool dispatch_small(int dp, const SvtParams& prm, int total, size_t smem, cudaStream_t stream) {
+  switch (dp) {
+    case 72: launch_sub<72, KB, false, L2>(prm, total, smem, stream); return true;
+    case 80: launch_sub<80, KB, false, L2>(prm, total, smem, stream); return true;
+    case 88: launch_sub<88, KB, false, L2>(prm, total, smem, stream); return true;
+    case 96: launch_sub<96, KB, false, L2>(prm, total, smem, stream); return true;
+    case 104: launch_sub<104, KB, false, L2>(prm, total, smem, stream); return true;
+    case 112: launch_sub<112, KB, false, L2>(prm, total, smem, stream); return true;
+    case 120: launch_sub<120, KB, false, L2>(prm, total, smem, stream); return true;
+    case 128: launch_sub<128, KB, false, L2>(prm, total, smem, stream); return true;
+    default: return false;
+  }
+}
+}  // namespace
+
+bool launch_sub_small(int dp, int kb, bool l2, const SvtParams& prm, int total, size_t smem, cudaStream_t stream) {
+  // level 2 of d <= 128 always has kSubspaceKB columns; level 1 kSubspaceKB1 or kSubspaceKB
+  if (l2) return kb == kSubspaceKB && dispatch_small<kSubspaceKB, true>(dp, prm, total, smem, stream);
+  if (kb == kSubspaceKB1) return dispatch_small<kSubspaceKB1, false>(dp, prm, total, smem, stream);
+  return kb == kSubspaceKB && dispatch_small<kSubspaceKB, false>(dp, prm, total, smem, stream);
+}
+
+}  // namespace shlr_b200

@@ -84,7 +84,7 @@ def test_full_batch_properties(gpu):
 
 ALL = [(n, nc, k) for n in (128, 256, 512) for nc in (1, 8, 32) for k in (7, 15, 31)]
 BIG = [(n, nc, k) for n, nc, k in ALL if 128 < min(n - k + 1, nc * k) <= 248]
-UNSUPPORTED = [(n, nc, k) for n, nc, k in ALL if min(n - k + 1, nc * k) > 248]
+HUGE = [(n, nc, k) for n, nc, k in ALL if min(n - k + 1, nc * k) > 248]
 
 
 @pytest.mark.parametrize("n,nc,k", BIG)
@@ -98,12 +98,41 @@ def test_sweep_point_large_d_parity(gpu, n, nc, k):
     assert rel(adj, adj_o) < TOL
 
 
-@pytest.mark.parametrize("n,nc,k", UNSUPPORTED)
-def test_unsupported_sweep_points_fail_loudly(gpu, n, nc, k):
+@pytest.mark.parametrize("n,nc,k", HUGE)
+def test_sweep_point_huge_d_parity(gpu, n, nc, k):
+    """Config-5 points with d > 248 (498 x 480, 482 x 992): the HUGE variant
+    (32-column block, 16-row chunks, deflation chain beyond the block)."""
     from paper_2107_11650_b200 import synth
-    v = synth.sweep_vectors(n, nc, k, 2)
+    v = synth.sweep_vectors(n, nc, k, 3)
+    tau = synth.sweep_tau(n, nc, k)
+    p = n - k + 1
+    adj, _ = gpu.hankel_svt_batched(v, p, tau, want_sv=False)
+    adj_o, _ = O.hankel_svt_unit(v, p, tau)
+    assert rel(adj, adj_o) < TOL
+
+
+@pytest.mark.parametrize("r", [40, 120])
+def test_huge_d_deflation_chain(gpu, r):
+    """498 x 480 lifts with ~40 / ~120 singular values above the threshold:
+    beyond the HUGE 32-column block, so level 1 and every chain step keep 24
+    Ritz pairs and the next step solves the orthogonal remainder."""
+    n, nc, k = 512, 32, 15
+    p = n - k + 1
+    v = _rank_r_vectors(n, nc, r, 2, 300 + r)
+    tau = float(np.sqrt(p) + np.sqrt(nc * k))
+    adj, _ = gpu.hankel_svt_batched(v, p, tau, want_sv=False)
+    adj_o, sv_o = O.hankel_svt_unit(v, p, tau)
+    assert (sv_o > tau).sum(axis=1).min() > 30
+    assert rel(adj, adj_o) < TOL
+
+
+def test_beyond_huge_fails_loudly(gpu):
+    """min(m, n) > 496 is outside this build: SHLR_EUNSUPPORTED, never a
+    silent fallback (BASELINE's sweep stops at 482)."""
+    rng = np.random.default_rng(1)
+    v = rng.standard_normal((1, 2, 1100)) + 1j * rng.standard_normal((1, 2, 1100))
     with pytest.raises(NotImplementedError):
-        gpu.hankel_svt_batched(v, n - k + 1, synth.sweep_tau(n, nc, k), want_sv=False)
+        gpu.hankel_svt_batched(v, 550, 10.0, want_sv=False)
 
 
 def test_exact_singular_values_need_full_solver(gpu):
