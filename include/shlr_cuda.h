@@ -152,6 +152,13 @@ typedef struct shlr_param_args {
    * problems (parammap.cpp:37-51): ranks of a multi-GPU job each take a range,
    * with no collective. */
   size_t slice_begin, slice_end;
+  /* Dataset mode only: 1 = y is already the hybrid (FE image, PE k-space) the
+   * reference's recon_param_dataset computes first (fft_along_axis(y, 0,
+   * inverse), parammap.cpp:32): the device skips its FE transform.  A caller
+   * that keeps the reference's own host FFT for that setup step (the drop-in,
+   * dropin/shlr_dropin.cpp) gets per-slice results bitwise equal to
+   * shlr_param_reconstruct_slice on the same hybrid planes. */
+  int hybrid_input;
 } shlr_param_args;
 
 /* Full parameter reconstruction, host buffers in and out.  x_out: (m ? m : 1)
@@ -215,6 +222,22 @@ int shlr_cuda_fft_along_axis(double* data, const size_t* dims, int ndim, int axi
  * register-resident FMA chain over all SMs, timed with CUDA events.  Used as
  * the roofline denominator of the FP32 Hankel-SVT kernel. */
 int shlr_cuda_fp32_peak_tflops(double* tflops);
+
+/* Image-quality metrics on the device in FP64, host
+ * buffers in and out, synchronous.
+ *   shlr_cuda_ssos   -- ssos (proj/src/io.cpp:105-117): x is m x n x j
+ *                       interleaved complex, out m x n; bitwise the reference's
+ *                       (same operation order, round-to-nearest, no FMA).
+ *   shlr_cuda_rlne   -- rlne (proj/src/metrics.cpp:9-21) over `count` pixels;
+ *                       SHLR_EINVAL for an identically zero reference.
+ *   shlr_cuda_mssim  -- mssim (metrics.cpp:23-75): mean SSIM over all 11 x 11
+ *                       Gaussian windows (sigma 1.5), C1/C2 from max(ref);
+ *                       SHLR_EINVAL for an image smaller than the window.
+ * The dimension checks of the reference's callers (RealImage shapes) stay on
+ * the host; the final sums are deterministic tree reductions. */
+int shlr_cuda_ssos(const double* x, size_t m, size_t n, size_t j, double* out);
+int shlr_cuda_rlne(const double* ref, const double* rec, size_t count, double* out);
+int shlr_cuda_mssim(const double* ref, const double* rec, size_t rows, size_t cols, double* out);
 
 /* Host-side helpers of the boundary (no GPU needed): the reference's mask
  * generators (proj/src/sampling.cpp:31-173), bit-exact. */

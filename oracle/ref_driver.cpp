@@ -23,6 +23,7 @@
 //          matrix (solvers.cpp:264-268,280-282 composition)
 //   mask   kind=gauss|random2d|uniform n= [m=] rate= acs= seed= out=
 //   calib  y= mask= acs= [kernel=5] [tikhonov=1e-4] out=
+//   metrics [x= (M x N x J) -> out.ssos.cplx] [ref= rec= (real, rank 2) -> rlne / mssim on stdout]
 #include <chrono>
 #include <cstdio>
 #include <fstream>
@@ -38,6 +39,7 @@
 #include "shlr/fft.hpp"
 #include "shlr/hankel.hpp"
 #include "shlr/io.hpp"
+#include "shlr/metrics.hpp"
 #include "shlr/operators.hpp"
 #include "shlr/parammap.hpp"
 #include "shlr/sampling.hpp"
@@ -410,6 +412,28 @@ int cmd_mask(const Args& a) {
   return 0;
 }
 
+// x= (M x N x J) -> out.ssos.cplx; with ref= and rec= (real images stored as
+// rank-2 .cplx): rlne and mssim printed with 17 digits
+int cmd_metrics(const Args& a) {
+  const std::string out = get(a, "out");
+  if (!get(a, "x").empty()) {
+    RealImage s = ssos(read_cplx(get(a, "x")));
+    ComplexTensor t({s.rows(), s.cols()});
+    for (std::size_t i = 0; i < s.size(); ++i) t[i] = cplx{s[i], 0.0};
+    write_cplx(t, out + ".ssos.cplx");
+  }
+  if (!get(a, "ref").empty()) {
+    auto to_real = [](const ComplexTensor& t) {
+      RealImage r(t.dim(0), t.dim(1));
+      for (std::size_t i = 0; i < r.size(); ++i) r[i] = t[i].real();
+      return r;
+    };
+    RealImage ref = to_real(read_cplx(get(a, "ref"))), rec = to_real(read_cplx(get(a, "rec", "\x01")));
+    std::printf("rlne=%.17g\nmssim=%.17g\n", rlne(ref, rec), mssim(ref, rec));
+  }
+  return 0;
+}
+
 int cmd_calib(const Args& a) {
   ComplexTensor y = read_cplx(get(a, "y", "\x01"));
   SamplingMask mask = read_mask(get(a, "mask", "\x01"));
@@ -444,6 +468,7 @@ int main(int argc, char** argv) {
     if (mode == "svt") return cmd_svt(a);
     if (mode == "mask") return cmd_mask(a);
     if (mode == "calib") return cmd_calib(a);
+    if (mode == "metrics") return cmd_metrics(a);
     std::fprintf(stderr, "unknown mode %s\n", mode.c_str());
     return 3;
   } catch (const DivergenceError& e) {

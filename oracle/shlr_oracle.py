@@ -733,3 +733,53 @@ def hankel_svt_unit(vecs: np.ndarray, p: int, tau: float):
     lifted = lift_plain(vecs, p)
     z, s = svt(lifted, tau, return_sv=True)
     return adjoint_lift_plain(z, n, nc), s
+
+
+# ---------------------------------------------------------------- metrics
+def ssos(x: np.ndarray) -> np.ndarray:
+    """``src/io.cpp:105-117``: sqrt(sum_k |x[r, c, k]|^2), k ascending."""
+    x = np.asarray(x)
+    if x.ndim != 3:
+        raise ValueError("ssos: expected an M x N x J tensor")
+    s = np.zeros(x.shape[:2])
+    for k in range(x.shape[2]):
+        s = s + (x[:, :, k].real * x[:, :, k].real + x[:, :, k].imag * x[:, :, k].imag)
+    return np.sqrt(s)
+
+
+def rlne(ref: np.ndarray, rec: np.ndarray) -> float:
+    """``src/metrics.cpp:9-21``: ||ref - rec|| / ||ref||."""
+    if ref.shape != rec.shape:
+        raise ValueError("rlne: dimension mismatch")
+    den = float(np.sum(ref * ref))
+    if den == 0.0:
+        raise ValueError("rlne: reference image is identically zero")
+    return float(np.sqrt(np.sum((ref - rec) ** 2) / den))
+
+
+def mssim(ref: np.ndarray, rec: np.ndarray) -> float:
+    """``src/metrics.cpp:23-75``: mean SSIM over every 11 x 11 window, Gaussian
+    weights sigma = 1.5 normalised to sum 1, C1 = (0.01 max ref)^2,
+    C2 = (0.03 max ref)^2, variances / covariance about the window means."""
+    if ref.shape != rec.shape:
+        raise ValueError("mssim: dimension mismatch")
+    k = 11
+    if ref.shape[0] < k or ref.shape[1] < k:
+        raise ValueError("mssim: image smaller than the 11x11 window")
+    d = np.arange(k) - 5.0
+    w = np.exp(-(d[:, None] ** 2 + d[None, :] ** 2) / (2.0 * 1.5 * 1.5))
+    w = w / w.sum()
+    mx = max(float(ref.max()), 0.0)
+    c1, c2 = (0.01 * mx) ** 2, (0.03 * mx) ** 2
+    from numpy.lib.stride_tricks import sliding_window_view
+    a = sliding_window_view(ref, (k, k))
+    b = sliding_window_view(rec, (k, k))
+    mu_a = np.einsum("rcij,ij->rc", a, w)
+    mu_b = np.einsum("rcij,ij->rc", b, w)
+    da = a - mu_a[:, :, None, None]
+    db = b - mu_b[:, :, None, None]
+    var_a = np.einsum("rcij,ij->rc", da * da, w)
+    var_b = np.einsum("rcij,ij->rc", db * db, w)
+    cov = np.einsum("rcij,ij->rc", da * db, w)
+    ssim = ((2 * mu_a * mu_b + c1) * (2 * cov + c2)) / ((mu_a ** 2 + mu_b ** 2 + c1) * (var_a + var_b + c2))
+    return float(ssim.mean())

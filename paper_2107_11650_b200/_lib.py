@@ -52,6 +52,7 @@ class ShlrParamArgs(C.Structure):
         ("max_outer", C.c_size_t), ("cg_max", C.c_size_t),
         ("enable_vc", C.c_int),
         ("slice_begin", C.c_size_t), ("slice_end", C.c_size_t),
+        ("hybrid_input", C.c_int),
     ]
 
 
@@ -105,6 +106,12 @@ PROTOTYPES = {
                                            C.POINTER(C.c_int32)]),
     "shlr_cuda_fft_along_axis": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_size_t), C.c_int,
                                            C.c_int, C.c_int]),
+    "shlr_cuda_ssos": (C.c_int, [C.POINTER(C.c_double), C.c_size_t, C.c_size_t, C.c_size_t,
+                                 C.POINTER(C.c_double)]),
+    "shlr_cuda_rlne": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_size_t,
+                                 C.POINTER(C.c_double)]),
+    "shlr_cuda_mssim": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_size_t, C.c_size_t,
+                                  C.POINTER(C.c_double)]),
     "shlr_mask_gauss_cartesian": (C.c_int, [C.c_size_t, C.c_double, C.c_size_t, C.c_uint64,
                                             C.POINTER(C.c_uint8)]),
     "shlr_mask_random2d": (C.c_int, [C.c_size_t, C.c_size_t, C.c_double, C.c_size_t, C.c_uint64,

@@ -544,6 +544,43 @@ def lift_index_map(n: int, p: int, coils: int, vc: bool) -> np.ndarray:
     return out
 
 
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+def ssos(x: np.ndarray) -> np.ndarray:
+    """``shlr::ssos`` (``io.hpp:31``, ``io.cpp:105-117``) on the device: the
+    root-sum-of-squares coil combination of an M x N x J image, FP64."""
+    xc = _c128(x)
+    if xc.ndim != 3:
+        raise ValueError("ssos: expected an M x N x J tensor")
+    m, n, j = xc.shape
+    out = np.empty((m, n), np.float64)
+    _check(lib.shlr_cuda_ssos(_dptr(xc), m, n, j, _dptr(out)), "ssos")
+    return out
+
+
+def rlne(ref: np.ndarray, rec: np.ndarray) -> float:
+    """``shlr::rlne`` (``metrics.hpp:17``, ``metrics.cpp:9-21``) on the device."""
+    a, b = _f64(ref), _f64(rec)
+    if a.ndim != 2 or a.shape != b.shape:
+        raise ValueError("rlne: dimension mismatch")
+    out = C.c_double()
+    _check(lib.shlr_cuda_rlne(_dptr(a), _dptr(b), a.size, C.byref(out)), "rlne")
+    return out.value
+
+
+def mssim(ref: np.ndarray, rec: np.ndarray) -> float:
+    """``shlr::mssim`` (``metrics.hpp:21``, ``metrics.cpp:23-75``) on the device:
+    mean SSIM over 11 x 11 Gaussian windows."""
+    a, b = _f64(ref), _f64(rec)
+    if a.ndim != 2 or a.shape != b.shape:
+        raise ValueError("mssim: dimension mismatch")
+    out = C.c_double()
+    _check(lib.shlr_cuda_mssim(_dptr(a), _dptr(b), a.shape[0], a.shape[1], C.byref(out)), "mssim")
+    return out.value
+
+
 def fft_along_axis(x: np.ndarray, axis: int, inverse: bool) -> np.ndarray:
     a = _c128(x).copy()
     dims = (C.c_size_t * a.ndim)(*a.shape)

@@ -6,6 +6,7 @@
 #include <vector>
 
 #include "../../include/shlr_cuda.h"
+#include "metrics.cuh"
 #include "param_solver.cuh"
 #include "pi_solver.cuh"
 
@@ -123,6 +124,7 @@ shlr_b200::ParamConfig param_config_of(const shlr_param_args* a) {
   c.dataset = a->m != 0;
   c.M_full = (int)a->m;
   c.s0 = shard ? (int)a->slice_begin : 0;
+  c.hybrid_input = a->m && a->hybrid_input;
   c.N = (int)a->n;
   c.L = (int)a->l;
   c.J = (int)a->j;
@@ -380,6 +382,34 @@ int shlr_cuda_lift_index_map(int n, int p, int coils, int vc, int32_t* map) {
       throw shlr_b200::InvalidArg("lift_index_map: invalid arguments");
     require_device();
     shlr_b200::lift_index_map_device(n, p, coils, vc, map);
+    return SHLR_OK;
+  });
+}
+
+int shlr_cuda_ssos(const double* x, size_t m, size_t n, size_t j, double* out) {
+  return guarded([&] {
+    if (!x || !out || m == 0 || n == 0 || j == 0) throw shlr_b200::InvalidArg("ssos: expected an M x N x J tensor");
+    require_device();
+    shlr_b200::ssos_host(x, m, n, j, out);
+    return SHLR_OK;
+  });
+}
+
+int shlr_cuda_rlne(const double* ref, const double* rec, size_t count, double* out) {
+  return guarded([&] {
+    if (!ref || !rec || !out || count == 0) throw shlr_b200::InvalidArg("rlne: dimension mismatch");
+    require_device();
+    *out = shlr_b200::rlne_host(ref, rec, count);
+    return SHLR_OK;
+  });
+}
+
+int shlr_cuda_mssim(const double* ref, const double* rec, size_t rows, size_t cols, double* out) {
+  return guarded([&] {
+    if (!ref || !rec || !out) throw shlr_b200::InvalidArg("mssim: dimension mismatch");
+    if (rows < 11 || cols < 11) throw shlr_b200::InvalidArg("mssim: image smaller than the 11x11 window");
+    require_device();
+    *out = shlr_b200::mssim_host(ref, rec, rows, cols);
     return SHLR_OK;
   });
 }

@@ -378,7 +378,7 @@ ParamPlan::ParamPlan(const ParamConfig& cfg, const double* y, const uint8_t* mas
     const size_t nel_in = (size_t)Mf * L * N * J;
     double* y_d = dalloc_s<double>(2 * nel_in, stream_);
     float2* a_d = dalloc_s<float2>(nel_in, stream_);
-    float2* b_d = cfg.dataset ? dalloc_s<float2>(nel_in, stream_) : nullptr;
+    float2* b_d = cfg.dataset && !cfg.hybrid_input ? dalloc_s<float2>(nel_in, stream_) : nullptr;
     uint8_t* m_d = dalloc_s<uint8_t>((size_t)N * L, stream_);
     SHLR_CUDA(cudaMemcpyAsync(y_d, y, 2 * nel_in * sizeof(double), cudaMemcpyHostToDevice, stream_));
     SHLR_CUDA(cudaMemcpyAsync(m_d, mask, (size_t)N * L, cudaMemcpyHostToDevice, stream_));
@@ -386,7 +386,9 @@ ParamPlan::ParamPlan(const ParamConfig& cfg, const double* y, const uint8_t* mas
     SHLR_LAUNCH_CHECK();
     const float2* hyb = a_d;
     float2* twM = nullptr;
-    if (cfg.dataset) {
+    if (cfg.dataset && cfg.hybrid_input) {
+      hyb = a_d + (size_t)cfg.s0 * N * L * J;
+    } else if (cfg.dataset) {
       FftTwiddles tM = make_twiddles(Mf, &twM, stream_);
       const long long inner = (long long)N * L * J;
       StridedCopyOp op{a_d, b_d, 0, inner, 1};

@@ -31,6 +31,7 @@ struct ParamConfig {
   bool vc;
   bool dataset;          // y is M x N x L x J k-space: iFFT along FE first (parammap.cpp:32)
   int M_full;            // dataset: FE lines of y (the plan solves slices [s0, s0 + S))
+  bool hybrid_input;     // dataset: y is already iFFT'd along FE (the caller did parammap.cpp:32)
   int s0;
   double lambda, lambda2, beta, tau, tol, cg_tol;
   int max_outer, cg_max;
