@@ -209,8 +209,14 @@ int shlr_cuda_debug_svt_sweeps(const void* vecs, int batch, int nc, int n, int p
  * (vc ? 2 : 1)), writes for every element (i, c), row-major, three int32:
  * source coil, source index into that coil's spectrum, conj flag (1 for the
  * conjugate-flipped virtual-coil blocks).  map must hold p*blocks*q*3 ints.
- * Computed on the device with the kernels' own index function. */
+ * Computed by running the kernels' own lift stage (spectra staging, offset
+ * table, chunk builder) on index-encoded spectra s_j[n] = (j+1) + i(n+1) with
+ * unit weights and decoding the lifted elements: path 0 = the full solver's
+ * load_chunk / lift_elem, 1 = the subspace solver's build_chunk / lift_tab,
+ * 2 = the large-d variants' build_chunk_big / lift_global (d <= 256 here).
+ * shlr_cuda_lift_index_map is path 1. */
 int shlr_cuda_lift_index_map(int n, int p, int coils, int vc, int32_t* map);
+int shlr_cuda_lift_index_map_path(int n, int p, int coils, int vc, int path, int32_t* map);
 
 /* Centered unitary FFT along one axis of a host complex128 tensor
  * (proj/src/fft.cpp:100-128), computed on the device in complex64.

@@ -104,6 +104,8 @@ PROTOTYPES = {
                                              C.c_float, C.c_void_p, C.c_void_p]),
     "shlr_cuda_lift_index_map": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int,
                                            C.POINTER(C.c_int32)]),
+    "shlr_cuda_lift_index_map_path": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                                C.POINTER(C.c_int32)]),
     "shlr_cuda_fft_along_axis": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_size_t), C.c_int,
                                            C.c_int, C.c_int]),
     "shlr_cuda_ssos": (C.c_int, [C.POINTER(C.c_double), C.c_size_t, C.c_size_t, C.c_size_t,

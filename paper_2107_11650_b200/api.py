@@ -535,12 +535,16 @@ def hankel_svt_batched_device(vecs_ptr: int, batch: int, nc: int, n: int, p: int
                                             C.c_void_p(stream or None)), "hankel_svt_batched")
 
 
-def lift_index_map(n: int, p: int, coils: int, vc: bool) -> np.ndarray:
+def lift_index_map(n: int, p: int, coils: int, vc: bool, path: int = 1) -> np.ndarray:
+    """(coil, source index, conj) of every element of the p x (blocks q)
+    weighted lift, read back from the kernels' own lift stage run on
+    index-encoded spectra: path 0 = full solver, 1 = subspace solver,
+    2 = large-d variants (``shlr_cuda_lift_index_map_path``)."""
     q = n - p + 1
     blocks = coils * (2 if vc else 1)
     out = np.empty((p, blocks * q, 3), np.int32)
-    _check(lib.shlr_cuda_lift_index_map(n, p, coils, int(vc), out.ctypes.data_as(C.POINTER(C.c_int32))),
-           "lift_index_map")
+    _check(lib.shlr_cuda_lift_index_map_path(n, p, coils, int(vc), path,
+                                             out.ctypes.data_as(C.POINTER(C.c_int32))), "lift_index_map")
     return out
 
 

@@ -376,14 +376,18 @@ int shlr_cuda_debug_svt_sweeps(const void* vecs, int batch, int nc, int n, int p
   });
 }
 
-int shlr_cuda_lift_index_map(int n, int p, int coils, int vc, int32_t* map) {
+int shlr_cuda_lift_index_map_path(int n, int p, int coils, int vc, int path, int32_t* map) {
   return guarded([&] {
-    if (n < 1 || p < 1 || p > n || coils < 1 || !map)
+    if (n < 1 || p < 1 || p > n || coils < 1 || !map || path < 0 || path > 2)
       throw shlr_b200::InvalidArg("lift_index_map: invalid arguments");
     require_device();
-    shlr_b200::lift_index_map_device(n, p, coils, vc, map);
+    shlr_b200::lift_index_map_device(n, p, coils, vc, path, map);
     return SHLR_OK;
   });
+}
+
+int shlr_cuda_lift_index_map(int n, int p, int coils, int vc, int32_t* map) {
+  return shlr_cuda_lift_index_map_path(n, p, coils, vc, 1, map);
 }
 
 int shlr_cuda_ssos(const double* x, size_t m, size_t n, size_t j, double* out) {

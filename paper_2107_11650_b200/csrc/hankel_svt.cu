@@ -19,6 +19,9 @@
 
 #include <cstdlib>
 
+#include <vector>
+
+#include "solver_util.cuh"
 #include "svt_device.cuh"
 #include "svt_subspace_launch.cuh"
 
@@ -96,20 +99,7 @@ __global__ void __maxnreg__(svt_max_regs(DP)) hankel_svt_kernel(const SvtParams 
   // ---------------------------------------------------------- phase 0
   {
     const float2* sp = F.spec + (long long)mat * F.s_mat;
-    for (int t = tid; t < (prm.wl_global ? 0 : J * len); t += NT) {
-      const int j = t / len, n = t - j * len;
-      const float2 s = sp[n * F.s_n + j * F.s_j];
-      if (weighted) {
-        S.wl[j * len + n] = cmul(F.wc[n], s);
-        if (F.vc) {
-          const int fl = dagger_src(n, len);
-          const float2 sf = sp[fl * F.s_n + j * F.s_j];
-          S.wl[(J + j) * len + n] = cmul(F.wc[n], cconj(sf));
-        }
-      } else {
-        S.wl[j * len + n] = s;
-      }
-    }
+    if (!prm.wl_global) stage_spectra(S.wl, F, sp, weighted, tid, NT);
     for (int t = tid; t < B * len; t += NT) S.acc[t] = make_float2(0.f, 0.f);
     if (tid < 4) S.flags[tid] = 0;
   }
@@ -500,6 +490,99 @@ void dispatch_r(const SvtParams& prm, int total, int maxB, int maxLen, cudaStrea
 }
 
 }  // namespace
+
+namespace {
+// Lift stage of the Hankel-SVT kernels on one matrix, dumped: the same
+// staging (stage_spectra, build_lofs) and chunk builders the kernels run --
+// path 0: load_chunk / lift_elem (full solver), path 1: build_chunk /
+// lift_tab (subspace solver, d <= 128), path 2: build_chunk_big / lift_global
+// (large-d subspace variants) -- writing Ahat (e x d, row-major).  Used on
+// index-encoded spectra by lift_index_map_device.
+constexpr int kDumpDP = 256, kDumpR = 32;
+__global__ void k_lift_dump(const SvtFamily F, int path, float2* ahat) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int CS = kDumpDP + 1;
+  float2* chunk = reinterpret_cast<float2*>(smem_raw);      // R x CS (path 0: R x DP)
+  float2* wl = chunk + kDumpR * CS;                         // B x len
+  float2* wcs = wl + F.B * F.len;                           // len
+  int* lofs = reinterpret_cast<int*>(wcs + F.len);          // max(d, e)
+  const float2* sp = F.spec;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if (path == 2) {
+    for (int t = tid; t < F.len; t += nt) wcs[t] = F.wc[t];
+    build_lofs(lofs, F, true, tid, nt);
+  } else {
+    stage_spectra(wl, F, sp, true, tid, nt);
+    build_lofs(lofs, F, false, tid, nt);
+  }
+  __syncthreads();
+  Smem<kDumpDP> S{};
+  S.wl = wl;
+  S.A = chunk;
+  for (int i0 = 0; i0 < F.e; i0 += kDumpR) {
+    const int rows = min(kDumpR, F.e - i0);
+    if (path == 0) load_chunk<kDumpDP, kDumpR>(S, F, nullptr, i0, rows, 0.f, false);
+    else if (path == 1) build_chunk<kDumpDP, CS, kDumpR>(chunk, wl, lofs, F, nullptr, i0, rows, 0.f);
+    else build_chunk_big<kDumpDP, CS, kDumpR>(chunk, F, sp, wcs, true, lofs, nullptr, i0, rows, 0.f);
+    __syncthreads();
+    const int stride = path == 0 ? kDumpDP : CS;
+    for (int t = tid; t < rows * F.d; t += nt) {
+      const int r = t / F.d, u = t - r * F.d;
+      ahat[(long long)(i0 + r) * F.d + u] = chunk[r * stride + u];
+    }
+    __syncthreads();
+  }
+}
+}  // namespace
+
+void lift_index_map_device(int n, int p, int coils, int vc, int path, int32_t* map_host) {
+  const int q = n - p + 1, J = coils, B = coils * (vc ? 2 : 1);
+  const int P = p, Bq = B * q, e = std::max(P, Bq), d = std::min(P, Bq);
+  if (d > kDumpDP || path < 0 || path > 2) throw InvalidArg("lift_index_map: geometry outside the dump kernel");
+  // index-encoded spectra: s_j[n] = (j + 1) + i (n + 1), unit weights (taps = [1])
+  std::vector<float2> spec((size_t)n * J), wc(n, make_float2(1.f, 0.f));
+  for (int t = 0; t < n; ++t)
+    for (int j = 0; j < J; ++j) spec[(size_t)t * J + j] = make_float2((float)(j + 1), (float)(t + 1));
+  float2 *dspec = util::dalloc<float2>(spec.size()), *dwc = util::dalloc<float2>(n),
+         *dah = util::dalloc<float2>((size_t)e * d);
+  SHLR_CUDA(cudaMemcpy(dspec, spec.data(), spec.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  SHLR_CUDA(cudaMemcpy(dwc, wc.data(), n * sizeof(float2), cudaMemcpyHostToDevice));
+  SvtFamily F{};
+  F.count = 1;
+  F.len = n;
+  F.P = P;
+  F.q = q;
+  F.J = J;
+  F.B = B;
+  F.vc = vc;
+  F.wide = Bq > P ? 1 : 0;
+  F.e = e;
+  F.d = d;
+  F.spec = dspec;
+  F.s_mat = 0;
+  F.s_n = J;
+  F.s_j = 1;
+  F.wc = dwc;
+  const size_t smem = sizeof(float2) * ((size_t)kDumpR * (kDumpDP + 1) + (size_t)B * n + n) + sizeof(int) * e + 64;
+  SHLR_CUDA(cudaFuncSetAttribute(k_lift_dump, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+  k_lift_dump<<<1, 512, smem>>>(F, path, dah);
+  SHLR_LAUNCH_CHECK();
+  std::vector<float2> ah((size_t)e * d);
+  SHLR_CUDA(cudaMemcpy(ah.data(), dah, ah.size() * sizeof(float2), cudaMemcpyDeviceToHost));
+  cudaFree(dspec);
+  cudaFree(dwc);
+  cudaFree(dah);
+  // decode A[i][c] (Ahat = A tall, A^H wide): coil = re - 1, index = |im| - 1, conj = im < 0
+  for (int i = 0; i < P; ++i)
+    for (int c = 0; c < Bq; ++c) {
+      float2 v = F.wide ? ah[(size_t)c * d + i] : ah[(size_t)i * d + c];
+      if (F.wide) v.y = -v.y;
+      int32_t* m = map_host + 3 * ((size_t)i * Bq + c);
+      m[0] = (int32_t)lrintf(v.x) - 1;
+      m[1] = (int32_t)lrintf(fabsf(v.y)) - 1;
+      m[2] = v.y < 0.f ? 1 : 0;
+    }
+}
 
 void launch_hankel_svt(const SvtParams& prm, int total, cudaStream_t stream) {
   if (total <= 0) return;

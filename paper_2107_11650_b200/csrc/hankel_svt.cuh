@@ -189,27 +189,12 @@ constexpr int kSmallSvtMaxLJ = 64;
 bool small_svt_applicable(const SvtParams& prm);
 bool launch_small_svt(const SvtParams& prm, cudaStream_t stream);
 
-// Index function shared by the kernel and shlr_cuda_lift_index_map: source
-// of element (i, c) of the p x (blocks*q) weighted lift (operators.cpp:36-56,
-// hankel.cpp:31-41): regular block b < J reads coil b at i + t; vc block
-// b >= J reads coil b - J at dagger_src(i + t) with conjugation.
-struct LiftSrc {
-  int coil, idx, conj;
-};
-__host__ __device__ __forceinline__ LiftSrc lift_source(int i, int c, int q, int J, int len) {
-  const int b = c / q, t = c - b * q;
-  LiftSrc s;
-  if (b < J) {
-    s.coil = b;
-    s.idx = i + t;
-    s.conj = 0;
-  } else {
-    s.coil = b - J;
-    s.idx = dagger_src(i + t, len);
-    s.conj = 1;
-  }
-  return s;
-}
+// Hankel lift index map of a p x (blocks q) weighted lift as the kernels
+// build it (operators.cpp:36-56, hankel.cpp:31-41,99-113): the lift stage of
+// path 0 (full solver), 1 (subspace solver) or 2 (large-d variants) run on
+// index-encoded spectra, decoded to (coil, source index, conj) per element,
+// row-major (map_host: 3 p blocks q int32).
+void lift_index_map_device(int n, int p, int coils, int vc, int path, int32_t* map_host);
 
 size_t svt_smem_bytes(int DP, int R, int maxB, int maxLen, bool wl_smem = true);
 int svt_padded_dim(int d);

@@ -1245,30 +1245,6 @@ void fft_along_axis_host(double* data, const size_t* dims, int ndim, int axis, b
   cudaStreamDestroy(st);
 }
 
-namespace {
-__global__ void k_lift_map(int n, int p, int coils, int vc, int32_t* map) {
-  const int q = n - p + 1;
-  const int blocks = coils * (vc ? 2 : 1);
-  const int total = p * blocks * q;
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
-    const int i = t / (blocks * q), c = t % (blocks * q);
-    const LiftSrc s = lift_source(i, c, q, coils, n);
-    map[3 * t] = s.coil;
-    map[3 * t + 1] = s.idx;
-    map[3 * t + 2] = s.conj;
-  }
-}
-}  // namespace
-
-void lift_index_map_device(int n, int p, int coils, int vc, int32_t* map_host) {
-  const int q = n - p + 1;
-  const size_t total = (size_t)p * coils * (vc ? 2 : 1) * q;
-  int32_t* d = dalloc<int32_t>(3 * total);
-  k_lift_map<<<grid_for(total), kThreads>>>(n, p, coils, vc, d);
-  SHLR_LAUNCH_CHECK();
-  SHLR_CUDA(cudaMemcpy(map_host, d, 3 * total * sizeof(int32_t), cudaMemcpyDeviceToHost));
-  cudaFree(d);
-}
 
 namespace {
 // 8 independent FMA chains per thread, unrolled; FLOPs = 2 per FMA.

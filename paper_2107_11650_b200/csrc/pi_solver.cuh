@@ -124,7 +124,6 @@ void hankel_svt_batched_device(const float2* vecs, int batch, int nc, int n, int
                                float2* out, float* sv, cudaStream_t stream,
                                int* sweeps_out = nullptr);
 void fft_along_axis_host(double* data, const size_t* dims, int ndim, int axis, bool inverse);
-void lift_index_map_device(int n, int p, int coils, int vc, int32_t* map_host);
 double fp32_peak_probe();
 
 }  // namespace shlr_b200

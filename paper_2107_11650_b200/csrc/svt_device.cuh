@@ -83,6 +83,39 @@ struct Smem {
   float* scal;   // 4
 };
 
+// Stage the J coil spectra of one lifted matrix in shared memory
+// (lift_weighted, operators.cpp:25-58): weighted modes hold wc[n] s_j[n] in
+// block j and, with virtual coils, wc[n] conj(s_j[dagger(n)]) in block J + j
+// (hankel.cpp:99-113); plain modes hold s_j[n].  Threads tid, tid + nt, ...
+__device__ __forceinline__ void stage_spectra(float2* wl, const SvtFamily& F, const float2* sp, bool weighted,
+                                              int tid, int nt) {
+  const int len = F.len, J = F.J;
+  for (int t = tid; t < J * len; t += nt) {
+    const int j = t / len, n = t - j * len;
+    const float2 s = sp[n * F.s_n + j * F.s_j];
+    if (weighted) {
+      wl[j * len + n] = cmul(F.wc[n], s);
+      if (F.vc) {
+        const int fl = dagger_src(n, len);
+        const float2 sf = sp[fl * F.s_n + j * F.s_j];
+        wl[(J + j) * len + n] = cmul(F.wc[n], cconj(sf));
+      }
+    } else {
+      wl[j * len + n] = s;
+    }
+  }
+}
+
+// Per-index lift offsets over the lifted matrix's block index (columns of A
+// when tall, rows of A^H when wide): b * len + t for the smem-staged spectra
+// (lift_tab), (b << 16) | t for the L2-resident spectra (lift_global).
+__device__ __forceinline__ void build_lofs(int* lofs, const SvtFamily& F, bool packed, int tid, int nt) {
+  for (int t = tid; t < (F.wide ? F.e : F.d); t += nt) {
+    const int b = t / F.q;
+    lofs[t] = packed ? ((b << 16) | (t - b * F.q)) : (b * F.len + (t - b * F.q));
+  }
+}
+
 // Ahat chunk rows [i0, i0 + rows) into S.A (zero padded to R x DP); with
 // want_d the raw D rows go to S.X.
 template <int DP, int R>

@@ -767,10 +767,7 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
     for (int t = tid; t < len; t += NT) wl[t] = weighted ? F.wc[t] : make_float2(1.f, 0.f);
     for (int t = tid; t < 2 * len; t += NT) acc[t] = make_float2(0.f, 0.f);
     // block/shift of the lifted index: rows of Ahat (wide) or its columns (tall)
-    for (int t = tid; t < (F.wide ? e : d); t += NT) {
-      const int b = t / F.q;
-      lofs[t] = (b << 16) | (t - b * F.q);
-    }
+    build_lofs(lofs, F, true, tid, NT);
     // tall: the adjoint accumulates into this matrix's own output region
     // across chunks (every chunk touches every block); the output must not
     // alias the spectra (read again in every pass)
@@ -784,26 +781,9 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
     if (tid < 4) S.flags[tid] = 0;
     if (tid == 0) *cnt = 0;
   } else {
-    const float2* sp = spg;
-    for (int t = tid; t < J * len; t += NT) {
-      const int j = t / len, n = t - j * len;
-      const float2 s = sp[n * F.s_n + j * F.s_j];
-      if (weighted) {
-        wl[j * len + n] = cmul(F.wc[n], s);
-        if (F.vc) {
-          const int fl = dagger_src(n, len);
-          const float2 sf = sp[fl * F.s_n + j * F.s_j];
-          wl[(J + j) * len + n] = cmul(F.wc[n], cconj(sf));
-        }
-      } else {
-        wl[j * len + n] = s;
-      }
-    }
+    stage_spectra(wl, F, spg, weighted, tid, NT);
     for (int t = tid; t < B * len; t += NT) acc[t] = make_float2(0.f, 0.f);
-    for (int t = tid; t < (F.wide ? e : d); t += NT) {
-      const int b = t / F.q;
-      lofs[t] = b * len + (t - b * F.q);
-    }
+    build_lofs(lofs, F, false, tid, NT);
     if (tid < 4) S.flags[tid] = 0;
     if (tid == 0) *cnt = 0;
   }

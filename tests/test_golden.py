@@ -153,14 +153,19 @@ def test_gpu_svt_matches_reference(gpu, path):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("path", [0, 1, 2])
 @pytest.mark.parametrize("n,p,coils,vc", [(20, 7, 3, False), (20, 7, 3, True), (21, 8, 2, True),
-                                          (256, 242, 8, False), (256, 23, 4, True)])
-def test_gpu_lift_index_map_bit_exact(gpu, n, p, coils, vc):
-    """The device lift's (coil, source index, conj) map equals the reference
-    lift_weighted order (operators.cpp:36-56): regular blocks, then vc blocks
-    reading the dagger index (hankel.cpp:99-113)."""
+                                          (256, 242, 8, False), (256, 23, 4, True), (256, 242, 8, True),
+                                          (180, 162, 4, True), (15, 5, 2, True)])
+def test_gpu_lift_index_map_bit_exact(gpu, n, p, coils, vc, path):
+    """The kernels' own lift stage -- run on index-encoded spectra and decoded
+    (shlr_cuda_lift_index_map_path): path 0 the full solver's lift_elem, 1 the
+    subspace solver's lift_tab, 2 the large-d lift_global -- gives the
+    reference lift_weighted order (operators.cpp:36-56) bit for bit: regular
+    blocks, then vc blocks reading the dagger index (hankel.cpp:99-113),
+    conjugated.  Tall and wide, odd and even lengths."""
     A = gpu
-    got = A.lift_index_map(n, p, coils, vc)
+    got = A.lift_index_map(n, p, coils, vc, path)
     q = n - p + 1
     blocks = coils * (2 if vc else 1)
     want = np.zeros((p, blocks * q, 3), np.int32)
