@@ -377,7 +377,8 @@ def gpu_arm(args, dist, rank, world, local):
         if rank == 0 and not args.no_cpu:
             extra["config4_param"]["cpu_baseline"] = param_cpu_baseline()
         extra["config3_large_d"] = large_d_workload(args, dist, world, fp32_peak)
-        extra["config5_sweep"] = sweep_workload(args, fp32_peak)
+        extra["config5_sweep"] = sweep_workload(args, fp32_peak, cpu=rank == 0 and not args.no_cpu)
+        extra["config2_shlr_sv"] = sv_workload(args, dist, world, fp32_peak)
         extra["config1_small"] = small_workload(args, dist, world, rank, fp32_peak)
 
     value = world * args.steps / (t_max_ms * 1e-3)
@@ -556,6 +557,52 @@ def large_d_workload(args, dist, world, fp32_peak):
     return out
 
 
+def sv_workload(args, dist, world, fp32_peak):
+    """SHLR-SV (SPIRiT + virtual coils, the paper's most accurate variant) on
+    the config-2 inputs: 256^2 x 8 coils, K = 15 -> 512 lifted 242 x 240
+    matrices per iteration (tall weighted, d = 240: the large-d subspace
+    levels).  Resident-plan iterations/s over iterations 4.. (after
+    --warmup), with the adaptive warm passes of the first iterations excluded
+    only by the warm-up.  The reference needs ~283 s per iteration on one core
+    (tests/golden/make_sv_golden.py: 12 iterations in 57 min)."""
+    from paper_2107_11650_b200 import api as A
+    cfg = CFG2
+    y, mask, g, hcfg = make_inputs(cfg)
+    acfg = A.AdmmConfig(lam=cfg["lam"], lambda1=cfg["lambda1"], beta=cfg["beta"], tau=cfg["tau"],
+                        max_outer=max(50, args.warmup + args.steps), tol=1e-300, cg_max=cfg["cg_max"],
+                        cg_tol=cfg["cg_tol"], enable_spirit=True, enable_vc=True)
+    plan = A.PiPlan(y, mask, g, hcfg, acfg)
+    plan.run(args.warmup)
+    plan.sync()
+    barrier(dist)
+    plan.run(args.steps)
+    plan.sync()
+    _, total_ms, launches = plan.timing()
+    t_max_ms = max_over_ranks(dist, total_ms)
+    plan.download()
+    plan.close()
+    e, d = 242, 240
+    flops = 512 * svt_flops(e, d)
+    out = {"workload": "config2 inputs, SHLR-SV (SPIRiT + virtual coils): 512 lifted 242x240 matrices/iter",
+           "value": world * args.steps / (t_max_ms * 1e-3), "unit": "iterations/s",
+           "ms_per_step": t_max_ms / args.steps, "gpu_launches_per_step": launches,
+           "algorithmic_tflops_whole_step": flops / (t_max_ms / args.steps * 1e-3) / 1e12,
+           "reference_cpu": {"value": 1.0 / 283.0, "unit": "iterations/s", "cores": 1,
+                             "sample": "offline: the reference's 12-iteration fixture run (make_sv_golden.py)"}}
+    if not args.no_e2e:
+        barrier(dist)
+        acfg.max_outer = cfg["outer"]
+        t0 = time.perf_counter()
+        st = A.SolveStats()
+        A.shlr_pi_reconstruct(y, mask, g, hcfg, acfg, stats=st)
+        t_e2e = max_over_ranks(dist, time.perf_counter() - t0)
+        out["e2e"] = {"value": world * st.outer_iters / t_e2e, "unit": "iterations/s",
+                      "h2d_bytes_per_step": int(y.size * 16 + mask.bits.size + g.weights.size * 16),
+                      "d2h_bytes_per_step": int(y.size * 16),
+                      "step": "one 50-iteration shlr_cuda_pi_reconstruct call with host buffers"}
+    return out
+
+
 def small_workload(args, dist, world, rank, fp32_peak):
     """BASELINE config 1 (the reference's CPU-runnable case): 128^2 x 8 coils,
     SHLR (no SPIRiT, no vc), R = 4 Gaussian Cartesian with 16 ACS lines,
@@ -608,49 +655,126 @@ def small_workload(args, dist, world, rank, fp32_peak):
     return out
 
 
-SWEEP_POINTS = [(128, 8, 15), (256, 1, 15), (256, 8, 7), (256, 8, 15), (256, 8, 31), (256, 32, 15),
-                (256, 32, 7), (512, 8, 15), (512, 8, 31), (512, 32, 7)]
+SWEEP_POINTS = [(n, nc, k) for n in (128, 256, 512) for nc in (1, 8, 32) for k in (7, 15, 31)]
+HBM_GBS = 6552.0  # MEASURED_PEAKS.json hbm_gbs (copy bandwidth) on this pool's B200s
 
 
-def sweep_workload(args, fp32_peak):
-    """BASELINE config 5 (batched Hankel-SVT unit, slices = 1, batch = 2N) at a
-    few sweep points: device-resident complex64 vectors in and out through the
-    device-pointer C-ABI call (lift_plain -> svt -> adjoint_lift_plain, cold:
-    the unit has no warm start), CUDA events around the call on its stream."""
+def hbm_peak() -> float:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f).get("hbm_gbs", HBM_GBS))
+    except (OSError, ValueError):
+        return HBM_GBS
+
+
+def sweep_cpu_rates(points, budget_s: float = 2.0):
+    """Host-core reference rate of every sweep point: oracle/_ref/ref_driver
+    svt (the reference's lift_plain -> svt -> adjoint_lift_plain, unmodified,
+    single-threaded) on the point's first matrices, `limit` sized for about
+    `budget_s` seconds from a 1.5 GFLOP/s estimate; the points run
+    concurrently, one process per host core."""
+    from paper_2107_11650_b200 import synth
+    from paper_2107_11650_b200.cplx_io import write_cplx
+    if not os.path.exists(REF_DRIVER):
+        return {}
+    tmp = tempfile.mkdtemp(prefix="shlr_sweep_")
+    jobs = []
+    try:
+        for n, nc, k in points:
+            p = n - k + 1
+            e, d = max(p, nc * k), min(p, nc * k)
+            est = svt_flops(e, d) / 1.5e9
+            limit = int(max(1, min(2 * n, np.ceil(budget_s / max(est, 1e-9)))))
+            name = f"v{n}_{nc}_{k}.cplx"
+            write_cplx(synth.sweep_vectors(n, nc, k, limit), os.path.join(tmp, name))
+            jobs.append(((n, nc, k), [REF_DRIVER, "svt", f"vecs={name}", f"p={p}",
+                                      f"tau={synth.sweep_tau(n, nc, k)}", "time=1", f"limit={limit}"]))
+        out, running = {}, []
+        ncpu = max(1, os.cpu_count() or 1)
+        queue = list(jobs)
+        while queue or running:
+            while queue and len(running) < ncpu:
+                key, cmd = queue.pop(0)
+                running.append((key, subprocess.Popen(cmd, cwd=tmp, stdout=subprocess.PIPE, text=True,
+                                                      env=dict(os.environ, OMP_NUM_THREADS="1"))))
+            key, proc = running.pop(0)
+            txt = proc.communicate(timeout=900)[0]
+            for tok in txt.split():
+                if tok.startswith("matrices="):
+                    mats = int(tok.split("=")[1])
+                elif tok.startswith("seconds="):
+                    secs = float(tok.split("=")[1])
+            out[key] = {"matrices_per_s_per_core": mats / secs, "sample": f"{mats} matrices, {secs:.2f} s, 1 core"}
+        return out
+    finally:
+        shutil.rmtree(tmp, ignore_errors=True)
+
+
+def sweep_workload(args, fp32_peak, cpu: bool = True):
+    """BASELINE config 5 (batched Hankel-SVT unit): all 27 points N x Nc x K,
+    batch = 2N slices, slices in {1, 16}; device-resident complex64 vectors in
+    and out through the device-pointer C-ABI call (lift_plain -> svt ->
+    adjoint_lift_plain, cold: the unit has no warm start), CUDA events around
+    the call on its stream.  slices = 16 tiles the 2N seeded matrices of slice
+    0 sixteen times (every matrix is solved independently; generating 32N
+    distinct seeded matrices on the host would take minutes at N = 512,
+    Nc = 32).  Beside each point: matrices/s, algorithmic TFLOP/s and its
+    fraction of the FP32 peak, HBM GB/s of the sweep's own bytes (16 Nc N per
+    matrix: vectors in, adjoint out) and its fraction of the measured copy
+    bandwidth, and the host-core reference rate."""
     import torch
     from paper_2107_11650_b200 import api as A
     from paper_2107_11650_b200 import synth
+    hbm = hbm_peak()
+    cpu_rates = sweep_cpu_rates(SWEEP_POINTS) if cpu else {}
+    ncpu = os.cpu_count() or 1
     out = []
     for n, nc, k in SWEEP_POINTS:
         p = n - k + 1
-        batch = 2 * n
-        v = synth.sweep_vectors(n, nc, k, batch)
+        e, d = max(p, nc * k), min(p, nc * k)
+        v1 = synth.sweep_vectors(n, nc, k, 2 * n).astype(np.complex64)
         tau = synth.sweep_tau(n, nc, k)
-        dv = torch.from_numpy(v.astype(np.complex64)).cuda()
-        do = torch.empty_like(dv)
-        st = torch.cuda.Stream()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        try:
-            with torch.cuda.stream(st):
-                A.hankel_svt_batched_device(dv.data_ptr(), batch, nc, n, p, tau, do.data_ptr(), 0, st.cuda_stream)
-                st.synchronize()
-                reps = 3
-                e0.record(st)
-                for _ in range(reps):
+        base = torch.from_numpy(v1).cuda()
+        for slices in (1, 16):
+            batch = 2 * n * slices
+            rec = {"N": n, "Nc": nc, "K": k, "slices": slices, "matrix": f"{p}x{nc * k}", "batch": batch}
+            try:
+                dv = base.repeat(slices, 1, 1) if slices > 1 else base
+                do = torch.empty_like(dv)
+                st = torch.cuda.Stream()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                with torch.cuda.stream(st):
                     A.hankel_svt_batched_device(dv.data_ptr(), batch, nc, n, p, tau, do.data_ptr(), 0,
                                                 st.cuda_stream)
-                e1.record(st)
-                st.synchronize()
-            ms = e0.elapsed_time(e1) / reps
-            e, d = max(p, nc * k), min(p, nc * k)
-            tf = batch * svt_flops(e, d) / (ms * 1e-3) / 1e12
-            out.append({"N": n, "Nc": nc, "K": k, "matrix": f"{p}x{nc * k}", "batch": batch,
-                        "matrices_per_s": batch / (ms * 1e-3), "ms": ms, "algorithmic_tflops": tf,
-                        "frac_of_fp32_peak": tf / fp32_peak})
-        except Exception as exc:  # geometry outside this build
-            out.append({"N": n, "Nc": nc, "K": k, "unsupported": str(exc)[:160]})
-    return {"workload": "config5: batched Hankel-SVT unit, CN(0,1) + rank-K/2 exponentials, tau = sqrt(m)+sqrt(n), "
-                        "batch 2N (slices 1), cold solves", "points": out}
+                    st.synchronize()
+                    reps = 3 if slices == 1 else 1
+                    e0.record(st)
+                    for _ in range(reps):
+                        A.hankel_svt_batched_device(dv.data_ptr(), batch, nc, n, p, tau, do.data_ptr(), 0,
+                                                    st.cuda_stream)
+                    e1.record(st)
+                    st.synchronize()
+                ms = e0.elapsed_time(e1) / reps
+                tf = batch * svt_flops(e, d) / (ms * 1e-3) / 1e12
+                gbs = batch * 16.0 * nc * n / (ms * 1e-3) / 1e9
+                rec.update({"ms": ms, "matrices_per_s": batch / (ms * 1e-3), "algorithmic_tflops": tf,
+                            "frac_of_fp32_peak": tf / fp32_peak, "hbm_gbs": gbs, "frac_of_hbm": gbs / hbm,
+                            "bound": "fp32" if tf / fp32_peak >= gbs / hbm else "hbm"})
+                c = cpu_rates.get((n, nc, k))
+                if c:
+                    rec["cpu_reference"] = dict(c, all_cores_matrices_per_s=c["matrices_per_s_per_core"] * ncpu,
+                                                cores=ncpu)
+                    rec["speedup_vs_all_host_cores"] = rec["matrices_per_s"] / (c["matrices_per_s_per_core"] * ncpu)
+                del dv, do
+            except Exception as exc:  # geometry outside this build
+                rec["unsupported"] = str(exc)[:160]
+            out.append(rec)
+        del base
+        torch.cuda.empty_cache()
+    return {"workload": "config5: batched Hankel-SVT unit, all 27 points N in {128,256,512} x Nc in {1,8,32} x "
+                        "K in {7,15,31}, CN(0,1) + rank-K/2 exponentials, tau = sqrt(m)+sqrt(n), batch 2N x "
+                        "slices, slices in {1,16}, cold solves",
+            "host_cores": ncpu, "points": out}
 
 
 def reference_arm(args, dist, rank, world):

@@ -351,6 +351,14 @@ bool launch_level(const SvtParams& prm, int total, cudaStream_t stream) {
   const SubGeom g = sub_geom(prm);
   if (!g.stores) return false;
   // worthwhile only when the level-1 block is well below d
+  if (g.dmax < 72) {  // small d: 16-column level 1, 32-column level 2
+    if (g.dmin < kSubspaceSmallMinD) return false;
+    constexpr int KBs = L2 ? kSubspaceKB1 : kSubspaceKBSmall;
+    const int dp = svt_padded_dim(g.dmax);
+    const size_t smem = svt_subspace_smem_bytes(dp, KBs, 32, g.maxB, g.maxLen, g.maxE, false);
+    if (smem > 227 * 1024) return false;
+    return launch_sub_small(dp, KBs, L2, prm, total, smem, stream);
+  }
   if (g.dmin < kSubspaceKB + 24) return false;
   if (g.dmax > 248) {
     // HUGE variant: 32-column block, 16-row chunks (every level is KB 32)
@@ -394,8 +402,9 @@ bool launch_hankel_svt_subspace(const SvtParams& prm, int total, cudaStream_t st
 int launch_hankel_svt_levels(const SvtParams& sp, int total, cudaStream_t stream, int kb1) {
   int dmax = 0;
   for (int f = 0; f < sp.nfam; ++f) dmax = std::max(dmax, sp.fam[f].d);
-  const bool big = dmax > 128, huge = dmax > 248;
+  const bool big = dmax > 128, huge = dmax > 248, small = dmax < 72;
   if (big) kb1 = kSubspaceKB;
+  if (small) kb1 = kSubspaceKBSmall;
   // HUGE level 1 hands its leading 24 of 32 Ritz pairs to the chain when the
   // rank exceeds the block: cold starts need 8 passes for that head to be
   // invariant enough (4 left 1.5e-4 at rank ~40, 8 left < 1e-4)
@@ -403,7 +412,7 @@ int launch_hankel_svt_levels(const SvtParams& sp, int total, cudaStream_t stream
   if (huge) s1.q_cold = std::max(s1.q_cold, 8);
   if (!launch_hankel_svt_subspace(s1, total, stream, kb1)) return 0;
   int n = 1;
-  if ((big && !huge) || kb1 == kSubspaceKB1) {  // (HUGE: level 1 hands straight to the chain)
+  if ((big && !huge) || kb1 == kSubspaceKB1 || small) {  // (HUGE: level 1 hands straight to the chain)
     SvtParams l2 = sp;
     l2.only_flagged = sp.fam[0].fallback;
     l2.q_cold = std::getenv("SHLR_L2_Q") ? std::atoi(std::getenv("SHLR_L2_Q")) : 8;
@@ -430,7 +439,7 @@ int launch_hankel_svt_levels(const SvtParams& sp, int total, cudaStream_t stream
   // the full solver redoes what the last subspace level handed on (cold)
   SvtParams fs = sp;
   fs.only_flagged = sp.fam[0].fallback;
-  fs.only_flag_value = kb1 == kSubspaceKB1 ? kLevelOverflow : kLevelHanded;
+  fs.only_flag_value = (kb1 == kSubspaceKB1 || small) ? kLevelOverflow : kLevelHanded;
   fs.warm = nullptr;
   launch_hankel_svt(fs, total, stream);
   return n + 1;

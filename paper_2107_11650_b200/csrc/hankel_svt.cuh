@@ -106,6 +106,10 @@ constexpr float kS2TolAbs = 1e-8f;
 // kSubspaceKBBig, then nothing.
 constexpr int kSubspaceKB1 = 32;
 constexpr int kSubspaceKB = 48;
+// Small d (40 <= d < 72, config-5 points 250 x 56, 122 x 56, 506 x 56): level 1
+// with kSubspaceKBSmall columns, level 2 with kSubspaceKB1, then the full solver.
+constexpr int kSubspaceKBSmall = 16;
+constexpr int kSubspaceSmallMinD = 40;
 // Large-d variant (128 < d <= 248, wide matrices): the same block size, with
 // spectra and adjoint accumulators not resident in shared memory.  Its
 // fallback for matrices whose rank above the threshold exceeds

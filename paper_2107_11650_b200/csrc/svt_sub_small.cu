@@ -1,4 +1,4 @@
-// Subspace Hankel-SVT instantiations for d <= 128 (svt_subspace.cuh).
+// Subspace Hankel-SVT instantiations for 40 <= d <= 128 (svt_subspace.cuh).
 #include "svt_subspace.cuh"
 #include "svt_subspace_launch.cuh"
 
@@ -19,10 +19,26 @@ bool dispatch_small(int dp, const SvtParams& prm, int total, size_t smem, cudaSt
     default: return false;
   }
 }
+// 40 <= d < 72: 16-column level 1, 32-column level 2
+template <int KB, bool L2>
+bool dispatch_smalld(int dp, const SvtParams& prm, int total, size_t smem, cudaStream_t stream) {
+  switch (dp) {
+    case 40: launch_sub<40, KB, false, L2>(prm, total, smem, stream); return true;
+    case 48: launch_sub<48, KB, false, L2>(prm, total, smem, stream); return true;
+    case 56: launch_sub<56, KB, false, L2>(prm, total, smem, stream); return true;
+    case 64: launch_sub<64, KB, false, L2>(prm, total, smem, stream); return true;
+    default: return false;
+  }
+}
 }  // namespace
 
 bool launch_sub_small(int dp, int kb, bool l2, const SvtParams& prm, int total, size_t smem, cudaStream_t stream) {
-  // level 2 of d <= 128 always has kSubspaceKB columns; level 1 kSubspaceKB1 or kSubspaceKB
+  // d < 72: level 1 kSubspaceKBSmall, level 2 kSubspaceKB1 columns
+  if (dp < 72) {
+    if (l2) return kb == kSubspaceKB1 && dispatch_smalld<kSubspaceKB1, true>(dp, prm, total, smem, stream);
+    return kb == kSubspaceKBSmall && dispatch_smalld<kSubspaceKBSmall, false>(dp, prm, total, smem, stream);
+  }
+  // level 2 of 72 <= d <= 128 always has kSubspaceKB columns; level 1 kSubspaceKB1 or kSubspaceKB
   if (l2) return kb == kSubspaceKB && dispatch_small<kSubspaceKB, true>(dp, prm, total, smem, stream);
   if (kb == kSubspaceKB1) return dispatch_small<kSubspaceKB1, false>(dp, prm, total, smem, stream);
   return kb == kSubspaceKB && dispatch_small<kSubspaceKB, false>(dp, prm, total, smem, stream);

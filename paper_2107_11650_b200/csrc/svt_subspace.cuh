@@ -656,10 +656,14 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
   // HUGE (248 < d <= 496): 16-row chunks, a 32-column block for every level
   // (level 1, then the deflation chain), one-output-per-thread chunk GEMM
   constexpr bool HUGE = BIG && R == 16;
-  constexpr int KB1 = HUGE ? kSubspaceKBHuge : BIG ? kSubspaceKB : (L2 ? kSubspaceKB1 : KB);
-  constexpr int KB2 = HUGE ? kSubspaceKBHuge : BIG ? kSubspaceKBBig : kSubspaceKB;
-  static_assert(HUGE ? KB == kSubspaceKBHuge
-                : L2 ? KB == KB2 : (BIG ? KB == kSubspaceKB : (KB == kSubspaceKB1 || KB == kSubspaceKB)),
+  // SMALLD (40 <= d < 72): 16-column level 1, 32-column level 2
+  constexpr bool SMALLD = !BIG && DP < 72;
+  constexpr int KB1 = HUGE ? kSubspaceKBHuge : BIG ? kSubspaceKB : SMALLD ? kSubspaceKBSmall : (L2 ? kSubspaceKB1 : KB);
+  constexpr int KB2 = HUGE ? kSubspaceKBHuge : BIG ? kSubspaceKBBig : SMALLD ? kSubspaceKB1 : kSubspaceKB;
+  static_assert(HUGE     ? KB == kSubspaceKBHuge
+                : SMALLD ? KB == (L2 ? KB2 : KB1)
+                : L2     ? KB == KB2
+                         : (BIG ? KB == kSubspaceKB : (KB == kSubspaceKB1 || KB == kSubspaceKB)),
                 "block size of the level");
   constexpr bool NOSPLIT = BIG && L2 && !HUGE;
   static_assert(KB % 16 == 0 && KB % 8 == 0, "KB must be a multiple of 16");
