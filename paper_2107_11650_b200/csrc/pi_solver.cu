@@ -11,6 +11,8 @@
 // SPIRiT the operator adds lambda1 F2D P F2D^-1 with P = (G-I)^H (G-I) per
 // pixel (proj/src/spirit.cpp:151-165), applied as row iFFT -> fused column
 // (iFFT, J x J matvec, FFT) -> row FFT.
+#include <cooperative_groups.h>
+
 #include "pi_solver.cuh"
 #include "solver_util.cuh"
 
@@ -20,10 +22,12 @@
 #include <cstring>
 
 namespace shlr_b200 {
+namespace cg = cooperative_groups;
 
 namespace {
 
 using util::block_sum;
+using util::block_sum_all;
 using util::dalloc;
 using util::dalloc_s;
 using util::grid_for;
@@ -51,6 +55,14 @@ __device__ double sum_partials(const double* partials, int nblocks, int slot, do
 }
 
 __device__ __forceinline__ bool halted(const SolverCtl* c) { return c->stopped || c->error; }
+
+// This thread's strided share of sum(partials[0:n]) (fixed order per thread;
+// the caller's block reduction makes the total deterministic).
+__device__ __forceinline__ double sum_partials_raw(const double* partials, int n) {
+  double v = 0.0;
+  for (int b = threadIdx.x; b < n; b += blockDim.x) v += __ldcg(partials + b);
+  return v;
+}
 
 // ------------------------------------------------------------ setup kernels
 __global__ void k_init_data(const double* __restrict__ y, const uint8_t* __restrict__ mask,
@@ -420,17 +432,14 @@ __global__ void k_cg_init_from_ap(const float2* __restrict__ bk, const float2* _
 
 // SPIRiT column stage on [M][N*J], tile of F = PPT*J fibres (PPT pixels):
 // v = iF0(tmp); w = P v per pixel; tmp2 = F0(w).
-__global__ void __launch_bounds__(kFftThreads) k_spirit_cols(const float2* __restrict__ tmp,
-                                                     float2* __restrict__ tmp2,
-                                                     const float2* __restrict__ pm, FftTwiddles tw,
-                                                     int N, int J, int PPT, const SolverCtl* ctl,
-                                                     int for_x) {
-  extern __shared__ float2 sm[];
-  if (halted(ctl) || (!for_x && ctl->cg.done)) return;
+// Column stage of one tile of PPT pixel columns starting at n0 (smem `sm`:
+// 2 M PPT J float2): v = iF0(tmp); w = P v per pixel; tmp2 = F0(w).
+__device__ void spirit_col_tile(const float2* __restrict__ tmp, float2* __restrict__ tmp2,
+                                const float2* __restrict__ pm, const FftTwiddles& tw, int N, int J, int PPT,
+                                int n0, float2* sm) {
   const int M = tw.n;
   const int F = PPT * J;
   const long long NJ = (long long)N * J;
-  const int n0 = blockIdx.x * PPT;  // first pixel column of the tile
   float2* a = sm;
   float2* b = sm + (size_t)M * F;
   const int lf = fib_log2(F), lj = fib_log2(J);
@@ -504,22 +513,24 @@ __global__ void __launch_bounds__(kFftThreads) k_spirit_cols(const float2* __res
   }
 }
 
-// SPIRiT row forward stage, one CTA per row m: v = F1(tmp2 row);
-// ap = dg p + lambda1 v.  mode 0: CG iteration (reduce denom, finalize alpha);
-// mode 1: initial residual (apply to x, store ap only).
-__global__ void __launch_bounds__(kFftThreads) k_spirit_rows_fwd(const float2* __restrict__ tmp2,
-                                                         const float2* __restrict__ vec,
-                                                         const float* __restrict__ dg,
-                                                         float2* __restrict__ ap, FftTwiddles tw,
-                                                         int J, float lambda1, SolverCtl* ctl,
-                                                         double* partials, int mode) {
+__global__ void __launch_bounds__(kFftThreads) k_spirit_cols(const float2* __restrict__ tmp,
+                                                     float2* __restrict__ tmp2,
+                                                     const float2* __restrict__ pm, FftTwiddles tw,
+                                                     int N, int J, int PPT, const SolverCtl* ctl,
+                                                     int for_x) {
   extern __shared__ float2 sm[];
-  __shared__ double sh[32];
-  if (halted(ctl) || (mode == 0 && ctl->cg.done)) return;
+  if (halted(ctl) || (!for_x && ctl->cg.done)) return;
+  spirit_col_tile(tmp, tmp2, pm, tw, N, J, PPT, blockIdx.x * PPT, sm);
+}
+
+// Row forward stage of row m (smem `sm`: 2 N J float2): v = F1(tmp2 row);
+// ap = dg p + lambda1 v.  Returns this thread's share of Re<p, ap>.
+__device__ double spirit_row_fwd(const float2* __restrict__ tmp2, const float2* __restrict__ vec,
+                                 const float* __restrict__ dg, float2* __restrict__ ap, const FftTwiddles& tw,
+                                 int J, float lambda1, int m, float2* sm) {
   const int N = tw.n;
   const int F = J;
   const long long NJ = (long long)N * J;
-  const int m = blockIdx.x;
   float2* a = sm;
   float2* b = sm + (size_t)N * F;
 #pragma unroll 4
@@ -557,6 +568,22 @@ __global__ void __launch_bounds__(kFftThreads) k_spirit_rows_fwd(const float2* _
     ap[idx] = av;
     s += (double)pv.x * av.x + (double)pv.y * av.y;
   }
+  return s;
+}
+
+// SPIRiT row forward stage, one CTA per row m: v = F1(tmp2 row);
+// ap = dg p + lambda1 v.  mode 0: CG iteration (reduce denom, finalize alpha);
+// mode 1: initial residual (apply to x, store ap only).
+__global__ void __launch_bounds__(kFftThreads) k_spirit_rows_fwd(const float2* __restrict__ tmp2,
+                                                         const float2* __restrict__ vec,
+                                                         const float* __restrict__ dg,
+                                                         float2* __restrict__ ap, FftTwiddles tw,
+                                                         int J, float lambda1, SolverCtl* ctl,
+                                                         double* partials, int mode) {
+  extern __shared__ float2 sm[];
+  __shared__ double sh[32];
+  if (halted(ctl) || (mode == 0 && ctl->cg.done)) return;
+  const double s = spirit_row_fwd(tmp2, vec, dg, ap, tw, J, lambda1, blockIdx.x, sm);
   if (mode != 0) return;
   double v = block_sum(s, sh);
   if (!publish_and_check_last(partials, gridDim.x, &v, 1, &ctl->arrive[1])) return;
@@ -564,6 +591,142 @@ __global__ void __launch_bounds__(kFftThreads) k_spirit_rows_fwd(const float2* _
   if (threadIdx.x == 0) {
     finalize_alpha(ctl, denom);
     ctl->arrive[1] = 0;
+  }
+}
+
+// ---------------------------------------------------------------- persistent SPIRiT CG
+// The whole SPIRiT CG loop of one outer iteration (cg_solve, solvers.cpp:37-66,
+// after k_cg_init_from_ap) in one cooperative launch.  Rows m = blockIdx.x +
+// k gridDim.x belong to one CTA for the whole loop; per CG iteration:
+//   P1 rows:    p = r + gamma p (p = r first), row iFFT -> tmp
+//   P2 columns: column iFFT, per-pixel P, column FFT -> tmp2
+//   P3 rows:    row FFT, ap = dg p + lambda1 v, partial Re<p, ap>
+//   (grid)      denom -> alpha (every CTA sums the partials in the same order)
+//   P4 rows:    x += alpha p, r -= alpha ap, partial <r, r>
+//   (grid)      rho' -> rel, gamma, stop (finalize_rho's rule)
+// with a grid barrier after each phase.  Every CTA evaluates the scalar
+// recurrences identically, so the stop decision is uniform; CTA 0 mirrors
+// them into ctl->cg for the log and the following kernels.
+__device__ void spirit_row_inv(const float2* __restrict__ r, float2* __restrict__ p, float2* __restrict__ tmp,
+                               const FftTwiddles& tw, int J, int m, bool first, float gamma, float2* sm) {
+  const int N = tw.n;
+  const long long NJ = (long long)N * J;
+  float2* a = sm;
+  float2* b = sm + (size_t)N * J;
+#pragma unroll 4
+  for (int t = threadIdx.x; t < N * J; t += blockDim.x) {
+    const long long idx = m * NJ + t;
+    float2 v = r[idx];
+    if (!first) {
+      const float2 pv = p[idx];
+      v = make_float2(fmaf(gamma, pv.x, v.x), fmaf(gamma, pv.y, v.y));
+    }
+    p[idx] = v;
+    a[t] = v;
+  }
+  __syncthreads();
+  float2* res = smem_centered_dft<true>(a, b, tw, J);
+  const float isn = rsqrtf((float)N);
+  const int lf = fib_log2(J);
+  for (int t = threadIdx.x; t < N * J; t += blockDim.x) {
+    int f, k;
+    tile_idx(t, J, lf, f, k);
+    tmp[m * NJ + t] = cscale(res[t], centered_out_scale(k, N, tw.logn, isn));
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kFftThreads, 2) k_spirit_cg_loop(float2* __restrict__ x, float2* __restrict__ r,
+                                                            float2* __restrict__ p, float2* __restrict__ ap,
+                                                            float2* __restrict__ tmp, float2* __restrict__ tmp2,
+                                                            const float2* __restrict__ pm,
+                                                            const float* __restrict__ dg, FftTwiddles twM,
+                                                            FftTwiddles twN, int J, float lambda1,
+                                                            SolverCtl* ctl, double* partials, int cg_max,
+                                                            double cg_tol) {
+  extern __shared__ float2 sm[];
+  __shared__ double sh[33];
+  cg::grid_group grid = cg::this_grid();
+  if (halted(ctl) || ctl->cg.done) return;  // uniform: set before the launch
+  const int M = twM.n, N = twN.n, G = gridDim.x;
+  const long long NJ = (long long)N * J;
+  CgState c = ctl->cg;  // every CTA's private copy of the recurrences
+  const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+  while (true) {
+    // P1
+    for (int m = blockIdx.x; m < M; m += G) spirit_row_inv(r, p, tmp, twN, J, m, c.it == 0, (float)c.gamma, sm);
+    grid.sync();
+    // P2
+    for (int n = blockIdx.x; n < N; n += G) {
+      spirit_col_tile(tmp, tmp2, pm, twM, N, J, 1, n, sm);
+      __syncthreads();
+    }
+    grid.sync();
+    // P3
+    double sd = 0.0;
+    for (int m = blockIdx.x; m < M; m += G) {
+      sd += spirit_row_fwd(tmp2, p, dg, ap, twN, J, lambda1, m, sm);
+      __syncthreads();
+    }
+    sd = block_sum(sd, sh);
+    if (threadIdx.x == 0) partials[blockIdx.x] = sd;
+    grid.sync();
+    const double denom = block_sum_all(sum_partials_raw(partials, G), sh);
+    if (!isfinite(denom) || denom <= 0.0) {  // solvers.cpp:44-45
+      if (lead) {
+        ctl->error = 2;
+        c.done = 1;
+        c.denom = denom;
+        ctl->cg = c;
+      }
+      return;
+    }
+    c.denom = denom;
+    c.alpha = c.rho / denom;
+    const float a = (float)c.alpha;
+    // P4
+    double sr = 0.0;
+    for (int m = blockIdx.x; m < M; m += G) {
+      for (int t = threadIdx.x; t < N * J; t += blockDim.x) {
+        const long long idx = m * NJ + t;
+        const float2 pv = p[idx], av = ap[idx];
+        float2 xv = x[idx], rv = r[idx];
+        xv = make_float2(fmaf(a, pv.x, xv.x), fmaf(a, pv.y, xv.y));
+        rv = make_float2(fmaf(-a, av.x, rv.x), fmaf(-a, av.y, rv.y));
+        x[idx] = xv;
+        r[idx] = rv;
+        sr += (double)rv.x * rv.x + (double)rv.y * rv.y;
+      }
+    }
+    sr = block_sum(sr, sh);
+    if (threadIdx.x == 0) partials[G + blockIdx.x] = sr;
+    grid.sync();
+    const double rho_next = block_sum_all(sum_partials_raw(partials + G, G), sh);
+    // finalize_rho (solvers.cpp:47-57)
+    bool stop = false;
+    if (!isfinite(rho_next)) {
+      if (lead) ctl->error = 1;
+      c.done = 1;
+      stop = true;
+    } else {
+      c.rel = sqrt(rho_next) / c.bnorm;
+      c.it += 1;
+      if (c.rel <= cg_tol) {
+        c.done = 1;
+        stop = true;
+      } else {
+        c.gamma = rho_next / c.rho;
+        c.rho = rho_next;
+        if (c.it >= cg_max) {
+          c.done = 1;
+          stop = true;
+        }
+      }
+    }
+    if (stop) {
+      if (lead) ctl->cg = c;
+      return;
+    }
   }
 }
 
@@ -691,7 +854,23 @@ PiPlan::PiPlan(const PiConfig& cfg, const double* y, const uint8_t* mask, size_t
   hcol0_ = dalloc_s<float2>(M, stream_);
   wcN_ = dalloc_s<float2>(N, stream_);
   wcM_ = dalloc_s<float2>(M, stream_);
-  partials_ = dalloc_s<double>(4 * (size_t)std::max(red_blocks_, M), stream_);
+  partials_ = dalloc_s<double>(4 * (size_t)std::max(red_blocks_, std::max(M, N)), stream_);
+  // persistent SPIRiT CG loop (k_spirit_cg_loop): one CTA per row / column
+  // pair, capped by what the cooperative launch can keep resident.  Opt-in
+  // (SHLR_PERSIST_CG=1): measured 2.443 ms per config-2 step against 2.388
+  // with the per-stage kernels in the CUDA graph -- 60 grid barriers per
+  // outer iteration cost more than 64 graph kernel boundaries.
+  if (cfg.spirit && std::getenv("SHLR_PERSIST_CG")) {
+    int dev = 0, sms = 0, per_sm = 0, coop = 0;
+    SHLR_CUDA(cudaGetDevice(&dev));
+    SHLR_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    SHLR_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+    cg_smem_ = 2 * (size_t)std::max(M, N) * cfg.J * sizeof(float2);
+    if (cg_smem_ > 48 * 1024)
+      SHLR_CUDA(cudaFuncSetAttribute(k_spirit_cg_loop, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cg_smem_));
+    SHLR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spirit_cg_loop, kFftThreads, cg_smem_));
+    if (coop && per_sm > 0) cg_grid_ = std::min(std::max(M, N), per_sm * sms);
+  }
   ctl_ = dalloc_s<SolverCtl>(1, stream_);
   log_ = dalloc_s<double>(3 * (size_t)std::max(cfg.max_outer, 1), stream_);
   const int er = std::max(cfg.Pr, B_ * qr_), dr = std::min(cfg.Pr, B_ * qr_);
@@ -877,11 +1056,25 @@ void PiPlan::enqueue_iteration(int k, bool record_events) {
                                                    cfg_.cg_tol);
     k_cg_zero_x<<<g, kThreads, 0, stream_>>>(x_, nel_, ctl_);
     launch_count_ += 2;
-    for (int it = 0; it < cfg_.cg_max; ++it) {
-      cg_apply_spirit(p_, ap_, false);
-      k_cg_b<<<g, kThreads, 0, stream_>>>(x_, r_, p_, ap_, dg_, nel_, J, ctl_, partials_, cfg_.cg_max,
-                                         cfg_.cg_tol);
+    if (cg_grid_ > 0) {
+      // the whole CG loop in one cooperative launch (grid barriers between phases)
+      const int Jv = J;
+      float l1 = (float)cfg_.lambda1;
+      int cgm = cfg_.cg_max;
+      double cgt = cfg_.cg_tol;
+      FftTwiddles twm = tM_, twn = tN_;
+      void* args[] = {&x_, &r_, &p_, &ap_, &tmp_, &tmp2_, &pmat_, &dg_, &twm, &twn,
+                      (void*)&Jv, &l1, &ctl_, &partials_, &cgm, &cgt};
+      SHLR_CUDA(cudaLaunchCooperativeKernel((const void*)k_spirit_cg_loop, dim3(cg_grid_), dim3(kFftThreads), args,
+                                            cg_smem_, stream_));
       launch_count_ += 1;
+    } else {
+      for (int it = 0; it < cfg_.cg_max; ++it) {
+        cg_apply_spirit(p_, ap_, false);
+        k_cg_b<<<g, kThreads, 0, stream_>>>(x_, r_, p_, ap_, dg_, nel_, J, ctl_, partials_, cfg_.cg_max,
+                                           cfg_.cg_tol);
+        launch_count_ += 1;
+      }
     }
   }
   SHLR_LAUNCH_CHECK();

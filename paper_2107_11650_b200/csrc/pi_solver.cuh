@@ -86,7 +86,9 @@ class PiPlan {
   float2 *vs2row_ = nullptr, *vs2col_ = nullptr;  // large-d level-2 block stores
   float2 *z1row_ = nullptr, *z1col_ = nullptr;    // large-d level-2 Z1 (level-3 deflation)
   float2 *vdrow_ = nullptr, *vdcol_ = nullptr;    // large-d deflation chain bases
-  int* ndefl_ = nullptr;                          // deflated columns per matrix (rows, then columns)
+  int* ndefl_ = nullptr;
+  int cg_grid_ = 0;         // persistent SPIRiT CG loop: cooperative grid (0: per-stage kernels)
+  size_t cg_smem_ = 0;                          // deflated columns per matrix (rows, then columns)
   int* fallback_ = nullptr;                     // per-matrix subspace -> full fallback flags
   int q_cold_ = 6, q_warm_ = 1;
   int kb1_ = kSubspaceKB;  // level-1 block of the subspace SVT (d <= 128); SHLR_KB1 overrides
