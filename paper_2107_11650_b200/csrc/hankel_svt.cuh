@@ -192,6 +192,11 @@ constexpr int kSmallSvtMaxP = 8;
 constexpr int kSmallSvtMaxLJ = 64;
 bool small_svt_applicable(const SvtParams& prm);
 bool launch_small_svt(const SvtParams& prm, cudaStream_t stream);
+// One-warp-per-matrix Hankel-SVT for plain lifts with d <= 32 (tiny_svt.cu):
+// the config-5 single-coil points.  Plain mode, one family, J * len <= 1024,
+// no singular-value output.
+bool tiny_svt_applicable(const SvtParams& prm);
+bool launch_tiny_svt(const SvtParams& prm, cudaStream_t stream);
 
 // Hankel lift index map of a p x (blocks q) weighted lift as the kernels
 // build it (operators.cpp:36-56, hankel.cpp:31-41,99-113): the lift stage of

@@ -1310,6 +1310,11 @@ void hankel_svt_batched_device(const float2* vecs, int batch, int nc, int n, int
   F.o_mat = F.s_mat;
   F.o_n = 1;
   F.o_j = n;
+  // d <= 32: one warp per matrix (tiny_svt.cu) -- opt-in (SHLR_TINY_SVT=1):
+  // measured 2.4x slower than the CTA-per-matrix full solver at 242x15 (0.66
+  // vs 0.28 ms per 512): with ~3.5 single-coil matrices per SM a warp per
+  // matrix leaves the SM latency-bound on the serial Gram and Jacobi chains
+  if (!sv && std::getenv("SHLR_TINY_SVT") && !sweeps_out && launch_tiny_svt(sp, stream)) return;
   // cold solves need a V1 spill area: process the batch in chunks so the
   // stream-ordered scratch stays <= 256 MB
   const int dp = svt_padded_dim(F.d);
