@@ -13,15 +13,15 @@ cap() {  # name kernel-regex skip command...
   ncu -i /tmp/$name.ncu-rep --page source --csv --print-source cuda,sass > /tmp/$name.src.csv 2>/dev/null
   python scripts/ncu_hot.py /tmp/$name.src.csv 40 > gpurun_out/$name.hot.txt 2>/dev/null
 }
-python scripts/param_probe.py > gpurun_out/p4.log 2>&1 && \
+python scripts/probes/param_probe.py > gpurun_out/p4.log 2>&1 && \
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv \
-    --log-file gpurun_out/param_launches.csv python scripts/param_probe.py > /dev/null 2>&1
+    --log-file gpurun_out/param_launches.csv python scripts/probes/param_probe.py > /dev/null 2>&1
 echo "param launches rc=$?"
-cap prof_param_pe svt_subspace 3 python scripts/param_probe.py
-cap prof_param_echo small_svt 3 python scripts/param_probe.py
-python scripts/c3_probe.py > gpurun_out/c3.log 2>&1 && \
+cap prof_param_pe svt_subspace 3 python scripts/probes/param_probe.py
+cap prof_param_echo small_svt 3 python scripts/probes/param_probe.py
+python scripts/probes/c3_probe.py > gpurun_out/c3.log 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
-    --log-file gpurun_out/c3_launches.csv python scripts/c3_probe.py > /dev/null 2>&1
+    --log-file gpurun_out/c3_launches.csv python scripts/probes/c3_probe.py > /dev/null 2>&1
 echo "c3 launches rc=$?"
-cap prof_c3 svt_subspace 12 python scripts/c3_probe.py
+cap prof_c3 svt_subspace 12 python scripts/probes/c3_probe.py
 du -sh gpurun_out

@@ -8,7 +8,7 @@ import os
 import subprocess
 import sys
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 rnd = sys.argv[1] if len(sys.argv) > 1 else "01"
 out = os.path.join(ROOT, "gpurun_out")
 

@@ -5,7 +5,7 @@ import os
 import subprocess
 import sys
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 rnd = sys.argv[1] if len(sys.argv) > 1 else "01"
 P = os.path.join(ROOT, "profiles")
 b = json.load(open(os.path.join(P, f"r{rnd}_bench.json")))
