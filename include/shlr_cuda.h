@@ -197,6 +197,14 @@ int shlr_cuda_hankel_svt_batched(const void* vecs, int batch, int nc, int n, int
 int shlr_cuda_hankel_svt_batched_host(const double* vecs, int batch, int nc, int n, int p,
                                       double tau, double* out, double* sv_out);
 
+/* Test hook: the X-update operator of shlr_pi_reconstruct alone, out = A x
+ * with A the reference's normal_apply (proj/src/operators.cpp:213-248) for
+ * the configuration in args (mask, taps, pencils, virtual coils, lambda,
+ * lambda1, beta, SPIRiT kernels), evaluated by the device's k-space operator
+ * (exact diagonal + F2D P F2D^-1).  x_img and out_img: m x n x j interleaved
+ * complex, image domain. */
+int shlr_cuda_debug_normal_apply(const shlr_pi_args* args, const double* x_img, double* out_img);
+
 /* Diagnostics: the device-pointer batched SVT that also writes, per matrix,
  * the number of Jacobi sweeps the eigen-solver used (sweeps_dev: device int
  * array of batch entries). */

@@ -69,6 +69,8 @@ PROTOTYPES = {
     "shlr_cuda_pi_reconstruct": (C.c_int, [C.POINTER(ShlrPiArgs), C.POINTER(C.c_double),
                                            C.POINTER(C.c_double), C.POINTER(ShlrStats),
                                            LOG_FN, C.c_void_p]),
+    "shlr_cuda_debug_normal_apply": (C.c_int, [C.POINTER(ShlrPiArgs), C.POINTER(C.c_double),
+                                               C.POINTER(C.c_double)]),
     "shlr_cuda_pi_plan_create": (C.c_int, [C.POINTER(ShlrPiArgs), C.POINTER(C.c_void_p)]),
     "shlr_cuda_pi_plan_reset": (C.c_int, [C.c_void_p]),
     "shlr_cuda_pi_plan_run": (C.c_int, [C.c_void_p, C.c_size_t]),

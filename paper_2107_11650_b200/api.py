@@ -242,6 +242,20 @@ def shlr_pi_reconstruct(y: np.ndarray, mask: SamplingMask, g: Optional[SpiritKer
     return x
 
 
+def debug_normal_apply(y: np.ndarray, mask: SamplingMask, g: Optional[SpiritKernels], hcfg: HankelConfig,
+                       acfg: AdmmConfig, x: np.ndarray) -> np.ndarray:
+    """Test hook: A x for the X-update operator of shlr_pi_reconstruct
+    (normal_apply, operators.cpp:213-248) as the device evaluates it."""
+    keep: list = []
+    a = _pi_args(y, mask, g, hcfg, acfg, 0, keep)
+    xc = _c128(x)
+    if xc.shape != np.shape(y):
+        raise ValueError("debug_normal_apply: x must have the shape of y")
+    out = np.empty_like(xc)
+    _check(lib.shlr_cuda_debug_normal_apply(C.byref(a), _dptr(xc), _dptr(out)), "normal_apply")
+    return out
+
+
 class PiPlan:
     """Resident plan (``shlr_cuda_pi_plan_*``): inputs uploaded once, the
     ADMM iterations run on-device, results downloaded on demand."""

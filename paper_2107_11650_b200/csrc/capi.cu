@@ -181,6 +181,19 @@ int shlr_cuda_pi_plan_create(const shlr_pi_args* args, shlr_pi_plan** out) {
   });
 }
 
+int shlr_cuda_debug_normal_apply(const shlr_pi_args* args, const double* x_img, double* out_img) {
+  return guarded([&] {
+    validate_pi(args);
+    if (!x_img || !out_img) throw shlr_b200::InvalidArg("normal_apply: null buffer");
+    require_device();
+    auto cfg = config_of(args);
+    shlr_b200::PiPlan plan(cfg, args->y, args->mask, args->mask_rows, args->taps, args->ntaps,
+                           cfg.spirit ? args->spirit_weights : nullptr, args->spirit_k);
+    plan.debug_normal_apply(x_img, out_img);
+    return SHLR_OK;
+  });
+}
+
 int shlr_cuda_pi_plan_reset(shlr_pi_plan* plan) {
   return guarded([&] {
     if (!plan) throw shlr_b200::InvalidArg("null plan");

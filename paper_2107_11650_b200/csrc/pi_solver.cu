@@ -773,6 +773,15 @@ __global__ void k_to_double(const float2* __restrict__ src, double* __restrict__
   }
 }
 
+// ap = dg (.) x on the k-space pixel grid (element (m, k, coil) -> pixel (m, k))
+__global__ void k_apply_diag(const float2* __restrict__ x, const float* __restrict__ dg, float2* __restrict__ ap,
+                             size_t n, int J) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const float d = dg[i / J];
+    ap[i] = make_float2(d * x[i].x, d * x[i].y);
+  }
+}
+
 __global__ void k_from_double(const double* __restrict__ src, float2* __restrict__ dst, size_t n) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
     dst[i] = make_float2((float)src[2 * i], (float)src[2 * i + 1]);
@@ -1269,6 +1278,44 @@ void PiPlan::download(double* x_out, size_t* outer_iters, double* final_rel,
       log_lines->push_back(buf);
     }
   }
+}
+
+// The X-update operator of the plan in the image domain, out = A x
+// (normal_apply, operators.cpp:213-248): x -> F2D -> the CG's own k-space
+// operator (diagonal dg, plus the SPIRiT stages F2D P F2D^-1 when enabled) ->
+// F2D^-1.  A test hook for the operator alone; uses the plan's work buffers,
+// so call it on a plan that is not mid-run.
+void PiPlan::debug_normal_apply(const double* x_img, double* out_img) {
+  const int M = cfg_.M, N = cfg_.N, J = cfg_.J;
+  const long long NJ = (long long)N * J;
+  double* xd = dalloc_s<double>(2 * nel_, stream_);
+  // (ap_ and tmp2_ exist only with SPIRiT: scratch of its own otherwise)
+  float2* t2 = tmp2_ ? tmp2_ : dalloc_s<float2>(nel_, stream_);
+  float2* ap = ap_ ? ap_ : dalloc_s<float2>(nel_, stream_);
+  SHLR_CUDA(cudaMemcpyAsync(xd, x_img, 2 * nel_ * sizeof(double), cudaMemcpyHostToDevice, stream_));
+  k_from_double<<<grid_for(nel_), kThreads, 0, stream_>>>(xd, tmp_, nel_);
+  SHLR_LAUNCH_CHECK();
+  StridedCopyOp f0{tmp_, t2, 0, NJ, 1};
+  launch_fft_axis<StridedCopyOp, false>(f0, tM_, 1, N * J, 16, stream_);
+  StridedCopyOp f1{t2, x_, NJ, J, 1};
+  launch_fft_axis<StridedCopyOp, false>(f1, tN_, M, J, J, stream_);
+  if (cfg_.spirit) {
+    cg_apply_spirit(x_, ap_, true);
+  } else {
+    k_apply_diag<<<grid_for(nel_), kThreads, 0, stream_>>>(x_, dg_, ap, nel_, J);
+    SHLR_LAUNCH_CHECK();
+  }
+  StridedCopyOp i1{ap, tmp_, NJ, J, 1};
+  launch_fft_axis<StridedCopyOp, true>(i1, tN_, M, J, J, stream_);
+  StridedCopyOp i0{tmp_, t2, 0, NJ, 1};
+  launch_fft_axis<StridedCopyOp, true>(i0, tM_, 1, N * J, 16, stream_);
+  k_to_double<<<grid_for(nel_), kThreads, 0, stream_>>>(t2, xd, nel_);
+  SHLR_LAUNCH_CHECK();
+  SHLR_CUDA(cudaMemcpyAsync(out_img, xd, 2 * nel_ * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+  SHLR_CUDA(cudaFreeAsync(xd, stream_));
+  if (t2 != tmp2_) SHLR_CUDA(cudaFreeAsync(t2, stream_));
+  if (ap != ap_) SHLR_CUDA(cudaFreeAsync(ap, stream_));
+  SHLR_CUDA(cudaStreamSynchronize(stream_));
 }
 
 void PiPlan::download_sv(double* sv_out) {

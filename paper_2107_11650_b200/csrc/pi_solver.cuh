@@ -49,6 +49,8 @@ class PiPlan {
   void download(double* x_out, size_t* outer_iters, double* final_rel,
                 std::vector<std::string>* log_lines, int* error);
   void download_sv(double* sv_out);   // debug hook (debug_sv_iter)
+  // test hook: out = A x in the image domain with the plan's X-update operator
+  void debug_normal_apply(const double* x_img, double* out_img);
   double svt_ms() const { return svt_ms_; }
   double total_ms() const { return total_ms_; }
   int launches_per_iter() const { return launches_per_iter_; }
