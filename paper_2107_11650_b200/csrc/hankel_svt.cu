@@ -371,6 +371,18 @@ bool launch_level(const SvtParams& prm, int total, cudaStream_t stream) {
     if (smem > 227 * 1024) return false;
     return launch_sub_huge(dph, L2, prm, total, smem, stream);
   }
+  // 112 < d <= 120 with a 48-column level 1 (the headline, config 2: 242 x
+  // 120): the large-d layout (spectra and duals read from L2, the adjoint
+  // read-modify-written in place, no split staging: 111 KB of shared memory)
+  // lets two CTAs share an SM, so one matrix's latency-bound QR and
+  // Rayleigh-Ritz phases overlap the other's chunk GEMMs (1.74 -> 1.66 ms
+  // per config-2 launch, same arithmetic).  Level 2 and the full solver
+  // behind it are unchanged.
+  static const bool coloc = std::getenv("SHLR_NO_COLOC") == nullptr;
+  if (coloc && !L2 && KB1 == kSubspaceKB && svt_padded_dim(g.dmax) == 120 && g.dmin >= 72 && g.maxLen <= 0xffff) {
+    const size_t smem = svt_subspace_smem_bytes(120, kSubspaceKB, 32, g.maxB, g.maxLen, g.maxE, true);
+    if (2 * (smem + 1024) <= 228 * 1024) return launch_sub_big(120, false, prm, total, smem, stream);
+  }
   if (g.dmax > 128) {
     // large-d variant (spectra and adjoint not resident)
     // (tall lifts accumulate the adjoint in the zeroed output, weighted and

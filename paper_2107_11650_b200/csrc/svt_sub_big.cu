@@ -10,6 +10,12 @@ template <bool L2>
 bool dispatch_big(int dp, const SvtParams& prm, int total, size_t smem, cudaStream_t stream) {
   constexpr int KB = L2 ? kSubspaceKBBig : kSubspaceKB;
   switch (dp) {
+    case 120:  // 112 < d <= 120 level 1, two CTAs per SM (hankel_svt.cu launch_level)
+      if constexpr (!L2) {
+        launch_sub<120, KB, true, L2, 2>(prm, total, smem, stream);
+        return true;
+      }
+      return false;
     case 160: launch_sub<160, KB, true, L2>(prm, total, smem, stream); return true;
     case 192: launch_sub<192, KB, true, L2>(prm, total, smem, stream); return true;
     case 248: launch_sub<248, KB, true, L2>(prm, total, smem, stream); return true;

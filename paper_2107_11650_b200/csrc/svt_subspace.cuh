@@ -164,19 +164,18 @@ __device__ void householder_qr(float2* M, float2* Q, int d, float* tau) {
   for (int j = 0; j < KB; ++j) {
     if (warp_act && CPW * w + CPW - 1 > j) {  // warp-uniform: some column k > j in this warp
       float2 part = make_float2(0.f, 0.f);
-      float2 v[T];
 #pragma unroll
-      for (int t = 0; t < T; ++t) {
-        v[t] = M[(s + GS * t) * KS + j];
-        cfmac(part, v[t], col[t]);  // sum conj(v) col
-      }
+      for (int t = 0; t < T; ++t) cfmac(part, M[(s + GS * t) * KS + j], col[t]);  // sum conj(v) col
       part.x = group_sum<GS>(part.x);
       part.y = group_sum<GS>(part.y);
       const float2 tw = (act && k > j) ? cscale(part, tau[j]) : make_float2(0.f, 0.f);
+      // the reflector is read again rather than kept: half the registers
+      // (two CTAs per SM at 64 registers need it)
 #pragma unroll
       for (int t = 0; t < T; ++t) {
-        col[t].x -= v[t].x * tw.x - v[t].y * tw.y;
-        col[t].y -= v[t].x * tw.y + v[t].y * tw.x;
+        const float2 v = M[(s + GS * t) * KS + j];
+        col[t].x -= v.x * tw.x - v.y * tw.y;
+        col[t].y -= v.x * tw.y + v.y * tw.x;
       }
       if (j + 1 < KB && w == (j + 1) / CPW) reflect(j + 1);
     }
@@ -189,19 +188,16 @@ __device__ void householder_qr(float2* M, float2* Q, int d, float* tau) {
   if (warp_act) {
     for (int j = min(CPW * w + CPW - 1, KB - 1); j >= 0; --j) {
       float2 part = make_float2(0.f, 0.f);
-      float2 v[T];
 #pragma unroll
-      for (int t = 0; t < T; ++t) {
-        v[t] = M[(s + GS * t) * KS + j];
-        cfmac(part, v[t], col[t]);
-      }
+      for (int t = 0; t < T; ++t) cfmac(part, M[(s + GS * t) * KS + j], col[t]);
       part.x = group_sum<GS>(part.x);
       part.y = group_sum<GS>(part.y);
       const float2 tw = (act && k >= j) ? cscale(part, tau[j]) : make_float2(0.f, 0.f);
 #pragma unroll
       for (int t = 0; t < T; ++t) {
-        col[t].x -= v[t].x * tw.x - v[t].y * tw.y;
-        col[t].y -= v[t].x * tw.y + v[t].y * tw.x;
+        const float2 v = M[(s + GS * t) * KS + j];
+        col[t].x -= v.x * tw.x - v.y * tw.y;
+        col[t].y -= v.x * tw.y + v.y * tw.x;
       }
     }
   }
@@ -640,8 +636,8 @@ __device__ void project_out(float2* M, const float2* __restrict__ V1, int ld, in
   __syncthreads();
 }
 
-template <int DP, int KB, int R, bool BIG, bool L2>
-__global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams prm) {
+template <int DP, int KB, int R, bool BIG, bool L2, int MINB = 1>
+__global__ void __launch_bounds__(kSubNT, MINB) svt_subspace_kernel(const SvtParams prm) {
   constexpr int NT = kSubNT;
   constexpr int KS = KB + 1;       // row stride of the d x KB blocks (conflict-free column walks)
   constexpr int CS = DP + 1;       // row stride of the R x d chunk (odd: conflict-free anti-diagonal walks)
@@ -1299,15 +1295,15 @@ __global__ void __launch_bounds__(kSubNT, 1) svt_subspace_kernel(const SvtParams
 
 
 namespace {
-template <int DP, int KB, bool BIG, bool L2>
+template <int DP, int KB, bool BIG, bool L2, int MINB = 1>
 void launch_sub(const SvtParams& prm, int total, size_t smem, cudaStream_t stream) {
   static bool configured = false;
   if (!configured) {
-    SHLR_CUDA(cudaFuncSetAttribute(svt_subspace_kernel<DP, KB, 32, BIG, L2>,
+    SHLR_CUDA(cudaFuncSetAttribute(svt_subspace_kernel<DP, KB, 32, BIG, L2, MINB>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     configured = true;
   }
-  svt_subspace_kernel<DP, KB, 32, BIG, L2><<<total, kSubNT, smem, stream>>>(prm);
+  svt_subspace_kernel<DP, KB, 32, BIG, L2, MINB><<<total, kSubNT, smem, stream>>>(prm);
   SHLR_LAUNCH_CHECK();
 }
 }  // namespace
