@@ -379,9 +379,24 @@ bool launch_level(const SvtParams& prm, int total, cudaStream_t stream) {
   // per config-2 launch, same arithmetic).  Level 2 and the full solver
   // behind it are unchanged.
   static const bool coloc = std::getenv("SHLR_NO_COLOC") == nullptr;
+  // The chunk contractions run as 3xTF32 on the tensor cores (svt_mma.cuh)
+  // and warm passes orthonormalise by a tensor-core Cholesky QR; SHLR_MMA=0 /
+  // SHLR_NS=0 keep the FP32 CUDA-core contractions / the Householder QR
+  // (config 2, per launch: 1.66 ms FP32 -> 1.40 ms)
+  static const bool mma = !std::getenv("SHLR_MMA") || std::atoi(std::getenv("SHLR_MMA")) != 0;
+  static const int ns = std::getenv("SHLR_NS") ? std::atoi(std::getenv("SHLR_NS")) : 1;
+  SvtParams pm = prm;
+  pm.ns_orth = ns;
   if (coloc && !L2 && KB1 == kSubspaceKB && svt_padded_dim(g.dmax) == 120 && g.dmin >= 72 && g.maxLen <= 0xffff) {
     const size_t smem = svt_subspace_smem_bytes(120, kSubspaceKB, 32, g.maxB, g.maxLen, g.maxE, true);
-    if (2 * (smem + 1024) <= 228 * 1024) return launch_sub_big(120, false, prm, total, smem, stream);
+    if (2 * (smem + 1024) <= 228 * 1024)
+      return mma ? launch_sub_mma(120, true, pm, total, smem, stream)
+                 : launch_sub_big(120, false, prm, total, smem, stream);
+  }
+  if (mma && !L2 && KB1 == kSubspaceKB && g.dmax <= 128) {
+    const int dp = svt_padded_dim(g.dmax);
+    const size_t smem = svt_subspace_smem_bytes(dp, kSubspaceKB, 32, g.maxB, g.maxLen, g.maxE, false);
+    if (smem <= 227 * 1024 && launch_sub_mma(dp, false, pm, total, smem, stream)) return true;
   }
   if (g.dmax > 128) {
     // large-d variant (spectra and adjoint not resident)

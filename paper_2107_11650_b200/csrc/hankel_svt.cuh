@@ -91,6 +91,10 @@ struct SvtParams {
                                  // iteration (device); while it is large the warm start is
                                  // far from the new subspace and warm solves take more passes
   float relc_q2, relc_q3;        // relc above these: at least 2 / 3 warm passes (with QR)
+  int ns_orth;         // tensor-core variants: warm passes orthonormalise by Newton-Schulz
+                       // (svt_mma.cuh) instead of the Householder QR
+  float2* ycache;      // optional scratch, total_matrices x max e x kSubspaceKB: the tensor-core
+                       // variants keep Ahat V of the Rayleigh-Ritz pass for the Z pass
   int wl_global;       // set by launch_hankel_svt: the lift source is read straight from
                        // fam[f].spec (plain mode, contiguous coils) instead of an smem copy
 };

@@ -227,24 +227,43 @@ __device__ __forceinline__ float2 lift_global(const SvtFamily& F, const float2* 
   return cconj(v);
 }
 
+// L2 prefetch of `count` contiguous complex64 (the dual rows of a coming
+// chunk): the large-d layout reads its duals straight from HBM, one
+// dependent load per element; with the lines already in L2 the chunk build
+// and the dual update pay L2 latency instead of HBM latency.
+__device__ __forceinline__ void prefetch_l2(const float2* p, int count) {
+  for (int t = threadIdx.x * 16; t < count; t += blockDim.x * 16)
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p + t));
+}
+
 template <int DP, int CS, int R>
 __device__ __forceinline__ void build_chunk_big(float2* dst, const SvtFamily& F, const float2* __restrict__ sp,
                                                 const float2* wcs, bool weighted, const int* lofs,
                                                 const float2* __restrict__ Dg, int i0, int rows, float inv_beta) {
   const int d = F.d;
-  for (int t = threadIdx.x; t < R * DP; t += blockDim.x) {
-    const int r = t / DP, u = t - r * DP;
-    float2 v = make_float2(0.f, 0.f);
-    if (r < rows && u < d) {
-      v = F.wide ? lift_global(F, sp, wcs, weighted, lofs[i0 + r], u)
-                 : cconj(lift_global(F, sp, wcs, weighted, lofs[u], i0 + r));  // tall: Ahat = A
-      if (Dg) {  // duals straight from HBM/L2 (coalesced rows)
-        const float2 dd = __ldcg(Dg + (long long)(i0 + r) * d + u);
-        v.x = fmaf(dd.x, inv_beta, v.x);
-        v.y = fmaf(dd.y, inv_beta, v.y);
+  // batches of four elements per thread: the four dual loads (HBM / L2) and
+  // the four lift sources (L2) are issued before the first is consumed
+  constexpr int NB4 = 4;
+  for (int t0 = threadIdx.x; t0 < R * DP; t0 += NB4 * blockDim.x) {
+    float2 dd[NB4], v[NB4];
+    int ru[NB4];
+#pragma unroll
+    for (int q = 0; q < NB4; ++q) {
+      const int t = t0 + q * blockDim.x;
+      const int r = t / DP, u = t - r * DP;
+      const bool ok = t < R * DP && r < rows && u < d;
+      ru[q] = t < R * DP ? r * CS + u : -1;
+      dd[q] = make_float2(0.f, 0.f);
+      v[q] = make_float2(0.f, 0.f);
+      if (ok) {
+        if (Dg) dd[q] = __ldcg(Dg + (long long)(i0 + r) * d + u);  // duals straight from HBM/L2 (coalesced rows)
+        v[q] = F.wide ? lift_global(F, sp, wcs, weighted, lofs[i0 + r], u)
+                      : cconj(lift_global(F, sp, wcs, weighted, lofs[u], i0 + r));  // tall: Ahat = A
       }
     }
-    dst[r * CS + u] = v;
+#pragma unroll
+    for (int q = 0; q < NB4; ++q)
+      if (ru[q] >= 0) dst[ru[q]] = make_float2(fmaf(dd[q].x, inv_beta, v[q].x), fmaf(dd[q].y, inv_beta, v[q].y));
   }
 }
 

@@ -6,6 +6,7 @@
 // svt_sub_huge.cu (248 < d <= 496) so the three build in parallel.
 #pragma once
 #include "svt_device.cuh"
+#include "svt_mma.cuh"
 
 namespace shlr_b200 {
 
@@ -636,7 +637,7 @@ __device__ void project_out(float2* M, const float2* __restrict__ V1, int ld, in
   __syncthreads();
 }
 
-template <int DP, int KB, int R, bool BIG, bool L2, int MINB = 1>
+template <int DP, int KB, int R, bool BIG, bool L2, int MINB = 1, bool MMA = false>
 __global__ void __launch_bounds__(kSubNT, MINB) svt_subspace_kernel(const SvtParams prm) {
   constexpr int NT = kSubNT;
   constexpr int KS = KB + 1;       // row stride of the d x KB blocks (conflict-free column walks)
@@ -662,6 +663,9 @@ __global__ void __launch_bounds__(kSubNT, MINB) svt_subspace_kernel(const SvtPar
                          : (BIG ? KB == kSubspaceKB : (KB == kSubspaceKB1 || KB == kSubspaceKB)),
                 "block size of the level");
   constexpr bool NOSPLIT = BIG && L2 && !HUGE;
+  // MMA: the chunk contractions run as 3xTF32 on the tensor cores (svt_mma.cuh)
+  static_assert(!MMA || (R == 32 && KB == 48 && !NOSPLIT && !HUGE && DP <= 128 && DP % 8 == 0),
+                "the mma.sync mappings cover 48-column blocks with d <= 128");
   static_assert(KB % 16 == 0 && KB % 8 == 0, "KB must be a multiple of 16");
   static_assert(R == 32 || HUGE, "the thread mappings assume 32-row chunks (HUGE: 16)");
   // Ritz pairs one deflation step keeps, and the margin below the block edge
@@ -737,6 +741,8 @@ __global__ void __launch_bounds__(kSubNT, MINB) svt_subspace_kernel(const SvtPar
   int* lofs = perm + KB;                             // max(d, e): lift offsets (lift_tab)
 
   float2* Dg = admm ? F.D + (long long)mat * e * d : nullptr;
+  // Ahat V of the Rayleigh-Ritz pass (e x KB), reused by the Z pass
+  float2* ycg = (MMA && prm.ycache) ? prm.ycache + (long long)blockIdx.x * e * KB : nullptr;
   float2* Vsg = F.Vs + (long long)mat * DP * KB1;  // level-1 store: KB1 columns
   float2* Vsg2 = L2 && F.Vs2 ? F.Vs2 + (long long)mat * DP * KB : nullptr;  // level-2 store
   // level 2 starts warm (from its own store) only for matrices it kept from
@@ -787,6 +793,8 @@ __global__ void __launch_bounds__(kSubNT, MINB) svt_subspace_kernel(const SvtPar
     if (tid < 4) S.flags[tid] = 0;
     if (tid == 0) *cnt = 0;
   }
+  int ns_steps = 0;  // Newton-Schulz steps taken (diagnostics)
+  if (BIG && Dg) prefetch_l2(Dg, min(R, e) * d);  // first chunk of the first pass
   long long clk_qr = 0, clk_pass = 0, clk_t = clock64();
   long long clk_wait = 0, clk_build = 0, clk_g1 = 0, clk_sum = 0, clk_g2 = 0, clk_u = 0;
 #define SUB_ACC(v) \
@@ -835,11 +843,16 @@ __global__ void __launch_bounds__(kSubNT, MINB) svt_subspace_kernel(const SvtPar
   // during the pass (X here, V in the epilogue pass): the copy of chunk c+1
   // overlaps the GEMMs of chunk c.
   for (int it = 0; it < iters; ++it) {
-    float2 xa[MR][NC];
+    float2 xa[MMA ? 1 : MR][MMA ? 1 : NC];
+    XAccMma xm;
+    if constexpr (MMA) {
+      xm.zero();
+    } else {
 #pragma unroll
-    for (int m = 0; m < MR; ++m)
+      for (int m = 0; m < MR; ++m)
 #pragma unroll
-      for (int n = 0; n < NC; ++n) xa[m][n] = make_float2(0.f, 0.f);
+        for (int n = 0; n < NC; ++n) xa[m][n] = make_float2(0.f, 0.f);
+    }
     __syncthreads();  // X (reflectors of the last QR) is free from here
     if (stg) stage_d_async(X, Dg, 0, min(R, e), d);
     if (prm.phase_clk) clk_u = clock64();
@@ -847,26 +860,32 @@ __global__ void __launch_bounds__(kSubNT, MINB) svt_subspace_kernel(const SvtPar
       const int rows = min(R, e - i0);
       if (stg) stage_d_wait();
       SUB_ACC(clk_wait);
+      if (BIG && Dg && i0 + R < e) prefetch_l2(Dg + (long long)(i0 + R) * d, min(R, e - i0 - R) * d);
       if (BIG) build_chunk_big<DP, CS, R>(C, F, spg, wl, weighted, lofs, Dg, i0, rows, prm.inv_beta);
       else build_chunk<DP, CS, R>(C, wl, lofs, F, Dg ? X : nullptr, i0, rows, prm.inv_beta);
       __syncthreads();
       SUB_ACC(clk_build);
       if (stg && i0 + R < e) stage_d_async(X, Dg, i0 + R, min(R, e - i0 - R), d);
       if constexpr (HUGE) chunk_block_huge<CS, KS, R>(C, V, Yc, d, KB, nullptr);  // Yc = C V
+      else if constexpr (MMA) chunk_block_mma<CS, KS, NC, R>(C, V, Yc, Yc2, d, nullptr);
       else chunk_block<CS, KS, NC, R, NOSPLIT>(C, V, Yc, Yc2, d, nullptr);
       SUB_ACC(clk_g1);
+      if constexpr (MMA) {
+        xacc_mma<CS, KS>(xm, C, Yc);  // X += C^H Yc (rows beyond the chunk are zero)
+      } else {
 #pragma unroll 4
-      for (int i = 0; i < rows; ++i) {  // X += C^H Yc
-        float2 yv[NC];
+        for (int i = 0; i < rows; ++i) {  // X += C^H Yc
+          float2 yv[NC];
 #pragma unroll
-        for (int n = 0; n < NC; ++n) yv[n] = Yc[i * KS + c16 + 16 * n];
+          for (int n = 0; n < NC; ++n) yv[n] = Yc[i * KS + c16 + 16 * n];
 #pragma unroll
-        for (int m = 0; m < MR; ++m) {
-          const int k = yi + 32 * m;
-          if (k < DP) {
-            const float2 a = C[i * CS + k];
+          for (int m = 0; m < MR; ++m) {
+            const int k = yi + 32 * m;
+            if (k < DP) {
+              const float2 a = C[i * CS + k];
 #pragma unroll
-            for (int n = 0; n < NC; ++n) cfmac(xa[m][n], a, yv[n]);
+              for (int n = 0; n < NC; ++n) cfmac(xa[m][n], a, yv[n]);
+            }
           }
         }
       }
@@ -874,16 +893,21 @@ __global__ void __launch_bounds__(kSubNT, MINB) svt_subspace_kernel(const SvtPar
       SUB_ACC(clk_g2);
     }
     if (stg) __syncthreads();
+    if constexpr (MMA) {
+      xacc_store<DP, KS>(xm, X);
+    } else {
 #pragma unroll
-    for (int m = 0; m < MR; ++m) {
-      const int k = yi + 32 * m;
-      if (k < DP)
+      for (int m = 0; m < MR; ++m) {
+        const int k = yi + 32 * m;
+        if (k < DP)
 #pragma unroll
-        for (int n = 0; n < NC; ++n) X[k * KS + c16 + 16 * n] = xa[m][n];
+          for (int n = 0; n < NC; ++n) X[k * KS + c16 + 16 * n] = xa[m][n];
+      }
     }
     __syncthreads();
     clk_pass += clock64() - clk_t;
     clk_t = clock64();
+    if (BIG && Dg) prefetch_l2(Dg, min(R, e) * d);  // first chunk of the next pass (behind the QR)
     if (defl3) project_defl(X);
     if (warm && inner_norm && it + 1 < iters) {
       // warm inner pass: X ~ V0 Lambda with V0 the previous (sorted) Ritz
@@ -901,7 +925,18 @@ __global__ void __launch_bounds__(kSubNT, MINB) svt_subspace_kernel(const SvtPar
       if (g < KB)
         for (int row = s8; row < DP; row += 8) V[row * KS + g] = cscale(X[row * KS + g], inv);
     } else {
-      householder_qr<KB, KS, DP, (HUGE ? 16 : 8)>(X, V, d, tau);
+      int ns = 0;
+      if constexpr (MMA) {
+        // warm pass: Cholesky QR on the tensor cores (ns_orth 1), or the
+        // Newton-Schulz trial (2: the tail columns of a warm block are too far
+        // from orthogonal for it, ||E||_F ~ 3)
+        if (warm && prm.ns_orth == 1)
+          ns = cholesky_qr_mma<KB, KS, DP>(X, V, C, BIG ? Yc : V, tau, S.flags + 3, 1e-3f);
+        else if (warm && prm.ns_orth == 2)
+          ns = newton_schulz_orth<KB, KS, DP>(X, V, C, tau);
+        ns_steps += ns;
+      }
+      if (ns == 0) householder_qr<KB, KS, DP, (HUGE ? 16 : 8)>(X, V, d, tau);
       if (defl3 && d - nd_in < KB) project_defl(V);
     }
     clk_qr += clock64() - clk_t;
@@ -921,30 +956,46 @@ __global__ void __launch_bounds__(kSubNT, MINB) svt_subspace_kernel(const SvtPar
   // ---------------------------------------------------------- Rayleigh-Ritz: H = (Ahat V)^H (Ahat V)
   {
     constexpr int HM = (KB + 31) / 32;
-    float2 h[HM][NC];
+    float2 h[MMA ? 1 : HM][MMA ? 1 : NC];
+    HAccMma hm;
+    if constexpr (MMA) {
+      hm.zero();
+    } else {
 #pragma unroll
-    for (int m = 0; m < HM; ++m)
+      for (int m = 0; m < HM; ++m)
 #pragma unroll
-      for (int n = 0; n < NC; ++n) h[m][n] = make_float2(0.f, 0.f);
+        for (int n = 0; n < NC; ++n) h[m][n] = make_float2(0.f, 0.f);
+    }
     __syncthreads();  // X is free from here
     if (stg) stage_d_async(X, Dg, 0, min(R, e), d);
     for (int i0 = 0; i0 < e; i0 += R) {
       const int rows = min(R, e - i0);
       if (stg) stage_d_wait();
+      if (BIG && Dg && i0 + R < e) prefetch_l2(Dg + (long long)(i0 + R) * d, min(R, e - i0 - R) * d);
       if (BIG) build_chunk_big<DP, CS, R>(C, F, spg, wl, weighted, lofs, Dg, i0, rows, prm.inv_beta);
       else build_chunk<DP, CS, R>(C, wl, lofs, F, Dg ? X : nullptr, i0, rows, prm.inv_beta);
       __syncthreads();
       if (stg && i0 + R < e) stage_d_async(X, Dg, i0 + R, min(R, e - i0 - R), d);
       if constexpr (HUGE) chunk_block_huge<CS, KS, R>(C, V, Yc, d, KB, nullptr);
+      else if constexpr (MMA) chunk_block_mma<CS, KS, NC, R>(C, V, Yc, Yc2, d, nullptr);
       else chunk_block<CS, KS, NC, R, NOSPLIT>(C, V, Yc, Yc2, d, nullptr);
-      for (int i = 0; i < rows; ++i) {
+      if constexpr (MMA) {
+        if (ycg)  // Ahat V rows of this chunk, kept for the Z pass
+          for (int t = tid; t < rows * KB; t += NT) {
+            const int i = t / KB, j = t - i * KB;
+            ycg[(long long)(i0 + i) * KB + j] = Yc[i * KS + j];
+          }
+        hacc_mma<KS>(hm, Yc);  // rows beyond the chunk are zero
+      } else {
+        for (int i = 0; i < rows; ++i) {
 #pragma unroll
-        for (int m = 0; m < HM; ++m) {
-          const int a = yi + 32 * m;
-          if (a < KB) {
-            const float2 ya = Yc[i * KS + a];
+          for (int m = 0; m < HM; ++m) {
+            const int a = yi + 32 * m;
+            if (a < KB) {
+              const float2 ya = Yc[i * KS + a];
 #pragma unroll
-            for (int n = 0; n < NC; ++n) cfmac(h[m][n], ya, Yc[i * KS + c16 + 16 * n]);
+              for (int n = 0; n < NC; ++n) cfmac(h[m][n], ya, Yc[i * KS + c16 + 16 * n]);
+            }
           }
         }
       }
@@ -952,26 +1003,44 @@ __global__ void __launch_bounds__(kSubNT, MINB) svt_subspace_kernel(const SvtPar
     }
     if (stg) __syncthreads();
     // H (full Hermitian, stride KB+1 = KS) into Hm, diagonal to S.dg
-#pragma unroll
-    for (int m = 0; m < HM; ++m) {
-      const int a = yi + 32 * m;
-      if (a < KB)
-#pragma unroll
-        for (int n = 0; n < NC; ++n) {
-          const int b = c16 + 16 * n;
-          if (a == b) S.dg[a] = h[m][n].x;
-          Hm[a * KS + b] = h[m][n];
+    if constexpr (MMA) {
+      hacc_store<KS>(hm, Hm);  // upper block triangle
+      __syncthreads();
+      // mirror into the lower triangle (the diagonal blocks hold both
+      // triangles, equal only to the last bits of the split products)
+      for (int t = tid; t < KB * KB; t += NT) {
+        const int a = t / KB, b = t - a * KB;
+        if (a < b) {
+          Hm[b * KS + a] = cconj(Hm[a * KS + b]);
+        } else if (a == b) {
+          const float2 v = Hm[a * KS + a];
+          Hm[a * KS + a] = make_float2(v.x, 0.f);
+          S.dg[a] = v.x;
         }
+      }
+    } else {
+#pragma unroll
+      for (int m = 0; m < HM; ++m) {
+        const int a = yi + 32 * m;
+        if (a < KB)
+#pragma unroll
+          for (int n = 0; n < NC; ++n) {
+            const int b = c16 + 16 * n;
+            if (a == b) S.dg[a] = h[m][n].x;
+            Hm[a * KS + b] = h[m][n];
+          }
+      }
     }
   }
   __syncthreads();
+  if (BIG && Dg) prefetch_l2(Dg, min(R, e) * d);  // first chunk of the Z pass (behind the Rayleigh-Ritz solve)
   if (!prm.rr_jacobi) {
     SUB_STAMP(4);
     hermitian_eig_tridiag<KB, KS>(Hm, reinterpret_cast<float*>(S.rec), reinterpret_cast<float*>(C), C, S.dg,
                                   0.25f * prm.thresh * prm.thresh,
                                   prm.phase_clk ? prm.phase_clk + (long long)blockIdx.x * kPhaseSlots + 16 : nullptr);
     SUB_STAMP(5);
-    if (prm.sweeps_out && tid == 0) prm.sweeps_out[blockIdx.x] = 0;
+    if (prm.sweeps_out && tid == 0) prm.sweeps_out[blockIdx.x] = ns_steps;
   } else {
   if (tid < 32) {  // absolute rotation floor relative to the largest Ritz value
     double mx = 0.0;
@@ -1020,7 +1089,13 @@ __global__ void __launch_bounds__(kSubNT, MINB) svt_subspace_kernel(const SvtPar
   }
   __syncthreads();
   // V <- V U (Ritz vectors, sorted) into X
-  {
+  if constexpr (MMA) {
+    XAccMma vm;
+    vm.zero();
+    vu_mma<KS, KB>(vm, V, C);
+    if (BIG) __syncthreads();  // in place: all reads of V are done
+    xacc_store_perm<DP, KS>(vm, X, perm);
+  } else {
     float2 va[MR][NC];
 #pragma unroll
     for (int m = 0; m < MR; ++m)
@@ -1116,70 +1191,153 @@ __global__ void __launch_bounds__(kSubNT, MINB) svt_subspace_kernel(const SvtPar
   // ---------------------------------------------------------- Z = (Ahat V) f V^H, duals, adjoint
   SUB_STAMP(6);
   float2* Ds = V;  // the old basis is dead: stage the duals there (non-BIG)
+  // cached Z pass (tensor-core variants): Ahat Vf = (Ahat V) U comes from the
+  // Rayleigh-Ritz pass's Ahat V (ycg) and the rotation U (sorted, scaled by
+  // the shrink factors) instead of rebuilding the chunk and multiplying by Vf
+  constexpr int US = 32;  // row stride of the scaled rotation (its first 16 nb <= 32 sorted columns)
+  constexpr bool CACHE_OK = MMA && (BIG || DP * KS - R * DP >= KB * US);
+  const bool cached = CACHE_OK && ycg != nullptr && r <= 32;
+  float2* Us = BIG ? Yc2 : V + R * DP;  // BIG: the idle split buffer; else behind the staged duals
+  const int nbz = (r + 15) >> 4;
+  float2 ypre[3];
+  auto ycache_fetch = [&](int i0) {
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const int t = tid + NT * q, i = t / KB, j = t - i * KB;
+      ypre[q] = (i0 + i < e) ? __ldcg(ycg + (long long)(i0 + i) * KB + j) : make_float2(0.f, 0.f);
+    }
+  };
+  if (cached) {
+    static_assert(!MMA || R * KB == 3 * kSubNT, "three cached elements per thread");
+    for (int t = tid; t < KB * KB; t += NT) {
+      const int j = t / KB, c = t - j * KB;
+      const int pc = perm[c];
+      if (pc < US) Us[j * US + pc] = cscale(C[j * KS + c], S.f[pc]);
+    }
+    ycache_fetch(0);
+  }
   __syncthreads();
   if (stg) stage_d_async(Ds, Dg, 0, min(R, e), d);
   for (int i0 = 0; i0 < e; i0 += R) {
     const int rows = min(R, e - i0);
+    if (cached) {  // Yc is free (the previous chunk's Z GEMM is behind a barrier)
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const int t = tid + NT * q, i = t / KB, j = t - i * KB;
+        Yc[i * KS + j] = ypre[q];
+      }
+    }
+    if (BIG && Dg && i0 + R < e) prefetch_l2(Dg + (long long)(i0 + R) * d, min(R, e - i0 - R) * d);
     if (stg) stage_d_wait();
+    else if (cached) __syncthreads();
+    if (cached) {
+      if constexpr (MMA) {
+        if (i0 + R < e) ycache_fetch(i0 + R);
+        ycache_rotate_mma<KS, US>(Yc, Us, nbz);
+      }
+    } else {
     if (BIG) build_chunk_big<DP, CS, R>(C, F, spg, wl, weighted, lofs, Dg, i0, rows, prm.inv_beta);
     else build_chunk<DP, CS, R>(C, wl, lofs, F, Dg ? Ds : nullptr, i0, rows, prm.inv_beta);
     __syncthreads();
-    {
+    }
+    if (!cached) {
       // only the first r (sorted) Ritz columns have f > 0 (Z1 mode: the
       // leading kDeflateK)
       static_assert(NC <= 4, "NC > 4 needs more cases");
       const int nb = ((to_defl ? DSTEP : r) + 15) >> 4;
       if constexpr (HUGE) chunk_block_huge<CS, KS, R>(C, Vf, Yc, d, min(KB, 16 * nb), S.f);
+      else if constexpr (MMA) {
+        if (nb <= 1) chunk_block_mma<CS, KS, 1, R>(C, Vf, Yc, Yc2, d, S.f);
+        else if (nb == 2) chunk_block_mma<CS, KS, 2, R>(C, Vf, Yc, Yc2, d, S.f);
+        else chunk_block_mma<CS, KS, 3, R>(C, Vf, Yc, Yc2, d, S.f);
+      }
       else if (nb <= 1) chunk_block<CS, KS, 1, R, NOSPLIT>(C, Vf, Yc, Yc2, d, S.f);
       else if (nb == 2 || NC == 2) chunk_block<CS, KS, (NC >= 2 ? 2 : 1), R, NOSPLIT>(C, Vf, Yc, Yc2, d, S.f);
       else if (nb == 3 || NC == 3) chunk_block<CS, KS, (NC >= 3 ? 3 : 1), R, NOSPLIT>(C, Vf, Yc, Yc2, d, S.f);
       else chunk_block<CS, KS, NC, R, NOSPLIT>(C, Vf, Yc, Yc2, d, S.f);
     }
     {
-      // Z[zr][k] = sum_{j < r} Yc[zr][j] conj(Vf[k][j]), k = zc + ZC m
-      constexpr int MZ = (DP + ZC - 1) / ZC;
-      const int zr = tid / ZC, zc = tid % ZC;
-      float2 z[MZ];
-#pragma unroll
-      for (int m = 0; m < MZ; ++m) z[m] = make_float2(0.f, 0.f);
+      // Z[zr][k] = sum_{j < r} Yc[zr][j] conj(Vf[k][j]), then the dual update
+      // and T = Z - D/beta into the chunk buffer for the adjoint
       const int rz = to_defl ? DSTEP : r;
-      for (int j = 0; j < rz; ++j) {
-        const float2 yv = Yc[zr * KS + j];
-#pragma unroll
-        for (int m = 0; m < MZ; ++m) {
-          const int k = zc + ZC * m;
-          if (k < DP) cfmac(z[m], Vf[k * KS + j], yv);  // yv * conj(V[k][j])
+      // dpre: the dual element, when the caller already loaded it (large-d layout)
+      auto finish = [&](int zr, int k, float2 z, const float2* dpre = nullptr) {
+        if (!(zr < rows && k < d)) return;
+        if (to_defl) {  // Z1 only (accumulated along the chain): level 3 finishes this matrix
+          float2* z1p = F.Z1 + (long long)mat * e * d + (long long)(i0 + zr) * d + k;
+          *z1p = defl3 ? cadd(__ldcg(z1p), z) : z;
+          return;
         }
-      }
-#pragma unroll
-      for (int m = 0; m < MZ; ++m) {
-        const int k = zc + ZC * m;
-        if (zr < rows && k < d) {
-          if (to_defl) {  // Z1 only (accumulated along the chain): level 3 finishes this matrix
-            float2* z1p = F.Z1 + (long long)mat * e * d + (long long)(i0 + zr) * d + k;
-            *z1p = defl3 ? cadd(__ldcg(z1p), z[m]) : z[m];
-            continue;
-          }
-          if (defl3) {
-            const float2 z1 = __ldcg(F.Z1 + (long long)mat * e * d + (long long)(i0 + zr) * d + k);
-            z[m].x += z1.x;
-            z[m].y += z1.y;
-          }
-          float2 tv = z[m];
-          if (admm) {
-            const float2 L = BIG ? (F.wide ? lift_global(F, spg, wl, weighted, lofs[i0 + zr], k)
-                                           : cconj(lift_global(F, spg, wl, weighted, lofs[k], i0 + zr)))
-                                 : lift_tab(wl, lofs, F.wide, i0 + zr, k);
-            const long long gi = (long long)(i0 + zr) * d + k;
-            float2 dn = BIG ? __ldcg(Dg + gi) : Ds[zr * d + k];
-            dn.x = fmaf(prm.tau_dual, L.x - z[m].x, dn.x);
-            dn.y = fmaf(prm.tau_dual, L.y - z[m].y, dn.y);
-            Dg[gi] = dn;
-            tv.x = fmaf(-dn.x, prm.inv_beta, z[m].x);
-            tv.y = fmaf(-dn.y, prm.inv_beta, z[m].y);
-          }
-          C[zr * CS + k] = tv;
+        if (defl3) {
+          const float2 z1 = __ldcg(F.Z1 + (long long)mat * e * d + (long long)(i0 + zr) * d + k);
+          z.x += z1.x;
+          z.y += z1.y;
         }
+        float2 tv = z;
+        if (admm) {
+          const float2 L = BIG ? (F.wide ? lift_global(F, spg, wl, weighted, lofs[i0 + zr], k)
+                                         : cconj(lift_global(F, spg, wl, weighted, lofs[k], i0 + zr)))
+                               : lift_tab(wl, lofs, F.wide, i0 + zr, k);
+          const long long gi = (long long)(i0 + zr) * d + k;
+          float2 dn = BIG ? (dpre ? *dpre : __ldcg(Dg + gi)) : Ds[zr * d + k];
+          dn.x = fmaf(prm.tau_dual, L.x - z.x, dn.x);
+          dn.y = fmaf(prm.tau_dual, L.y - z.y, dn.y);
+          Dg[gi] = dn;
+          tv.x = fmaf(-dn.x, prm.inv_beta, z.x);
+          tv.y = fmaf(-dn.y, prm.inv_beta, z.y);
+        }
+        C[zr * CS + k] = tv;
+      };
+      if constexpr (MMA) {
+        // all reads of the chunk (the GEMM above) are behind chunk_block_mma's barrier
+        ZAccMma zm;
+        zgemm_mma<DP, KS>(zm, Yc, Vf, (rz + 7) >> 3);
+        // through the chunk buffer, so the dual update below walks rows
+        // contiguously (coalesced dual stores, conflict-free lifts)
+        zm.for_each<DP>([&](int zr, int k, float2 z) {
+          if (k < DP) C[zr * CS + k] = z;
+        });
+        __syncthreads();
+        if (BIG && admm) {
+          // duals straight from HBM / L2: four loads in flight per thread
+          for (int t0 = tid; t0 < rows * d; t0 += 4 * NT) {
+            float2 dp4[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int t = t0 + q * NT;
+              dp4[q] = t < rows * d ? __ldcg(Dg + (long long)i0 * d + t) : make_float2(0.f, 0.f);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int t = t0 + q * NT;
+              if (t < rows * d) {
+                const int zr = t / d, k = t - zr * d;
+                finish(zr, k, C[zr * CS + k], &dp4[q]);
+              }
+            }
+          }
+        } else {
+          for (int t = tid; t < rows * d; t += NT) {
+            const int zr = t / d, k = t - zr * d;
+            finish(zr, k, C[zr * CS + k]);
+          }
+        }
+      } else {
+        constexpr int MZ = (DP + ZC - 1) / ZC;
+        const int zr = tid / ZC, zc = tid % ZC;
+        float2 z[MZ];
+#pragma unroll
+        for (int m = 0; m < MZ; ++m) z[m] = make_float2(0.f, 0.f);
+        for (int j = 0; j < rz; ++j) {
+          const float2 yv = Yc[zr * KS + j];
+#pragma unroll
+          for (int m = 0; m < MZ; ++m) {
+            const int k = zc + ZC * m;
+            if (k < DP) cfmac(z[m], Vf[k * KS + j], yv);  // yv * conj(V[k][j])
+          }
+        }
+#pragma unroll
+        for (int m = 0; m < MZ; ++m) finish(zr, zc + ZC * m, z[m]);
       }
     }
     __syncthreads();
@@ -1295,15 +1453,15 @@ __global__ void __launch_bounds__(kSubNT, MINB) svt_subspace_kernel(const SvtPar
 
 
 namespace {
-template <int DP, int KB, bool BIG, bool L2, int MINB = 1>
+template <int DP, int KB, bool BIG, bool L2, int MINB = 1, bool MMA = false>
 void launch_sub(const SvtParams& prm, int total, size_t smem, cudaStream_t stream) {
   static bool configured = false;
   if (!configured) {
-    SHLR_CUDA(cudaFuncSetAttribute(svt_subspace_kernel<DP, KB, 32, BIG, L2, MINB>,
+    SHLR_CUDA(cudaFuncSetAttribute(svt_subspace_kernel<DP, KB, 32, BIG, L2, MINB, MMA>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     configured = true;
   }
-  svt_subspace_kernel<DP, KB, 32, BIG, L2, MINB><<<total, kSubNT, smem, stream>>>(prm);
+  svt_subspace_kernel<DP, KB, 32, BIG, L2, MINB, MMA><<<total, kSubNT, smem, stream>>>(prm);
   SHLR_LAUNCH_CHECK();
 }
 }  // namespace
