@@ -188,13 +188,20 @@ struct RhsOp {
 
 // First SPIRiT stage: p = r + gamma p (or x for the initial residual), then
 // the row iFFT of it into tmp.
+// With xu / ap set (fused CG): the previous iteration's x += alpha p, r -=
+// alpha A p is applied here first -- its alpha and the new residual norm were
+// both finalised by the previous row-forward stage (rho' = rho - 2 alpha
+// Re<r, A p> + alpha^2 <A p, A p>), so the vector update needs no kernel and no
+// reduction of its own.
 struct SpiritRowInvOp {
-  const float2* r;
+  float2* r;
   float2* p;
   const float2* x;   // non-null: apply to x instead of p
   float2* tmp;
   long long NJ, J;
   const SolverCtl* ctl;
+  float2* xu = nullptr;        // fused CG: the iterate to update
+  const float2* ap = nullptr;  // fused CG: A p of the previous iteration
   __device__ bool skip() const { return halted(ctl) || (x == nullptr && ctl->cg.done); }
   __device__ float2 load(int o, int k, int i) const {
     const long long idx = o * NJ + k * J + i;
@@ -203,6 +210,15 @@ struct SpiritRowInvOp {
     if (ctl->cg.it > 0) {
       const float g = (float)ctl->cg.gamma;
       const float2 pv = p[idx];
+      if (xu) {
+        const float a = (float)ctl->cg.alpha;
+        const float2 av = ap[idx];
+        float2 xv = xu[idx];
+        xv = make_float2(fmaf(a, pv.x, xv.x), fmaf(a, pv.y, xv.y));
+        v = make_float2(fmaf(-a, av.x, v.x), fmaf(-a, av.y, v.y));
+        xu[idx] = xv;
+        r[idx] = v;
+      }
       v = make_float2(fmaf(g, pv.x, v.x), fmaf(g, pv.y, v.y));
     }
     p[idx] = v;
@@ -241,6 +257,7 @@ __global__ void k_cg_init_diag(const float2* __restrict__ bk, const float* __res
     c.it = 0;
     c.zero_b = 0;
     c.done = 0;
+    c.pending = 0;
     c.gamma = 0.0;
     c.bnorm = sqrt(b2);
     if (c.bnorm == 0.0) {  // solvers.cpp:30-33: zero right-hand side -> x = 0
@@ -409,6 +426,7 @@ __global__ void k_cg_init_from_ap(const float2* __restrict__ bk, const float2* _
     c.it = 0;
     c.zero_b = 0;
     c.done = 0;
+    c.pending = 0;
     c.gamma = 0.0;
     c.bnorm = sqrt(b2);
     if (c.bnorm == 0.0) {
@@ -525,9 +543,12 @@ __global__ void __launch_bounds__(kFftThreads) k_spirit_cols(const float2* __res
 
 // Row forward stage of row m (smem `sm`: 2 N J float2): v = F1(tmp2 row);
 // ap = dg p + lambda1 v.  Returns this thread's share of Re<p, ap>.
+// rres (optional, fused CG): the residual; then s2 = Re<r, ap>, s3 = <ap, ap>.
 __device__ double spirit_row_fwd(const float2* __restrict__ tmp2, const float2* __restrict__ vec,
                                  const float* __restrict__ dg, float2* __restrict__ ap, const FftTwiddles& tw,
-                                 int J, float lambda1, int m, float2* sm) {
+                                 int J, float lambda1, int m, float2* sm,
+                                 const float2* __restrict__ rres = nullptr, double* s2 = nullptr,
+                                 double* s3 = nullptr) {
   const int N = tw.n;
   const int F = J;
   const long long NJ = (long long)N * J;
@@ -540,23 +561,25 @@ __device__ double spirit_row_fwd(const float2* __restrict__ tmp2, const float2* 
   // their L2 latency hides under it (up to 4 elements per thread)
   constexpr int kPre = 4;
   const bool pre = N * F <= kPre * (int)blockDim.x;
-  float2 pv_pre[kPre];
+  float2 pv_pre[kPre], rv_pre[kPre];
   float dv_pre[kPre];
   if (pre) {
 #pragma unroll
     for (int u = 0; u < kPre; ++u) {
       const int t = threadIdx.x + u * blockDim.x;
+      rv_pre[u] = make_float2(0.f, 0.f);
       if (t < N * F) {
         const int k = lf >= 0 ? t >> lf : t / F;
         pv_pre[u] = vec[m * NJ + t];
         dv_pre[u] = dg[(long long)m * N + k];
+        if (rres) rv_pre[u] = rres[m * NJ + t];
       }
     }
   }
   __syncthreads();
   float2* res = smem_centered_dft<false>(a, b, tw, F);
   const float isn = rsqrtf((float)N);
-  double s = 0.0;
+  double s = 0.0, sra = 0.0, saa = 0.0;
 #pragma unroll 4
   for (int t = threadIdx.x, u = 0; t < N * F; t += blockDim.x, ++u) {
     const int k = lf >= 0 ? t >> lf : t / F;
@@ -567,30 +590,78 @@ __device__ double spirit_row_fwd(const float2* __restrict__ tmp2, const float2* 
     const float2 av = make_float2(fmaf(dv, pv.x, lambda1 * v.x), fmaf(dv, pv.y, lambda1 * v.y));
     ap[idx] = av;
     s += (double)pv.x * av.x + (double)pv.y * av.y;
+    if (rres) {
+      const float2 rv = pre ? rv_pre[u & (kPre - 1)] : rres[idx];
+      sra += (double)rv.x * av.x + (double)rv.y * av.y;
+      saa += (double)av.x * av.x + (double)av.y * av.y;
+    }
   }
+  if (s2) *s2 = sra;
+  if (s3) *s3 = saa;
   return s;
 }
 
 // SPIRiT row forward stage, one CTA per row m: v = F1(tmp2 row);
 // ap = dg p + lambda1 v.  mode 0: CG iteration (reduce denom, finalize alpha);
 // mode 1: initial residual (apply to x, store ap only).
+// mode 2 (fused CG, rres = the residual): also Re<r, A p> and <A p, A p>, from
+// which the last CTA finalises alpha AND the next residual norm
+//   rho' = rho - 2 alpha Re<r, A p> + alpha^2 <A p, A p>   (= |r - alpha A p|^2,
+// alpha rounded to FP32 as the vector update uses it), the stop test and
+// gamma (cg_solve, solvers.cpp:44-62); the vector update itself is left
+// pending for the next row-inverse stage or k_cg_flush.
 __global__ void __launch_bounds__(kFftThreads) k_spirit_rows_fwd(const float2* __restrict__ tmp2,
                                                          const float2* __restrict__ vec,
                                                          const float* __restrict__ dg,
                                                          float2* __restrict__ ap, FftTwiddles tw,
                                                          int J, float lambda1, SolverCtl* ctl,
-                                                         double* partials, int mode) {
+                                                         double* partials, int mode,
+                                                         const float2* __restrict__ rres, int cg_max,
+                                                         double cg_tol) {
   extern __shared__ float2 sm[];
   __shared__ double sh[32];
-  if (halted(ctl) || (mode == 0 && ctl->cg.done)) return;
-  const double s = spirit_row_fwd(tmp2, vec, dg, ap, tw, J, lambda1, blockIdx.x, sm);
-  if (mode != 0) return;
-  double v = block_sum(s, sh);
-  if (!publish_and_check_last(partials, gridDim.x, &v, 1, &ctl->arrive[1])) return;
+  if (halted(ctl) || (mode != 1 && ctl->cg.done)) return;
+  double s2 = 0.0, s3 = 0.0;
+  const double s = spirit_row_fwd(tmp2, vec, dg, ap, tw, J, lambda1, blockIdx.x, sm, mode == 2 ? rres : nullptr,
+                                  &s2, &s3);
+  if (mode == 1) return;
+  double vals[3];
+  vals[0] = block_sum(s, sh);
+  if (mode == 2) {
+    vals[1] = block_sum(s2, sh);
+    vals[2] = block_sum(s3, sh);
+  }
+  if (!publish_and_check_last(partials, gridDim.x, vals, mode == 2 ? 3 : 1, &ctl->arrive[1])) return;
   const double denom = sum_partials(partials, gridDim.x, 0, sh);
+  double rap = 0.0, apap = 0.0;
+  if (mode == 2) {
+    rap = sum_partials(partials, gridDim.x, 1, sh);
+    apap = sum_partials(partials, gridDim.x, 2, sh);
+  }
   if (threadIdx.x == 0) {
     finalize_alpha(ctl, denom);
+    if (mode == 2 && !ctl->cg.done) {
+      const double a = (double)(float)ctl->cg.alpha;
+      double rho_next = ctl->cg.rho - 2.0 * a * rap + a * a * apap;
+      if (rho_next < 0.0) rho_next = 0.0;  // (a NaN stays a NaN: finalize_rho reports it)
+      ctl->cg.pending = 1;
+      finalize_rho(ctl, rho_next, cg_max, cg_tol);
+    }
     ctl->arrive[1] = 0;
+  }
+}
+
+// The pending vector update of the last fused CG iteration: x += alpha p
+// (the residual is not used after the loop).
+__global__ void k_cg_flush(float2* __restrict__ x, const float2* __restrict__ p, size_t nel,
+                           const SolverCtl* ctl) {
+  if (halted(ctl) || !ctl->cg.pending) return;
+  const float a = (float)ctl->cg.alpha;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nel; i += stride) {
+    const float2 pv = p[i];
+    float2 xv = x[i];
+    x[i] = make_float2(fmaf(a, pv.x, xv.x), fmaf(a, pv.y, xv.y));
   }
 }
 
@@ -907,11 +978,14 @@ PiPlan::PiPlan(const PiConfig& cfg, const double* y, const uint8_t* mask, size_t
       ndefl_ = dalloc_s<int>((size_t)(M + N), stream_);
     }
   }
+  if (std::max(dr, dc) <= 128)
+    ycache_ = dalloc_s<float2>((size_t)(M + N) * std::max(er, ec) * kSubspaceKB, stream_);
   fallback_ = dalloc_s<int>((size_t)(M + N), stream_);
   SHLR_CUDA(cudaMemsetAsync(fallback_, 0, sizeof(int) * (M + N), stream_));
   if (const char* s = std::getenv("SHLR_Q_COLD")) q_cold_ = std::atoi(s);
   if (const char* s = std::getenv("SHLR_Q_WARM")) q_warm_ = std::atoi(s);
   if (std::getenv("SHLR_FULL_SVT")) subspace_ = false;
+  if (std::getenv("SHLR_CG_UNFUSED")) cg_fused_ = false;
   if (const char* s = std::getenv("SHLR_KB1")) kb1_ = std::atoi(s) == kSubspaceKB1 ? kSubspaceKB1 : kSubspaceKB;
   if (const char* s = std::getenv("SHLR_RR_REL")) rr_tol_rel_ = (float)std::atof(s);
   if (const char* s = std::getenv("SHLR_RR_ABS")) rr_tol_abs_ = (float)std::atof(s);
@@ -988,7 +1062,7 @@ PiPlan::~PiPlan() {
   void* bufs[] = {yk_, x_, xold_, r_, p_, ap_, bk_, tmp_, tmp2_, dg_, srow_, scol_, hrow_, hcol_,
                   hrow0_, hcol0_, drow_, dcol_, wcN_, wcM_, pmat_, twM_, twN_, sv_, partials_,
                   ctl_, log_, x0_, vrow_, vcol_, sweeps_, vsrow_, vscol_, vs2row_, vs2col_, z1row_, z1col_, vdrow_, vdcol_, ndefl_,
-                  fallback_};
+                  fallback_, ycache_};
   for (void* b : bufs)
     if (b) cudaFreeAsync(b, stream_);
   if (ev0_) cudaEventDestroy(ev0_);
@@ -1016,7 +1090,12 @@ void PiPlan::cg_apply_spirit(float2* in_vec, float2* out_ap, bool init) {
   const int M = cfg_.M, N = cfg_.N, J = cfg_.J;
   const long long NJ = (long long)N * J;
   // stage 1: row iFFT (with p update)
-  SpiritRowInvOp op1{r_, p_, init ? in_vec : nullptr, tmp_, NJ, J, ctl_};
+  // fused CG (default): the vector update of the previous CG iteration rides
+  // in this stage's loads, its scalars come from the row-forward stage
+  // (SHLR_CG_UNFUSED=1: the separate k_cg_b update kernel per iteration)
+  const bool fused = !init && cg_fused_;
+  SpiritRowInvOp op1{r_, p_, init ? in_vec : nullptr, tmp_, NJ, J, ctl_, fused ? x_ : nullptr,
+                     fused ? ap_ : nullptr};
   launch_fft_axis<SpiritRowInvOp, true>(op1, tN_, M, J, J, stream_);
   ++launch_count_;
   // stage 2: columns
@@ -1030,7 +1109,8 @@ void PiPlan::cg_apply_spirit(float2* in_vec, float2* out_ap, bool init) {
   // stage 3: row FFT + combine (+ alpha)
   const size_t smem3 = 2 * (size_t)N * J * sizeof(float2);
   k_spirit_rows_fwd<<<M, kFftThreads, smem3, stream_>>>(tmp2_, init ? in_vec : p_, dg_, out_ap, tN_, J,
-                                                     (float)cfg_.lambda1, ctl_, partials_, init ? 1 : 0);
+                                                     (float)cfg_.lambda1, ctl_, partials_,
+                                                     init ? 1 : (fused ? 2 : 0), r_, cfg_.cg_max, cfg_.cg_tol);
   SHLR_LAUNCH_CHECK();
   ++launch_count_;
 }
@@ -1080,8 +1160,14 @@ void PiPlan::enqueue_iteration(int k, bool record_events) {
     } else {
       for (int it = 0; it < cfg_.cg_max; ++it) {
         cg_apply_spirit(p_, ap_, false);
-        k_cg_b<<<g, kThreads, 0, stream_>>>(x_, r_, p_, ap_, dg_, nel_, J, ctl_, partials_, cfg_.cg_max,
-                                           cfg_.cg_tol);
+        if (!cg_fused_) {
+          k_cg_b<<<g, kThreads, 0, stream_>>>(x_, r_, p_, ap_, dg_, nel_, J, ctl_, partials_, cfg_.cg_max,
+                                             cfg_.cg_tol);
+          launch_count_ += 1;
+        }
+      }
+      if (cg_fused_) {
+        k_cg_flush<<<g, kThreads, 0, stream_>>>(x_, p_, nel_, ctl_);
         launch_count_ += 1;
       }
     }
@@ -1161,6 +1247,7 @@ void PiPlan::enqueue_iteration(int k, bool record_events) {
       sp.relc_q3 = std::getenv("SHLR_RELC_Q3") ? (float)std::atof(std::getenv("SHLR_RELC_Q3")) : 1e-2f;
     }
     sp.phase_clk = phase_clk_;
+    sp.ycache = ycache_;
     if (record_events) SHLR_CUDA(cudaEventRecord(evA_, stream_));
     // The debug singular-value hook needs every singular value: full solver.
     const bool want_sv = sp.fam[0].sv != nullptr;

@@ -13,7 +13,9 @@ namespace shlr_b200 {
 
 struct CgState {
   double bnorm, rho, denom, alpha, gamma, rel, rho_next, pad0;
-  int it, done, zero_b, pad1;
+  int it, done, zero_b;
+  int pending;  // SPIRiT CG: x += alpha p, r -= alpha A p of the last iteration not yet applied
+                // (fused into the next iteration's row stage, or flushed by k_cg_flush)
 };
 
 struct SolverCtl {
@@ -84,6 +86,8 @@ class PiPlan {
   float2 *hrow0_ = nullptr, *hcol0_ = nullptr;
   float2 *drow_ = nullptr, *dcol_ = nullptr;
   float2 *vrow_ = nullptr, *vcol_ = nullptr;  // SVT eigenvector stores (warm start)
+  bool cg_fused_ = true;      // SPIRiT CG: vector update fused into the row stages (SHLR_CG_UNFUSED=1: off)
+  float2* ycache_ = nullptr;  // Ahat V of the Rayleigh-Ritz pass, kept for the Z pass (SvtParams::ycache)
   float2 *vsrow_ = nullptr, *vscol_ = nullptr;  // subspace-solver block stores (warm start)
   float2 *vs2row_ = nullptr, *vs2col_ = nullptr;  // large-d level-2 block stores
   float2 *z1row_ = nullptr, *z1col_ = nullptr;    // large-d level-2 Z1 (level-3 deflation)
