@@ -267,6 +267,128 @@ __device__ __forceinline__ void build_chunk_big(float2* dst, const SvtFamily& F,
   }
 }
 
+// Large-d layout, staged lift sources.  A chunk of R rows of Ahat only touches
+// a few hundred distinct source elements (a wide chunk: the whole vector of
+// the 3-4 blocks its rows belong to; a tall chunk: rows + q - 1 positions of
+// every block), each of them ~R times (Hankel structure).  With two CTAs per
+// SM there is almost no L1 left, so lift_global's per-element loads all go to
+// L2, one 32-byte sector per lane (coil-fastest spectra).  Here the sources
+// are loaded once per chunk into a small shared buffer, weighting and
+// virtual-coil dagger applied (lift_weighted, operators.cpp:36-56), and the
+// chunk is built from shared memory.
+constexpr int kBuildThreads = 512;  // threads of the subspace kernel (kSubNT)
+struct ChunkSources {
+  int b_lo, span, ok;
+};
+__device__ __forceinline__ ChunkSources stage_chunk_sources(float2* st, int cap, const SvtFamily& F,
+                                                            const float2* __restrict__ sp, const float2* wcs,
+                                                            bool weighted, int i0, int rows) {
+  ChunkSources cs;
+  int nblk, n0;
+  if (F.wide) {
+    cs.b_lo = i0 / F.q;
+    nblk = (i0 + rows - 1) / F.q - cs.b_lo + 1;
+    cs.span = F.len;
+    n0 = 0;
+  } else {
+    cs.b_lo = 0;
+    nblk = F.B;
+    cs.span = min(rows + F.q - 1, F.len - i0);
+    n0 = i0;
+  }
+  cs.ok = nblk * cs.span <= cap;
+  if (!cs.ok) return cs;
+  for (int t = threadIdx.x; t < nblk * cs.span; t += blockDim.x) {
+    const int bb = t / cs.span, n = n0 + (t - bb * cs.span);
+    const int b = cs.b_lo + bb;
+    float2 v;
+    if (b < F.J) {
+      v = __ldg(sp + (long long)n * F.s_n + (long long)b * F.s_j);
+      if (weighted) v = cmul(wcs[n], v);
+    } else {
+      const int fl = dagger_src(n, F.len);
+      v = cmul(wcs[n], cconj(__ldg(sp + (long long)fl * F.s_n + (long long)(b - F.J) * F.s_j)));
+    }
+    st[t] = v;
+  }
+  return cs;
+}
+
+// Chunk build from the staged sources (after a barrier): same values as build_chunk_big.
+template <int DP, int CS, int R>
+__device__ __forceinline__ void build_chunk_staged(float2* dst, const SvtFamily& F, const float2* st,
+                                                   const ChunkSources cs, const int* lofs,
+                                                   const float2* __restrict__ Dg, int i0, int rows, float inv_beta) {
+  const int d = F.d;
+  auto lift = [&](int r, int u) -> float2 {
+    if (F.wide) {
+      const int bt = lofs[i0 + r];
+      return cconj(st[((bt >> 16) - cs.b_lo) * cs.span + (bt & 0xffff) + u]);
+    }
+    const int bt = lofs[u];
+    return st[(bt >> 16) * cs.span + (bt & 0xffff) + r];
+  };
+  if (Dg && (d & 1) == 0 && (DP & 1) == 0 && (reinterpret_cast<uintptr_t>(Dg) & 15) == 0) {
+    // the chunk's duals are rows * d contiguous complex64: 16-byte loads, two
+    // elements each, all of a thread's loads (<= 4) in flight before the first use
+    constexpr int HP = DP / 2;                                  // element pairs per chunk row
+    constexpr int NP = (R * HP + kBuildThreads - 1) / kBuildThreads;  // pairs per thread
+    static_assert(NP <= 8, "pairs per thread");
+    const float4* d4 = reinterpret_cast<const float4*>(Dg + (long long)i0 * d);
+    float4 dd[NP];
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      const int t = threadIdx.x + q * kBuildThreads;
+      const int r = t / HP, u = 2 * (t - r * HP);
+      dd[q] = (t < R * HP && r < rows && u < d) ? __ldcg(d4 + ((long long)r * d + u) / 2) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      const int t = threadIdx.x + q * kBuildThreads;
+      if (t < R * HP) {
+        const int r = t / HP, u = 2 * (t - r * HP);
+        float2 v0 = make_float2(0.f, 0.f), v1 = v0;
+        if (r < rows && u < d) {
+          v0 = lift(r, u);
+          v1 = lift(r, u + 1);
+          v0.x = fmaf(dd[q].x, inv_beta, v0.x);
+          v0.y = fmaf(dd[q].y, inv_beta, v0.y);
+          v1.x = fmaf(dd[q].z, inv_beta, v1.x);
+          v1.y = fmaf(dd[q].w, inv_beta, v1.y);
+        }
+        dst[r * CS + u] = v0;
+        dst[r * CS + u + 1] = v1;
+      }
+    }
+    return;
+  }
+  constexpr int NB4 = 4;
+  for (int t0 = threadIdx.x; t0 < R * DP; t0 += NB4 * blockDim.x) {
+    float2 dd[NB4];
+#pragma unroll
+    for (int q = 0; q < NB4; ++q) {
+      const int t = t0 + q * blockDim.x;
+      const int r = t / DP, u = t - r * DP;
+      dd[q] = (Dg && t < R * DP && r < rows && u < d) ? __ldcg(Dg + (long long)(i0 + r) * d + u)
+                                                      : make_float2(0.f, 0.f);
+    }
+#pragma unroll
+    for (int q = 0; q < NB4; ++q) {
+      const int t = t0 + q * blockDim.x;
+      if (t < R * DP) {
+        const int r = t / DP, u = t - r * DP;
+        float2 v = make_float2(0.f, 0.f);
+        if (r < rows && u < d) {
+          v = lift(r, u);
+          v.x = fmaf(dd[q].x, inv_beta, v.x);
+          v.y = fmaf(dd[q].y, inv_beta, v.y);
+        }
+        dst[r * CS + u] = v;
+      }
+    }
+  }
+}
+
 // Yc = C B over all 512 threads: the k range is split in two halves (threads
 // 0-255 -> Yc, 256-511 -> Yc2), each half a 2 x NB register tile per thread
 // (2 + NB shared loads per 2 NB complex FMAs).  The caller sums the halves

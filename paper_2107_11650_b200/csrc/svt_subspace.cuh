@@ -826,6 +826,19 @@ __global__ void __launch_bounds__(kSubNT, MINB) svt_subspace_kernel(const SvtPar
     if (defl3 && d - nd_in < KB) project_defl(V);
   }
 
+  // large-d chunk build; the tensor variants have the split buffer Yc2 free
+  // during the passes and stage the chunk's lift sources there
+  auto build_big = [&](int i0, int rows) {
+    if constexpr (BIG && MMA) {
+      const ChunkSources cs = stage_chunk_sources(Yc2, R * KS, F, spg, wl, weighted, i0, rows);
+      if (cs.ok) {
+        __syncthreads();
+        build_chunk_staged<DP, CS, R>(C, F, Yc2, cs, lofs, Dg, i0, rows, prm.inv_beta);
+        return;
+      }
+    }
+    if constexpr (BIG) build_chunk_big<DP, CS, R>(C, F, spg, wl, weighted, lofs, Dg, i0, rows, prm.inv_beta);
+  };
   // mappings: Yc rows yi / X rows k0 + 32m, columns c + 16n
   const int yi = tid >> 4, c16 = tid & 15;
   int iters = warm ? prm.q_warm : prm.q_cold;
@@ -861,7 +874,7 @@ __global__ void __launch_bounds__(kSubNT, MINB) svt_subspace_kernel(const SvtPar
       if (stg) stage_d_wait();
       SUB_ACC(clk_wait);
       if (BIG && Dg && i0 + R < e) prefetch_l2(Dg + (long long)(i0 + R) * d, min(R, e - i0 - R) * d);
-      if (BIG) build_chunk_big<DP, CS, R>(C, F, spg, wl, weighted, lofs, Dg, i0, rows, prm.inv_beta);
+      if (BIG) build_big(i0, rows);
       else build_chunk<DP, CS, R>(C, wl, lofs, F, Dg ? X : nullptr, i0, rows, prm.inv_beta);
       __syncthreads();
       SUB_ACC(clk_build);
@@ -972,7 +985,7 @@ __global__ void __launch_bounds__(kSubNT, MINB) svt_subspace_kernel(const SvtPar
       const int rows = min(R, e - i0);
       if (stg) stage_d_wait();
       if (BIG && Dg && i0 + R < e) prefetch_l2(Dg + (long long)(i0 + R) * d, min(R, e - i0 - R) * d);
-      if (BIG) build_chunk_big<DP, CS, R>(C, F, spg, wl, weighted, lofs, Dg, i0, rows, prm.inv_beta);
+      if (BIG) build_big(i0, rows);
       else build_chunk<DP, CS, R>(C, wl, lofs, F, Dg ? X : nullptr, i0, rows, prm.inv_beta);
       __syncthreads();
       if (stg && i0 + R < e) stage_d_async(X, Dg, i0 + R, min(R, e - i0 - R), d);
