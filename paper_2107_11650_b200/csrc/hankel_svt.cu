@@ -390,13 +390,16 @@ bool launch_level(const SvtParams& prm, int total, cudaStream_t stream) {
   if (coloc && !L2 && KB1 == kSubspaceKB && svt_padded_dim(g.dmax) == 120 && g.dmin >= 72 && g.maxLen <= 0xffff) {
     const size_t smem = svt_subspace_smem_bytes(120, kSubspaceKB, 32, g.maxB, g.maxLen, g.maxE, true);
     if (2 * (smem + 1024) <= 228 * 1024)
-      return mma ? launch_sub_mma(120, true, pm, total, smem, stream)
+      return mma ? launch_sub_mma(120, kSubspaceKB, false, true, pm, total, smem, stream)
                  : launch_sub_big(120, false, prm, total, smem, stream);
   }
-  if (mma && !L2 && KB1 == kSubspaceKB && g.dmax <= 128) {
+  if (mma && g.dmax <= 128) {
+    // resident layout (one CTA per SM): Householder QR (the Cholesky QR only
+    // pays at 64 registers)
+    constexpr int KBm = L2 ? kSubspaceKB : KB1;
     const int dp = svt_padded_dim(g.dmax);
-    const size_t smem = svt_subspace_smem_bytes(dp, kSubspaceKB, 32, g.maxB, g.maxLen, g.maxE, false);
-    if (smem <= 227 * 1024 && launch_sub_mma(dp, false, pm, total, smem, stream)) return true;
+    const size_t smem = svt_subspace_smem_bytes(dp, KBm, 32, g.maxB, g.maxLen, g.maxE, false);
+    if (smem <= 227 * 1024 && launch_sub_mma(dp, KBm, L2, false, prm, total, smem, stream)) return true;
   }
   if (g.dmax > 128) {
     // large-d variant (spectra and adjoint not resident)

@@ -351,6 +351,7 @@ ParamPlan::ParamPlan(const ParamConfig& cfg, const double* y, const uint8_t* mas
       vdpe_ = dalloc_s<float2>((size_t)S * L * sd * sd, stream_);
       ndpe_ = dalloc_s<int>((size_t)S * L, stream_);
     }
+    if (d <= 128) ycpe_ = dalloc_s<float2>((size_t)S * L * e * kSubspaceKB, stream_);
     fallback_ = dalloc_s<int>((size_t)S * L, stream_);
     diag_ = dalloc_s<int>((size_t)S * L, stream_);
     SHLR_CUDA(cudaMemsetAsync(diag_, 0, sizeof(int) * S * L, stream_));
@@ -413,7 +414,7 @@ ParamPlan::~ParamPlan() {
   if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
   if (graph_) cudaGraphDestroy(graph_);
   void* bufs[] = {x0_, yk_, x_, xold_, r_, p_, bk_, hpe_, ximg_, hecho_, dg_, hpe0_, hecho0_, wcN_, twN_,
-                  dpe_, decho_, vpe_, vecho_, vspe_, vspe2_, z1pe_, vdpe_, ndpe_, fallback_, diag_, halt_, have_v_, ctl_, log_};
+                  dpe_, decho_, vpe_, vecho_, vspe_, vspe2_, ycpe_, z1pe_, vdpe_, ndpe_, fallback_, diag_, halt_, have_v_, ctl_, log_};
   for (void* b : bufs)
     if (b) cudaFreeAsync(b, stream_);
   if (ev0_) cudaEventDestroy(ev0_);
@@ -476,6 +477,7 @@ SvtParams ParamPlan::svt_params(bool pe) const {
     F.Vs = vspe_;
     F.fallback = fallback_;
     F.halt_div = L;
+    sp.ycache = ycpe_;
   } else {   // P_n: plain lift along echoes of (slice, PE row) (solvers.cpp:279-283)
     sp.mode = SVT_ADMM_PLAIN;
     sp.thresh = (float)(cfg_.lambda2 / cfg_.beta);

@@ -84,6 +84,7 @@ class ParamPlan {
   float2 *vpe_ = nullptr, *vecho_ = nullptr;    // full-solver eigenvector stores
   float2* vspe_ = nullptr;                      // subspace-solver block store (PE family)
   float2* vspe2_ = nullptr;                     // its level-2 store
+  float2* ycpe_ = nullptr;                      // Ahat V of the Rayleigh-Ritz pass (SvtParams::ycache)
   float2* z1pe_ = nullptr;                      // PE d > 128: Z1 of the deflated level 3
   float2* vdpe_ = nullptr;                      // PE d > 128: deflation chain bases
   int* ndpe_ = nullptr;                         // PE d > 128: deflated columns per matrix

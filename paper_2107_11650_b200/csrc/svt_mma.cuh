@@ -177,27 +177,30 @@ __device__ __forceinline__ void chunk_block_mma(const float2* C, const float2* B
   __syncthreads();
 }
 
-// Accumulators of a DP x 48 block product, 16 warps: warp w takes the 16-row
-// tile w >> 1 and three 8-column tiles (tile index 3 (w & 1) + j: the two
-// tiles of a 16-column group hold its columns 4 a + b + 2 sub).  Rows at or
-// beyond DP are computed from whatever follows in shared memory and never
-// stored (an MMA output row depends on its own A row only).
+// Accumulators of a DP x KB block product (KB = 48 or 32), 16 warps: warp w
+// takes the 16-row tile w >> 1 and NTW = KB / 16 8-column tiles (tile index
+// NTW (w & 1) + j: the two tiles of a 16-column group hold its columns
+// 4 a + b + 2 sub).  Rows at or beyond DP are computed from whatever follows
+// in shared memory and never stored (an MMA output row depends on its own A
+// row only).
+template <int NTW>
 struct XAccMma {
-  float xr[3][4], xi[3][4];
+  float xr[NTW][4], xi[NTW][4];
   __device__ __forceinline__ void zero() {
 #pragma unroll
-    for (int j = 0; j < 3; ++j)
+    for (int j = 0; j < NTW; ++j)
 #pragma unroll
       for (int i = 0; i < 4; ++i) xr[j][i] = xi[j][i] = 0.f;
   }
 };
-// first physical column of tile tl (0..5) in the stride-1 scheme
+// first physical column of tile tl in the stride-1 scheme
 __device__ __forceinline__ int tile_col_s1(int tl) { return 16 * (tl >> 1) + 2 * (tl & 1); }
 
-// X (DP x 48) += C^H Yc over one chunk of R = 32 rows.
+// X (DP x KB) += C^H Yc over one chunk of R = 32 rows.
 template <int CS, int KS>
-__device__ __forceinline__ void xacc_mma(XAccMma& x, const float2* C, const float2* Yc) {
+__device__ __forceinline__ void xacc_mma(XAccMma<(KS - 1) / 16>& x, const float2* C, const float2* Yc) {
   static_assert(KS % 16 == 1 && (CS % 16 == 9 || CS % 16 == 1), "fragment permutations assume these strides");
+  constexpr int NTW = (KS - 1) / 16;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int pg = perm_s1(g);
@@ -212,8 +215,8 @@ __device__ __forceinline__ void xacc_mma(XAccMma& x, const float2* C, const floa
     a.set(2, ccol[(i0 + 4) * CS]);
     a.set(3, ccol[(i0 + 4) * CS + 2]);
 #pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      const int cb = tile_col_s1(3 * (w & 1) + j);
+    for (int j = 0; j < NTW; ++j) {
+      const int cb = tile_col_s1(NTW * (w & 1) + j);
       CFragB b;
       b.set(0, ycol[i0 * KS + cb]);
       b.set(1, ycol[(i0 + 4) * KS + cb]);
@@ -224,13 +227,14 @@ __device__ __forceinline__ void xacc_mma(XAccMma& x, const float2* C, const floa
 
 // Stores the accumulators; perm (optional) maps a column to its destination.
 template <int DP, int KS>
-__device__ __forceinline__ void xacc_store_perm(const XAccMma& x, float2* X, const int* perm) {
+__device__ __forceinline__ void xacc_store_perm(const XAccMma<(KS - 1) / 16>& x, float2* X, const int* perm) {
+  constexpr int NTW = (KS - 1) / 16;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int m0 = 16 * (w >> 1) + perm_s1(g);
 #pragma unroll
-  for (int j = 0; j < 3; ++j) {
-    const int cb = tile_col_s1(3 * (w & 1) + j);
+  for (int j = 0; j < NTW; ++j) {
+    const int cb = tile_col_s1(NTW * (w & 1) + j);
     int c0 = cb + perm_s1(2 * t), c1 = cb + perm_s1(2 * t + 1);
     if (perm) {
       c0 = perm[c0];
@@ -247,14 +251,15 @@ __device__ __forceinline__ void xacc_store_perm(const XAccMma& x, float2* X, con
   }
 }
 template <int DP, int KS>
-__device__ __forceinline__ void xacc_store(const XAccMma& x, float2* X) {
+__device__ __forceinline__ void xacc_store(const XAccMma<(KS - 1) / 16>& x, float2* X) {
   xacc_store_perm<DP, KS>(x, X, nullptr);
 }
 
-// acc (DP x 48) = V M: V a DP x KS block, M a 48 x KS matrix (KB = 48).
+// acc (DP x KB) = V M: V a DP x KS block, M a KB x KS matrix.
 template <int KS, int KB>
-__device__ __forceinline__ void vu_mma(XAccMma& x, const float2* V, const float2* U) {
-  static_assert(KB == 48 && KS % 16 == 1, "48-column block");
+__device__ __forceinline__ void vu_mma(XAccMma<KB / 16>& x, const float2* V, const float2* U) {
+  static_assert((KB == 48 || KB == 32) && KS == KB + 1, "32- or 48-column block");
+  constexpr int NTW = KB / 16;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int pg = perm_s1(g);
@@ -269,8 +274,8 @@ __device__ __forceinline__ void vu_mma(XAccMma& x, const float2* V, const float2
     a.set(2, arow[k0 + 4]);
     a.set(3, arow[2 * KS + k0 + 4]);
 #pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      const int cb = tile_col_s1(3 * (w & 1) + j);
+    for (int j = 0; j < NTW; ++j) {
+      const int cb = tile_col_s1(NTW * (w & 1) + j);
       CFragB b;
       b.set(0, bcol[k0 * KS + cb]);
       b.set(1, bcol[(k0 + 4) * KS + cb]);
@@ -287,21 +292,30 @@ struct HAccMma {
   CAcc8 acc;
   __device__ __forceinline__ void zero() { acc.zero(); }
 };
-__device__ __forceinline__ void sym_tile(int w, int& mt, int& grp, int& sub) {
+// tile w of the upper block triangle of an NBK x NBK grid of 16 x 16 blocks
+// (NBK = 3: 12 tiles, NBK = 2: 6 tiles); false beyond the last tile
+template <int NBK>
+__device__ __forceinline__ bool sym_tile(int w, int& mt, int& grp, int& sub) {
+  static_assert(NBK == 2 || NBK == 3, "32- or 48-column block");
   const int bi = w >> 1;
   sub = w & 1;
-  mt = bi < 3 ? 0 : bi < 5 ? 1 : 2;
-  grp = bi < 3 ? bi : bi < 5 ? bi - 2 : 2;
+  if (NBK == 3) {
+    mt = bi < 3 ? 0 : bi < 5 ? 1 : 2;
+    grp = bi < 3 ? bi : bi < 5 ? bi - 2 : 2;
+    return w < 12;
+  }
+  mt = bi < 2 ? 0 : 1;
+  grp = bi < 2 ? bi : 1;
+  return w < 6;
 }
 
 template <int KS>
 __device__ __forceinline__ void hacc_mma(HAccMma& h, const float2* Y, int ksteps = 4) {
   static_assert(KS % 16 == 1, "fragment permutations assume this stride");
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (w >= 12) return;
   const int g = lane >> 2, t = lane & 3;
   int mt, grp, sub;
-  sym_tile(w, mt, grp, sub);
+  if (!sym_tile<(KS - 1) / 16>(w, mt, grp, sub)) return;
   const int pg = perm_s1(g);
   const float2* acol = Y + t * KS + 16 * mt + pg;
   const float2* bcol = Y + t * KS + 16 * grp + 2 * sub + pg;
@@ -323,10 +337,9 @@ __device__ __forceinline__ void hacc_mma(HAccMma& h, const float2* Y, int ksteps
 template <int KS>
 __device__ __forceinline__ void hacc_store(const HAccMma& h, float2* Hm) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (w >= 12) return;
   const int g = lane >> 2, t = lane & 3;
   int mt, grp, sub;
-  sym_tile(w, mt, grp, sub);
+  if (!sym_tile<(KS - 1) / 16>(w, mt, grp, sub)) return;
   float2* out = Hm + (16 * mt + perm_s1(g)) * KS + 16 * grp + 2 * sub;
   const int c0 = perm_s1(2 * t), c1 = perm_s1(2 * t + 1);
   out[c0] = h.acc.get(0);
@@ -407,7 +420,7 @@ __device__ __forceinline__ void ycache_rotate_mma(float2* Yc, const float2* Us, 
     const float2* arow = Yc + (16 * mt + pg) * KS + t;
     const float2* bcol = Us + t * US + tile_col_s1(tl) + pg;
 #pragma unroll 2
-    for (int s = 0; s < 6; ++s) {
+    for (int s = 0; s < (KS - 1) / 8; ++s) {
       const int k0 = 8 * s;
       CFragA a;
       a.set(0, arow[k0]);
@@ -457,7 +470,7 @@ __device__ __forceinline__ void gram_sym_mma(const float2* B, float2* Sm, int ks
 // scratch; red: 32 floats of scratch.  Called by the whole CTA.
 template <int KB, int KS, int DP>
 __device__ int newton_schulz_orth(const float2* X, float2* V, float2* Sm, float* red) {
-  static_assert(KB == 48, "48-column block");
+  static_assert(KB == 48 || KB == 32, "32- or 48-column block");
   constexpr int NT = 512, PER = (KB * KB + NT - 1) / NT;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const float2* B = X;
@@ -507,7 +520,7 @@ __device__ int newton_schulz_orth(const float2* X, float2* V, float2* Sm, float*
       }
     }
     __syncthreads();
-    XAccMma acc;
+    XAccMma<KB / 16> acc;
     acc.zero();
     vu_mma<KS, KB>(acc, B, Sm);
     __syncthreads();  // in place: all reads of B are done
@@ -538,7 +551,7 @@ __device__ int newton_schulz_orth(const float2* X, float2* V, float2* Sm, float*
 template <int KB, int KS, int DP>
 __device__ int cholesky_qr_mma(const float2* X, float2* V, float2* Sm, float2* Mb, float* dinv, int* flag,
                                float pivtol) {
-  static_assert(KB == 48, "48-column block");
+  static_assert(KB == 48 || KB == 32, "32- or 48-column block");
   constexpr int NT = 512, PER = (KB * KB + NT - 1) / NT;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   gram_sym_mma<KS>(X, Sm, DP / 8);
@@ -632,7 +645,7 @@ __device__ int cholesky_qr_mma(const float2* X, float2* V, float2* Sm, float2* M
     Mb[j * KS + i] = cscale(cconj(Mb[j * KS + i]), dinv[j]);
   }
   __syncthreads();
-  XAccMma acc;
+  XAccMma<KB / 16> acc;
   acc.zero();
   vu_mma<KS, KB>(acc, X, Mb);
   __syncthreads();  // all reads of X and of Mb (which may alias V) are done

@@ -664,8 +664,8 @@ __global__ void __launch_bounds__(kSubNT, MINB) svt_subspace_kernel(const SvtPar
                 "block size of the level");
   constexpr bool NOSPLIT = BIG && L2 && !HUGE;
   // MMA: the chunk contractions run as 3xTF32 on the tensor cores (svt_mma.cuh)
-  static_assert(!MMA || (R == 32 && KB == 48 && !NOSPLIT && !HUGE && DP <= 128 && DP % 8 == 0),
-                "the mma.sync mappings cover 48-column blocks with d <= 128");
+  static_assert(!MMA || (R == 32 && (KB == 48 || KB == 32) && !NOSPLIT && !HUGE && DP <= 128 && DP % 8 == 0),
+                "the mma.sync mappings cover 32- and 48-column blocks with d <= 128");
   static_assert(KB % 16 == 0 && KB % 8 == 0, "KB must be a multiple of 16");
   static_assert(R == 32 || HUGE, "the thread mappings assume 32-row chunks (HUGE: 16)");
   // Ritz pairs one deflation step keeps, and the margin below the block edge
@@ -857,7 +857,7 @@ __global__ void __launch_bounds__(kSubNT, MINB) svt_subspace_kernel(const SvtPar
   // overlaps the GEMMs of chunk c.
   for (int it = 0; it < iters; ++it) {
     float2 xa[MMA ? 1 : MR][MMA ? 1 : NC];
-    XAccMma xm;
+    XAccMma<KB / 16> xm;
     if constexpr (MMA) {
       xm.zero();
     } else {
@@ -1103,7 +1103,7 @@ __global__ void __launch_bounds__(kSubNT, MINB) svt_subspace_kernel(const SvtPar
   __syncthreads();
   // V <- V U (Ritz vectors, sorted) into X
   if constexpr (MMA) {
-    XAccMma vm;
+    XAccMma<KB / 16> vm;
     vm.zero();
     vu_mma<KS, KB>(vm, V, C);
     if (BIG) __syncthreads();  // in place: all reads of V are done
@@ -1208,20 +1208,22 @@ __global__ void __launch_bounds__(kSubNT, MINB) svt_subspace_kernel(const SvtPar
   // Rayleigh-Ritz pass's Ahat V (ycg) and the rotation U (sorted, scaled by
   // the shrink factors) instead of rebuilding the chunk and multiplying by Vf
   constexpr int US = 32;  // row stride of the scaled rotation (its first 16 nb <= 32 sorted columns)
-  constexpr bool CACHE_OK = MMA && (BIG || DP * KS - R * DP >= KB * US);
+  constexpr bool CACHE_OK = MMA;
+  static_assert(!MMA || R * KS >= KB * US, "the scaled rotation fits the split buffer");
   const bool cached = CACHE_OK && ycg != nullptr && r <= 32;
-  float2* Us = BIG ? Yc2 : V + R * DP;  // BIG: the idle split buffer; else behind the staged duals
+  float2* Us = Yc2;  // the split-k buffer the tensor path does not use
   const int nbz = (r + 15) >> 4;
-  float2 ypre[3];
+  constexpr int YPT = MMA ? R * KB / kSubNT : 1;  // cached elements per thread
+  float2 ypre[YPT];
   auto ycache_fetch = [&](int i0) {
 #pragma unroll
-    for (int q = 0; q < 3; ++q) {
+    for (int q = 0; q < YPT; ++q) {
       const int t = tid + NT * q, i = t / KB, j = t - i * KB;
       ypre[q] = (i0 + i < e) ? __ldcg(ycg + (long long)(i0 + i) * KB + j) : make_float2(0.f, 0.f);
     }
   };
   if (cached) {
-    static_assert(!MMA || R * KB == 3 * kSubNT, "three cached elements per thread");
+    static_assert(!MMA || R * KB == YPT * kSubNT, "whole cached elements per thread");
     for (int t = tid; t < KB * KB; t += NT) {
       const int j = t / KB, c = t - j * KB;
       const int pc = perm[c];
@@ -1235,7 +1237,7 @@ __global__ void __launch_bounds__(kSubNT, MINB) svt_subspace_kernel(const SvtPar
     const int rows = min(R, e - i0);
     if (cached) {  // Yc is free (the previous chunk's Z GEMM is behind a barrier)
 #pragma unroll
-      for (int q = 0; q < 3; ++q) {
+      for (int q = 0; q < YPT; ++q) {
         const int t = tid + NT * q, i = t / KB, j = t - i * KB;
         Yc[i * KS + j] = ypre[q];
       }
@@ -1261,8 +1263,8 @@ __global__ void __launch_bounds__(kSubNT, MINB) svt_subspace_kernel(const SvtPar
       if constexpr (HUGE) chunk_block_huge<CS, KS, R>(C, Vf, Yc, d, min(KB, 16 * nb), S.f);
       else if constexpr (MMA) {
         if (nb <= 1) chunk_block_mma<CS, KS, 1, R>(C, Vf, Yc, Yc2, d, S.f);
-        else if (nb == 2) chunk_block_mma<CS, KS, 2, R>(C, Vf, Yc, Yc2, d, S.f);
-        else chunk_block_mma<CS, KS, 3, R>(C, Vf, Yc, Yc2, d, S.f);
+        else if (nb == 2 || NC == 2) chunk_block_mma<CS, KS, 2, R>(C, Vf, Yc, Yc2, d, S.f);
+        else chunk_block_mma<CS, KS, (NC >= 3 ? 3 : 2), R>(C, Vf, Yc, Yc2, d, S.f);
       }
       else if (nb <= 1) chunk_block<CS, KS, 1, R, NOSPLIT>(C, Vf, Yc, Yc2, d, S.f);
       else if (nb == 2 || NC == 2) chunk_block<CS, KS, (NC >= 2 ? 2 : 1), R, NOSPLIT>(C, Vf, Yc, Yc2, d, S.f);

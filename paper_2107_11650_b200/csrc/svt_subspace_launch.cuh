@@ -15,7 +15,8 @@ bool launch_sub_small(int dp, int kb, bool l2, const SvtParams& prm, int total, 
 bool launch_sub_big(int dp, bool l2, const SvtParams& prm, int total, size_t smem, cudaStream_t stream);
 // 3xTF32 tensor-core contractions (svt_sub_mma.cu): level 1 with 48 columns;
 // coloc = the co-located large-d layout (d = 120, two CTAs per SM)
-bool launch_sub_mma(int dp, bool coloc, const SvtParams& prm, int total, size_t smem, cudaStream_t stream);
+bool launch_sub_mma(int dp, int kb, bool l2, bool coloc, const SvtParams& prm, int total, size_t smem,
+                    cudaStream_t stream);
 // 248 < d <= 496 (svt_sub_huge.cu): DP in {320, 384, 496}; KB 32, 16-row chunks;
 // l2 = the deflation-chain launches
 bool launch_sub_huge(int dp, bool l2, const SvtParams& prm, int total, size_t smem, cudaStream_t stream);
