@@ -113,6 +113,13 @@ int shlr_cuda_pi_plan_set_warm_start(shlr_pi_plan* plan, int on);
 /* Diagnostics: Jacobi sweeps (stage1 * 100 + stage2) per matrix of the last
  * Hankel-SVT launch, rows first then columns; n = m + n entries. */
 int shlr_cuda_pi_plan_debug_sweeps(shlr_pi_plan* plan, int* out, int n);
+/* Diagnostics: the solver level each lifted matrix ended the last outer
+ * iteration at, rows first then columns; n = m + n entries.  0: level 1;
+ * 1: handed to the next level and redone there; 2: beyond the last level's
+ * block (d > 128 without a deflation buffer: reported on download); 3: kept
+ * at level 2; 4 / 5: large d, solved by the deflation chain (4 only while a
+ * chain is in flight). */
+int shlr_cuda_pi_plan_debug_levels(shlr_pi_plan* plan, int* out, int n);
 /* Diagnostics: per-matrix clock64 stamps of the subspace solver's phases
  * (8 per matrix) of the last launch; zeros unless SHLR_PHASE_CLK was set in
  * the environment when the plan was created. */

@@ -83,6 +83,7 @@ PROTOTYPES = {
     "shlr_cuda_pi_plan_set_timing": (C.c_int, [C.c_void_p, C.c_int]),
     "shlr_cuda_pi_plan_set_warm_start": (C.c_int, [C.c_void_p, C.c_int]),
     "shlr_cuda_pi_plan_debug_sweeps": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.c_int]),
+    "shlr_cuda_pi_plan_debug_levels": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.c_int]),
     "shlr_cuda_pi_plan_debug_phases": (C.c_int, [C.c_void_p, C.POINTER(C.c_longlong), C.c_int]),
     "shlr_cuda_param_reconstruct": (C.c_int, [C.POINTER(ShlrParamArgs), C.POINTER(C.c_double),
                                               C.POINTER(ShlrStats), LOG_FN, C.c_void_p]),

@@ -296,6 +296,15 @@ class PiPlan:
                "plan_debug_sweeps")
         return out
 
+    def debug_levels(self) -> np.ndarray:
+        """Solver level of each lifted matrix after the last outer iteration
+        (shlr_cuda_pi_plan_debug_levels: 0 level 1 ... 5 deflation chain)."""
+        n = self.shape[0] + self.shape[1]
+        out = np.zeros(n, np.int32)
+        _check(lib.shlr_cuda_pi_plan_debug_levels(self._h, out.ctypes.data_as(C.POINTER(C.c_int)), n),
+               "plan_debug_levels")
+        return out
+
     def timing(self):
         s, t, n = C.c_double(), C.c_double(), C.c_int()
         _check(lib.shlr_cuda_pi_plan_timing(self._h, C.byref(s), C.byref(t), C.byref(n)), "timing")

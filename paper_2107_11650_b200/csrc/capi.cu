@@ -278,6 +278,14 @@ int shlr_cuda_pi_plan_debug_sweeps(shlr_pi_plan* plan, int* out, int n) {
   });
 }
 
+int shlr_cuda_pi_plan_debug_levels(shlr_pi_plan* plan, int* out, int n) {
+  return guarded([&] {
+    if (!plan || !out) throw shlr_b200::InvalidArg("null plan/output");
+    plan->impl->debug_levels(out, n);
+    return SHLR_OK;
+  });
+}
+
 int shlr_cuda_pi_plan_set_timing(shlr_pi_plan* plan, int on) {
   return guarded([&] {
     if (!plan) throw shlr_b200::InvalidArg("null plan");

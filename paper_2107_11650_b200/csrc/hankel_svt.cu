@@ -393,6 +393,17 @@ bool launch_level(const SvtParams& prm, int total, cudaStream_t stream) {
       return mma ? launch_sub_mma(120, kSubspaceKB, false, true, pm, total, smem, stream)
                  : launch_sub_big(120, false, prm, total, smem, stream);
   }
+  // the parameter path's PE lifts (config 4: 244 x 104, 32-column level 1): same layout, tensor variant only
+  static const bool coloc_pe = std::getenv("SHLR_NO_COLOC_PE") == nullptr;
+  if (coloc && coloc_pe && mma && !L2 && KB1 == kSubspaceKB1 && svt_padded_dim(g.dmax) == 104 && g.dmin >= 72 &&
+      g.maxLen <= 0xffff) {
+    bool vc_ok = true;  // (plain lifts have no virtual coils in the large-d layout)
+    for (int f = 0; f < prm.nfam; ++f) vc_ok = vc_ok && !(prm.fam[f].vc && prm.mode != SVT_ADMM_WEIGHTED);
+    const size_t smem = svt_subspace_smem_bytes(104, kSubspaceKB1, 32, g.maxB, g.maxLen, g.maxE, true);
+    if (vc_ok && 2 * (smem + 1024) <= 228 * 1024 &&
+        launch_sub_mma(104, kSubspaceKB1, false, true, pm, total, smem, stream))
+      return true;
+  }
   if (mma && g.dmax <= 128) {
     // resident layout (one CTA per SM): Householder QR (the Cholesky QR only
     // pays at 64 registers)

@@ -1543,6 +1543,14 @@ void PiPlan::debug_sweeps(int* out, int n) {
   for (int i = 0; i < std::min(n, total); ++i) out[i] = h[i];
 }
 
+void PiPlan::debug_levels(int* out, int n) {
+  const int total = cfg_.M + cfg_.N;
+  std::vector<int> h(total);
+  SHLR_CUDA(cudaMemcpyAsync(h.data(), fallback_, total * sizeof(int), cudaMemcpyDeviceToHost, stream_));
+  SHLR_CUDA(cudaStreamSynchronize(stream_));
+  for (int i = 0; i < std::min(n, total); ++i) out[i] = h[i];
+}
+
 void fft_along_axis_host(double* data, const size_t* dims, int ndim, int axis, bool inverse) {
   if (axis < 0 || axis >= ndim) throw InvalidArg("fft_along_axis: axis out of range");
   size_t outer = 1, inner = 1, total = 1;

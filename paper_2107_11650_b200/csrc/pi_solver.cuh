@@ -60,6 +60,7 @@ class PiPlan {
   void set_warm_start(bool on) { warm_start_ = on; }
   // per-matrix Jacobi sweeps (stage1 * 100 + stage2) of the last SVT launch
   void debug_sweeps(int* out, int n);
+  void debug_levels(int* out, int n);
   // subspace-solver phase clocks of the last SVT launch (8 per matrix; needs
   // SHLR_PHASE_CLK in the environment at plan creation)
   void debug_phases(long long* out, int n);

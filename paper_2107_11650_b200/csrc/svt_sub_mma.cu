@@ -9,10 +9,17 @@ namespace shlr_b200 {
 
 bool launch_sub_mma(int dp, int kb, bool l2, bool coloc, const SvtParams& prm, int total, size_t smem,
                     cudaStream_t stream) {
-  if (coloc) {
-    if (dp != 120 || kb != kSubspaceKB || l2) return false;
-    launch_sub<120, kSubspaceKB, true, false, 2, true>(prm, total, smem, stream);
-    return true;
+  if (coloc) {  // the large-d layout, two CTAs per SM
+    if (l2) return false;
+    if (dp == 120 && kb == kSubspaceKB) {
+      launch_sub<120, kSubspaceKB, true, false, 2, true>(prm, total, smem, stream);
+      return true;
+    }
+    if (dp == 104 && kb == kSubspaceKB1) {
+      launch_sub<104, kSubspaceKB1, true, false, 2, true>(prm, total, smem, stream);
+      return true;
+    }
+    return false;
   }
   if (dp == 120 && kb == kSubspaceKB && !l2) {
     launch_sub<120, kSubspaceKB, false, false, 1, true>(prm, total, smem, stream);

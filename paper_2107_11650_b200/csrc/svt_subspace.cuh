@@ -655,13 +655,19 @@ __global__ void __launch_bounds__(kSubNT, MINB) svt_subspace_kernel(const SvtPar
   constexpr bool HUGE = BIG && R == 16;
   // SMALLD (40 <= d < 72): 16-column level 1, 32-column level 2
   constexpr bool SMALLD = !BIG && DP < 72;
-  constexpr int KB1 = HUGE ? kSubspaceKBHuge : BIG ? kSubspaceKB : SMALLD ? kSubspaceKBSmall : (L2 ? kSubspaceKB1 : KB);
-  constexpr int KB2 = HUGE ? kSubspaceKBHuge : BIG ? kSubspaceKBBig : SMALLD ? kSubspaceKB1 : kSubspaceKB;
+  // COLOC: the large-d *layout* used at d <= 128 so that two CTAs share an SM
+  // (MINB = 2); its levels are those of d <= 128 (level 2 and the full solver
+  // behind it run in the resident layout)
+  constexpr bool COLOC = BIG && MINB == 2;
+  constexpr bool BIGLV = BIG && !COLOC;
+  constexpr int KB1 = HUGE ? kSubspaceKBHuge : BIGLV ? kSubspaceKB : SMALLD ? kSubspaceKBSmall : (L2 ? kSubspaceKB1 : KB);
+  constexpr int KB2 = HUGE ? kSubspaceKBHuge : BIGLV ? kSubspaceKBBig : SMALLD ? kSubspaceKB1 : kSubspaceKB;
   static_assert(HUGE     ? KB == kSubspaceKBHuge
                 : SMALLD ? KB == (L2 ? KB2 : KB1)
                 : L2     ? KB == KB2
-                         : (BIG ? KB == kSubspaceKB : (KB == kSubspaceKB1 || KB == kSubspaceKB)),
+                         : (BIGLV ? KB == kSubspaceKB : (KB == kSubspaceKB1 || KB == kSubspaceKB)),
                 "block size of the level");
+  static_assert(!COLOC || !L2, "the co-located layout is a level-1 variant");
   constexpr bool NOSPLIT = BIG && L2 && !HUGE;
   // MMA: the chunk contractions run as 3xTF32 on the tensor cores (svt_mma.cuh)
   static_assert(!MMA || (R == 32 && (KB == 48 || KB == 32) && !NOSPLIT && !HUGE && DP <= 128 && DP % 8 == 0),

@@ -1,0 +1,13 @@
+set -u
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_param.py tests/test_gpu_large_d.py -m gpu -q > gpurun_out/pc.test.log 2>&1; echo "test rc=$?"
+tail -3 gpurun_out/pc.test.log
+timeout 900 python bench.py --no-cpu --no-e2e > gpurun_out/pc_bench.json 2> gpurun_out/pc_bench.err; echo "bench rc=$?"
+python - <<P
+import json
+l=[x for x in open('gpurun_out/pc_bench.json') if x.startswith('{')]
+d=json.loads(l[-1])
+print(d['value'], d['ms_per_step'], d['roofline']['frac'], d['hankel_svt']['kernel_ms'])
+for k,v in d.get('other_workloads',{}).items():
+    print('  ', k, v.get('value'), v.get('ms_per_step'), v.get('svt_ms'))
+P
