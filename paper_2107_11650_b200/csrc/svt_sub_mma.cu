@@ -25,6 +25,10 @@ bool launch_sub_mma(int dp, int kb, bool l2, bool coloc, const SvtParams& prm, i
     launch_sub<120, kSubspaceKB, false, false, 1, true>(prm, total, smem, stream);
     return true;
   }
+  if (dp == 72 && kb == kSubspaceKB && !l2) {
+    launch_sub<72, kSubspaceKB, false, false, 1, true>(prm, total, smem, stream);
+    return true;
+  }
   if (dp == 104 && kb == kSubspaceKB1 && !l2) {
     launch_sub<104, kSubspaceKB1, false, false, 1, true>(prm, total, smem, stream);
     return true;

@@ -668,6 +668,11 @@ __global__ void __launch_bounds__(kSubNT, MINB) svt_subspace_kernel(const SvtPar
                          : (BIGLV ? KB == kSubspaceKB : (KB == kSubspaceKB1 || KB == kSubspaceKB)),
                 "block size of the level");
   static_assert(!COLOC || !L2, "the co-located layout is a level-1 variant");
+  // the chunk buffer doubles as the eigen-solver's work area (3 KB^2 floats)
+  // and the Cholesky QR's Gram matrix (KB x KS); in the large-d layout the
+  // Rayleigh-Ritz matrix sits right behind it (d = 72 with a 48-column block
+  // does not fit: config 1 stays in the resident layout)
+  static_assert(!COLOC || (2 * R * CS >= 3 * KB * KB && R * CS >= KB * KS), "chunk buffer too small for this block");
   constexpr bool NOSPLIT = BIG && L2 && !HUGE;
   // MMA: the chunk contractions run as 3xTF32 on the tensor cores (svt_mma.cuh)
   static_assert(!MMA || (R == 32 && (KB == 48 || KB == 32) && !NOSPLIT && !HUGE && DP <= 128 && DP % 8 == 0),

@@ -42,12 +42,51 @@ def make_inputs():
     return y, bits
 
 
+ITERS50 = (30, 40, 45, 50)
+COILS50 = (0, 18)
+
+
+def pack50(d: str) -> None:
+    """The 50-iteration run (round 2): the reference's images after iterations
+    30, 40, 45 and 50 (two coils as complex64 + the root-sum-of-squares image
+    as float32, whichever dumps exist in DIR) and its log.  From iteration ~38
+    on more than 62 singular values per lifted matrix exceed the threshold,
+    which is where the B200 path's deflation chain (level 3) takes over.
+
+        oracle/_ref/ref_driver pi y=DIR/y.cplx mask=DIR/m.cplx out=DIR/ref50 vc=1 pencil=246 \
+            max_outer=50 tol=1e-300 x_iters=10,20,30,38,40,42,45,50 time=1     (~5 h on one core)
+        python tests/golden/make_c3_golden.py pack50 DIR
+    """
+    out = {"coils": np.array(COILS50)}
+    its = []
+    for it in ITERS50:
+        f = os.path.join(d, f"ref50.x{it}.cplx")
+        if not os.path.exists(f):
+            continue
+        x = io.read_cplx(f)
+        out[f"x{it}_coils"] = x[:, :, list(COILS50)].astype(np.complex64)
+        out[f"rss{it}"] = np.sqrt((np.abs(x) ** 2).sum(axis=2)).astype(np.float32)
+        its.append(it)
+    out["iters"] = np.array(its)
+    logf = os.path.join(d, "ref50.log")
+    if os.path.exists(logf) and os.path.getsize(logf) > 0:
+        log = open(logf).read().splitlines()
+        out["log"] = np.array(log)
+        out["relchange"] = np.array([float(re.match(r"iter=\d+ relchange=(\S+)", ln).group(1)) for ln in log])
+    dst = os.path.join(os.path.dirname(os.path.abspath(__file__)), "c3_ref50.npz")
+    np.savez_compressed(dst, **out)
+    print(dst, os.path.getsize(dst), "iterations", its)
+
+
 def main(cmd: str, d: str) -> None:
     if cmd == "inputs":
         os.makedirs(d, exist_ok=True)
         y, bits = make_inputs()
         io.write_cplx(y, os.path.join(d, "y.cplx"))
         io.write_mask(bits, os.path.join(d, "m.cplx"))
+        return
+    if cmd == "pack50":
+        pack50(d)
         return
     x = io.read_cplx(os.path.join(d, "ref30.x.cplx"))
     log = open(os.path.join(d, "ref30.log")).read().splitlines()
