@@ -157,6 +157,34 @@ __global__ void k_spirit_pmat(const float2* __restrict__ maps, int npix, int J,
   }
 }
 
+// Packed Hermitian P for the 8-coil column stage (k_spirit_cols_bulk): P is
+// Hermitian, so a pixel keeps the 36 entries E[s][a] = P[a][(a + s) mod 8]
+// (s = 0..3: a = 0..7; s = 4: a = 0..3) -- 288 B instead of 512 -- and the
+// pixels of one image column are contiguous ([n][k][36]) so that a CTA's
+// whole column of P (M x 288 B) arrives by a handful of bulk copies.
+constexpr int kPackedP = 36;
+__global__ void k_spirit_pmat_packed8(const float2* __restrict__ maps, int M, int N, float2* __restrict__ pk) {
+  constexpr int J = 8, JJ = 64;
+  const size_t total = (size_t)M * N * kPackedP;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const int e = (int)(t % kPackedP);
+    const size_t pix = t / kPackedP;  // n * M + k
+    const int n = (int)(pix / M), k = (int)(pix % M);
+    const int sft = e >> 3, a = e & 7, b = (a + sft) & 7;
+    const float2* mp = maps + ((size_t)k * N + n) * JJ;
+    float2 acc = make_float2(0.f, 0.f);
+    for (int dst = 0; dst < J; ++dst) {
+      float2 ga = mp[a * J + dst];
+      float2 gb = mp[b * J + dst];
+      if (dst == a) ga.x -= 1.f;
+      if (dst == b) gb.x -= 1.f;
+      cfmac(acc, ga, gb);  // conj(Gm1[dst][a]) * Gm1[dst][b]
+    }
+    pk[t] = acc;
+  }
+}
+
 // ------------------------------------------------------------ FFT ops
 struct CopyOpCtl {
   const float2* in;
@@ -539,6 +567,100 @@ __global__ void __launch_bounds__(kFftThreads) k_spirit_cols(const float2* __res
   extern __shared__ float2 sm[];
   if (halted(ctl) || (!for_x && ctl->cg.done)) return;
   spirit_col_tile(tmp, tmp2, pm, tw, N, J, PPT, blockIdx.x * PPT, sm);
+}
+
+// ---- 8-coil column stage with the column's packed P prefetched by bulk copies
+// (cp.async.bulk -> shared memory, completion on an mbarrier): the copies are
+// issued before the column is even loaded, so P's L2 / HBM latency -- which
+// bounded k_spirit_cols (256 scattered 512-byte segments per CTA, read after
+// the inverse FFT) -- hides under the load and the inverse FFT.
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "W_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra W_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// smem: a, b (M x 8 float2 each), the packed P column (M x 36 float2), the mbarrier.
+__global__ void __launch_bounds__(kFftThreads, 2) k_spirit_cols_bulk(const float2* __restrict__ tmp,
+                                                                    float2* __restrict__ tmp2,
+                                                                    const float2* __restrict__ pk, FftTwiddles tw,
+                                                                    int N, const SolverCtl* ctl, int for_x) {
+  extern __shared__ float2 sm[];
+  if (halted(ctl) || (!for_x && ctl->cg.done)) return;
+  constexpr int J = 8;
+  const int M = tw.n, n0 = blockIdx.x;
+  const long long NJ = (long long)N * J;
+  float2* a = sm;
+  float2* b = sm + (size_t)M * J;
+  float2* ps = b + (size_t)M * J;
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(ps + (size_t)M * kPackedP);
+  if (threadIdx.x == 0) mbar_init(bar, 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned bytes = (unsigned)M * kPackedP * (unsigned)sizeof(float2);
+    mbar_expect_tx(bar, bytes);
+    const char* src = reinterpret_cast<const char*>(pk + (size_t)n0 * M * kPackedP);
+    char* dst = reinterpret_cast<char*>(ps);
+    constexpr unsigned kPiece = 16 * 1024;
+    for (unsigned o = 0; o < bytes; o += kPiece) bulk_g2s(dst + o, src + o, min(kPiece, bytes - o), bar);
+  }
+#pragma unroll 4
+  for (int t = threadIdx.x; t < M * J; t += blockDim.x) a[t] = tmp[(t >> 3) * NJ + (long long)n0 * J + (t & 7)];
+  __syncthreads();
+  float2* res = smem_centered_dft<true>(a, b, tw, J);
+  float2* oth = res == a ? b : a;
+  const float isn = rsqrtf((float)M);
+  mbar_wait(bar, 0);
+  {
+    // 8 lanes per pixel, lane ai = output coil; the half-warp's two pixels
+    // are two apart (packed stride 72 words: banks 0-15 / 16-31)
+    const int lane = threadIdx.x & 31, ai = lane & 7, pl = lane >> 3;
+    const int kin = ((pl & 1) << 1) | (pl >> 1);
+    for (int k = (threadIdx.x >> 5) * 4 + kin; k < M; k += (blockDim.x >> 5) * 4) {
+      const float2* e = ps + (size_t)k * kPackedP;
+      const float2* vv = res + k * J;
+      float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int s = 0; s < 4; ++s) cfma(acc, e[s * 8 + ai], vv[(ai + s) & 7]);
+      {
+        const float2 p4 = e[32 + (ai & 3)];  // P[a][a+4], a < 4; conj for the lower half
+        cfma(acc, ai < 4 ? p4 : make_float2(p4.x, -p4.y), vv[(ai + 4) & 7]);
+      }
+#pragma unroll
+      for (int s = 5; s < 8; ++s) {  // P[ai][b] = conj(P[b][ai]) = conj(E[8 - s][b]), b = ai + s
+        const int bb = (ai + s) & 7;
+        const float2 pc = e[(8 - s) * 8 + bb];
+        cfma(acc, make_float2(pc.x, -pc.y), vv[bb]);
+      }
+      oth[k * J + ai] = cscale(acc, centered_out_scale(k, M, tw.logn, isn));
+    }
+  }
+  __syncthreads();
+  float2* res2 = smem_centered_dft<false>(oth, res, tw, J);
+  for (int t = threadIdx.x; t < M * J; t += blockDim.x) {
+    const int k = t >> 3;
+    tmp2[k * NJ + (long long)n0 * J + (t & 7)] = cscale(res2[t], centered_out_scale(k, M, tw.logn, isn));
+  }
 }
 
 // Row forward stage of row m (smem `sm`: 2 N J float2): v = F1(tmp2 row);
@@ -1040,8 +1162,20 @@ PiPlan::PiPlan(const PiConfig& cfg, const double* y, const uint8_t* mask, size_t
       StridedCopyOp op0{tmpc, conv, 0, (long long)N * JJ, 1};
       launch_fft_axis<StridedCopyOp, true>(op0, tM_, 1, N * JJ, 16, stream_);
     }
-    pmat_ = dalloc_s<float2>(npl, stream_);
-    k_spirit_pmat<<<grid_for(npl), kThreads, 0, stream_>>>(conv, M * N, J, pmat_);
+    // 8 coils, per-stage kernels: the packed Hermitian P, one contiguous
+    // block per image column, prefetched by bulk copies (k_spirit_cols_bulk;
+    // SHLR_SPIRIT_BULK=0 keeps the full P and k_spirit_cols)
+    const size_t bulk_smem = (2 * (size_t)M * J + (size_t)M * kPackedP) * sizeof(float2) + 16;
+    static const bool bulk_env = !std::getenv("SHLR_SPIRIT_BULK") || std::atoi(std::getenv("SHLR_SPIRIT_BULK")) != 0;
+    if (bulk_env && J == 8 && cg_grid_ == 0 && !std::getenv("SHLR_SPIRIT_PPT") && 2 * (bulk_smem + 1024) <= 227 * 1024) {
+      ppack_ = dalloc_s<float2>((size_t)M * N * kPackedP, stream_);
+      k_spirit_pmat_packed8<<<grid_for((size_t)M * N * kPackedP), kThreads, 0, stream_>>>(conv, M, N, ppack_);
+      cols_bulk_smem_ = bulk_smem;
+      SHLR_CUDA(cudaFuncSetAttribute(k_spirit_cols_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bulk_smem));
+    } else {
+      pmat_ = dalloc_s<float2>(npl, stream_);
+      k_spirit_pmat<<<grid_for(npl), kThreads, 0, stream_>>>(conv, M * N, J, pmat_);
+    }
     SHLR_LAUNCH_CHECK();
     SHLR_CUDA(cudaStreamSynchronize(stream_));
     SHLR_CUDA(cudaFreeAsync(conv, stream_));
@@ -1062,7 +1196,7 @@ PiPlan::~PiPlan() {
   void* bufs[] = {yk_, x_, xold_, r_, p_, ap_, bk_, tmp_, tmp2_, dg_, srow_, scol_, hrow_, hcol_,
                   hrow0_, hcol0_, drow_, dcol_, wcN_, wcM_, pmat_, twM_, twN_, sv_, partials_,
                   ctl_, log_, x0_, vrow_, vcol_, sweeps_, vsrow_, vscol_, vs2row_, vs2col_, z1row_, z1col_, vdrow_, vdcol_, ndefl_,
-                  fallback_, ycache_};
+                  fallback_, ycache_, ppack_};
   for (void* b : bufs)
     if (b) cudaFreeAsync(b, stream_);
   if (ev0_) cudaEventDestroy(ev0_);
@@ -1102,8 +1236,11 @@ void PiPlan::cg_apply_spirit(float2* in_vec, float2* out_ap, bool init) {
   static const int ppt_env = std::getenv("SHLR_SPIRIT_PPT") ? std::atoi(std::getenv("SHLR_SPIRIT_PPT")) : 0;
   const int ppt = ppt_env > 0 ? ppt_env : std::max(1, 8 / J);
   const size_t smem2 = 2 * (size_t)M * ppt * J * sizeof(float2);
-  k_spirit_cols<<<(N + ppt - 1) / ppt, kFftThreads, smem2, stream_>>>(tmp_, tmp2_, pmat_, tM_, N, J, ppt,
-                                                                   ctl_, init ? 1 : 0);
+  if (ppack_)
+    k_spirit_cols_bulk<<<N, kFftThreads, cols_bulk_smem_, stream_>>>(tmp_, tmp2_, ppack_, tM_, N, ctl_, init ? 1 : 0);
+  else
+    k_spirit_cols<<<(N + ppt - 1) / ppt, kFftThreads, smem2, stream_>>>(tmp_, tmp2_, pmat_, tM_, N, J, ppt,
+                                                                     ctl_, init ? 1 : 0);
   SHLR_LAUNCH_CHECK();
   ++launch_count_;
   // stage 3: row FFT + combine (+ alpha)

@@ -109,6 +109,8 @@ class PiPlan {
   int svt_dp_ = 0;
   float2 *wcN_ = nullptr, *wcM_ = nullptr;
   float2* pmat_ = nullptr;  // SPIRiT (G-I)^H(G-I) per pixel, [M][N][J][J]
+  float2* ppack_ = nullptr;  // 8 coils: its packed Hermitian form, [N][M][36] (k_spirit_cols_bulk)
+  size_t cols_bulk_smem_ = 0;
   float2 *twM_ = nullptr, *twN_ = nullptr;
   float* sv_ = nullptr;     // debug singular values
   double* partials_ = nullptr;
