@@ -550,10 +550,19 @@ __device__ int newton_schulz_orth(const float2* X, float2* V, float2* Sm, float*
 // floats; flag: one int.  Called by the whole CTA (512 threads).
 template <int KB, int KS, int DP>
 __device__ int cholesky_qr_mma(const float2* X, float2* V, float2* Sm, float2* Mb, float* dinv, int* flag,
-                               float pivtol) {
+                               float pivtol, long long* clk = nullptr) {
   static_assert(KB == 48 || KB == 32, "32- or 48-column block");
   constexpr int NT = 512, PER = (KB * KB + NT - 1) / NT;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x;
+  // diagnostics: durations of Gram + scaling / Cholesky / inverse / product
+  // into clk[0], clk[1], clk[2], clk[7] (phase slots 13, 14, 15, 20 are taken: see the caller)
+  long long t_ = clk ? clock64() : 0;
+#define CQR_ACC(k)                         \
+  if (clk && tid == 0) {                   \
+    const long long n_ = clock64();        \
+    clk[k] = n_ - t_;                      \
+    t_ = n_;                               \
+  }
   gram_sym_mma<KS>(X, Sm, DP / 8);
   if (tid == 0) *flag = 0;
   __syncthreads();
@@ -582,75 +591,117 @@ __device__ int cholesky_qr_mma(const float2* X, float2* V, float2* Sm, float2* M
     }
   }
   __syncthreads();
-  // ---- Cholesky, left-looking, in place in the lower triangle: warps 0-1,
-  // thread i owns row i; column j: s_i = S'[i][j] - sum_{k<j} L[i][k] conj(L[j][k])
-  if (warp < 2) {
-    const int i = tid;
+  CQR_ACC(0);
+  // ---- Cholesky and the inverse factor in one right-looking sweep, all 16
+  // warps, one barrier per column.  Every thread keeps up to PERL elements
+  // (i, k), i >= k, in registers: the trailing-matrix value S(i, k) until
+  // column k is final (after step k - 1), then B(i, k), the forward
+  // substitution of the identity (L^-1 = diag(d)^-1/2 B).  With the unscaled
+  // column C_j = L[:, j] sqrt(d_j), d_j = C_j[j], step j is one rank-1 update
+  // for both roles,
+  //     v(i, k) -= (C_j[i] / d_j) g_j[k],   g_j = [B(j, 0..j-1), 1, conj(C_j[j+1..])],
+  // so row j of the work matrix Gm (= Mb) holds g_j (and C_j[i] = conj(g_j[i])),
+  // published by the owners of column j / of row j of B at step j - 1; d_j
+  // goes to the diagonal of Sm.  (The left-looking factorisation on two warps
+  // plus the 8-lane substitution this replaces took 174 k of the co-located
+  // CTA's 1175 k cycles; a first fused version with separate branches for the
+  // two roles was issue-bound at ~300 instructions per warp and step.)
+  {
+    constexpr int NL = KB * (KB + 1) / 2, PERL = (NL + NT - 1) / NT;
+    int eik[PERL];
+    float2 ev[PERL];
+#pragma unroll
+    for (int q = 0; q < PERL; ++q) {
+      const int e = tid + NT * q;
+      int i = (int)((sqrtf(8.f * (float)e + 1.f) - 1.f) * 0.5f);
+      while ((i + 1) * (i + 2) / 2 <= e) ++i;
+      while (i * (i + 1) / 2 > e) --i;
+      const int k = e - i * (i + 1) / 2;
+      eik[q] = e < NL ? (i | (k << 8)) : 0;  // (i = 0: never active)
+      ev[q] = make_float2(0.f, 0.f);         // column 0 is final: B role
+      if (e < NL) {
+        const float2 sv = Sm[i * KS + k];
+        if (k > 0) ev[q] = sv;
+        else Mb[i] = i == 0 ? make_float2(1.f, 0.f) : cconj(sv);  // g_0
+      }
+    }
     for (int j = 0; j < KB; ++j) {
-      float2 sacc = make_float2(0.f, 0.f);
-      if (i < KB && i >= j) {
-        sacc = Sm[i * KS + j];
-        const float2* li = Sm + i * KS;
-        const float2* lj = Sm + j * KS;
-#pragma unroll 4
-        for (int k = 0; k < j; ++k) {
-          const float2 x = li[k], y = lj[k];  // sacc -= x conj(y)
-          sacc.x -= x.x * y.x + x.y * y.y;
-          sacc.y -= x.y * y.x - x.x * y.y;
+      __syncthreads();  // g_j and d_j are published
+      const float dj = Sm[j * KS + j].x;
+      if (!(dj > pivtol)) *flag = 1;  // (every thread writes the same value)
+      const float inv = 1.f / fmaxf(dj, 1e-30f);
+      const float2* gj = Mb + j * KS;
+      float2* gn = Mb + (j + 1) * KS;
+      // (all loads before the first publishing store: the compiler cannot
+      // reorder them across a store that may alias)
+      float2 ga[PERL], gg[PERL];
+#pragma unroll
+      for (int q = 0; q < PERL; ++q) {
+        const int i = eik[q] & 0xff, k = eik[q] >> 8;
+        ga[q] = gj[i];
+        gg[q] = gj[k];
+      }
+#pragma unroll
+      for (int q = 0; q < PERL; ++q) {
+        const int i = eik[q] & 0xff, k = eik[q] >> 8;
+        if (i > j) {
+          const float2 a = ga[q], g = gg[q];
+          const float cx = a.x * inv, cy = -a.y * inv;  // C_j[i] / d_j
+          float2 v = ev[q];
+          v.x -= cx * g.x - cy * g.y;
+          v.y -= cx * g.y + cy * g.x;
+          if (k == j + 1) {  // column j + 1 is final: publish, switch to the B role
+            if (i == k) {
+              Sm[k * KS + k] = make_float2(v.x, 0.f);
+              gn[k] = make_float2(1.f, 0.f);
+            } else {
+              gn[i] = cconj(v);
+            }
+            v = make_float2(0.f, 0.f);
+          } else if (i == j + 1) {  // row j + 1 of B is final
+            gn[k] = v;
+          }
+          ev[q] = v;
         }
       }
-      if (i == j) {
-        if (!(sacc.x > pivtol)) *flag = 1;
-        Sm[j * KS + j] = make_float2(sqrtf(fmaxf(sacc.x, 1e-30f)), 0.f);
-      }
-      asm volatile("bar.sync 1, 64;" ::: "memory");
-      if (i < KB && i > j) Sm[i * KS + j] = cscale(sacc, 1.f / Sm[j * KS + j].x);
-      asm volatile("bar.sync 1, 64;" ::: "memory");
     }
   }
   __syncthreads();
+  CQR_ACC(1);
   if (*flag) return 0;
-  // ---- T = (L^-1)^T: group of 8 lanes per column j of W = L^-1, stored
-  // transposed (T[j][i] = W[i][j], row j contiguous).  Row i of column j:
-  // W[i][j] = -(sum_{k=j}^{i-1} L[i][k] W[k][j]) / L[i][i]
+  // ---- M = D W^H, W = L^-1: M[c][i] = dinv[c] conj(W[i][c]) = dinv[c] conj(B(i, c)) / sqrt(d_i), i >= c,
+  // B(i, c) = Gm[i][c]: transposed in place through registers
   {
-    const int j = tid >> 3, s8 = tid & 7;
-    if (j < KB) {  // whole warps: 4 groups per warp, 12 warps
-      float2* tj = Mb + j * KS;
-      for (int i = tid & 7; i < j; i += 8) tj[i] = make_float2(0.f, 0.f);  // above the diagonal
-      if (s8 == 0) tj[j] = make_float2(1.f / Sm[j * KS + j].x, 0.f);
-      __syncwarp();
-      // (the four groups of a warp run the same trip count: full-mask shuffles)
-      for (int i = 4 * warp + 1; i < KB; ++i) {
-        const bool on = i > j;
-        float2 part = make_float2(0.f, 0.f);
-        const float2* li = Sm + i * KS;
-        if (on)
-          for (int k = j + s8; k < i; k += 8) cfma(part, li[k], tj[k]);
-        part.x += __shfl_xor_sync(0xffffffffu, part.x, 4);
-        part.y += __shfl_xor_sync(0xffffffffu, part.y, 4);
-        part.x += __shfl_xor_sync(0xffffffffu, part.x, 2);
-        part.y += __shfl_xor_sync(0xffffffffu, part.y, 2);
-        part.x += __shfl_xor_sync(0xffffffffu, part.x, 1);
-        part.y += __shfl_xor_sync(0xffffffffu, part.y, 1);
-        if (on && s8 == 0) tj[i] = cscale(part, -1.f / li[i].x);
-        __syncwarp();
+    float2 m[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int t = tid + NT * q;
+      m[q] = make_float2(0.f, 0.f);
+      if (t < KB * KB) {
+        const int c = t / KB, i = t - c * KB;
+        if (i >= c) {
+          const float w = dinv[c] * rsqrtf(Sm[i * KS + i].x);
+          m[q] = i == c ? make_float2(w, 0.f) : cscale(cconj(Mb[i * KS + c]), w);
+        }
       }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int t = tid + NT * q;
+      if (t < KB * KB) Mb[(t / KB) * KS + (t % KB)] = m[q];
     }
   }
   __syncthreads();
-  // ---- M = D W^H: M[j][i] = dinv[j] conj(W[i][j]) = dinv[j] conj(T[j][i]) (upper triangular)
-  for (int t = tid; t < KB * KB; t += NT) {
-    const int j = t / KB, i = t - j * KB;
-    Mb[j * KS + i] = cscale(cconj(Mb[j * KS + i]), dinv[j]);
-  }
-  __syncthreads();
+  CQR_ACC(2);
   XAccMma<KB / 16> acc;
   acc.zero();
   vu_mma<KS, KB>(acc, X, Mb);
   __syncthreads();  // all reads of X and of Mb (which may alias V) are done
   xacc_store<DP, KS>(acc, V);
   __syncthreads();
+  CQR_ACC(10);
+#undef CQR_ACC
   return 1;
 }
 

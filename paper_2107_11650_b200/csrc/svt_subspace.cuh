@@ -955,7 +955,9 @@ __global__ void __launch_bounds__(kSubNT, MINB) svt_subspace_kernel(const SvtPar
         // Newton-Schulz trial (2: the tail columns of a warm block are too far
         // from orthogonal for it, ||E||_F ~ 3)
         if (warm && prm.ns_orth == 1)
-          ns = cholesky_qr_mma<KB, KS, DP>(X, V, C, BIG ? Yc : V, tau, S.flags + 3, 1e-3f);
+          ns = cholesky_qr_mma<KB, KS, DP>(X, V, C, BIG ? Yc : V, tau, S.flags + 3, 1e-3f,
+                                           prm.phase_clk ? prm.phase_clk + (long long)blockIdx.x * kPhaseSlots + 13
+                                                         : nullptr);  // slots 13, 14, 15, 23
         else if (warm && prm.ns_orth == 2)
           ns = newton_schulz_orth<KB, KS, DP>(X, V, C, tau);
         ns_steps += ns;

@@ -28,6 +28,7 @@ if os.environ.get("SHLR_PHASE_CLK"):
     print("pass split kcycles: wait %.0f build %.0f gemm1 %.0f sum %.0f gemm2 %.0f" % tuple(ph[ok, 8 + i].mean() / 1e3 for i in range(5)))
     e = [(ph[ok, 17 + i] - ph[ok, 16 + i]).mean() / 1e3 for i in range(6)]
     print("RR split kcycles: tridiag %.0f similarity %.0f bisection %.0f twisted+clusters %.0f mgs %.0f backtransform %.0f" % tuple(e))
+    print("QR split kcycles (Cholesky QR): gram+scale %.0f cholesky %.0f inverse %.0f product %.0f" % tuple(ph[ok, i].mean() / 1e3 for i in (13, 14, 15, 23)))
     tot = d(0, 7)
     print("total kcycles percentiles 50/90/99/max:", np.percentile(tot, [50, 90, 99]).round(0), tot.max().round(0),
           "| RR max", d(4, 5).max().round(0), "| matrices stamped", int(ok.sum()))
