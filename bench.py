@@ -323,11 +323,18 @@ def gpu_arm(args, dist, rank, world, local):
     flops = (m + n) * svt_flops(e, d)
     fp32_peak = A.fp32_peak_tflops()
     achieved_tf = flops / (svt_ms * 1e-3) / 1e12
+    # DRAM bytes of one launch of the dominant kernel from the committed ncu
+    # --set full capture of this round (profiles/r02_ncu_summary.json, c2_svt)
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    prof = os.path.join(ROOT, "profiles", "r02_ncu_summary.json")
     if os.path.exists(prof):
         with open(prof) as f:
-            traffic = json.load(f).get("svt_dram_bytes_per_launch")
+            cap = json.load(f).get("c2_svt") or {}
+        scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        rd, wr = cap.get("dram__bytes_read.sum"), cap.get("dram__bytes_write.sum")
+        if rd is not None and wr is not None:
+            traffic = (rd * scale.get(cap.get("dram__bytes_read.sum.unit", "byte"), 1.0)
+                       + wr * scale.get(cap.get("dram__bytes_write.sum.unit", "byte"), 1.0))
 
     # e2e: the public call with host buffers, H2D of y and D2H of x inside
     e2e = None
@@ -399,11 +406,14 @@ def gpu_arm(args, dist, rank, world, local):
         "config": bench_config(world),
         "hankel_svt": {"matrices_per_s": (m + n) / (svt_ms * 1e-3), "kernel_ms": svt_ms,
                        "share_of_step": svt_ms / (t_max_ms / args.steps),
-                       "solver": "subspace iteration (block 48; 1 pass per ADMM iteration warm, 6 cold) + Rayleigh-Ritz by tridiagonalisation/multisection, "
-                                 "full two-stage Jacobi for matrices with > 40 singular values above tau"},
+                       "solver": "subspace iteration (block 48; 1 pass per ADMM iteration warm, 6 cold), chunk contractions as 3xTF32 "
+                                 "mma.sync, tensor-core Cholesky QR, Rayleigh-Ritz by tridiagonalisation/multisection, two co-located "
+                                 "CTAs per SM; full two-stage Jacobi for matrices with > 40 singular values above tau"},
         "roofline": {"bound": "fp32", "achieved": achieved_tf, "peak": fp32_peak, "unit": "TFLOP/s",
                      "frac": achieved_tf / fp32_peak, "traffic": traffic,
-                     "kernel": "svt_subspace_kernel<120,48,32> (+ flagged-matrix hankel_svt_kernel)",
+                     "kernel": "svt_subspace_kernel<120,48,32,BIG,L1,2,MMA> (+ flagged-matrix hankel_svt_kernel)",
+                     "bound_note": "compute-bound; the denominator is the FP32 FMA peak north_star names "
+                                   "(contractions run as 3xTF32 on the tensor cores: 12 mma.sync per complex tile step)",
                      "algorithmic": f"{m + n} x (16 e d^2 + 44 d^3), e={e}, d={d}: {flops / 1e9:.2f} GFLOP/launch",
                      "peak_source": "measured FP32 FMA probe on this GPU (MEASURED_PEAKS.json has no FP32 figure)"},
         "gpu_launches": launches * args.steps,

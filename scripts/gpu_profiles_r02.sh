@@ -25,6 +25,6 @@ cap() {  # name, kernel regex, skip, command...
 cap c2_svt "svt_subspace_kernel<[^,]*120,[^,]*48," 2 $SHORT
 [ -z "${SKIP_COLS:-}" ] && cap c2_cols "k_spirit_cols" 40 $SHORT
 cap sv_tall "svt_subspace_kernel<[^,]*248,[^,]*48," 3 python scripts/sv_probe.py 6
-cap huge "svt_subspace_kernel<[^,]*496,[^,]*32,[^,]*16,[^,]*(1|true),[^,]*(0|false)>" 1 python scripts/sweep_points.py 512,32,15
+cap huge "svt_subspace_kernel<[^,]*496,[^,]*32,[^,]*16,[^,]*(1|true),[^,]*(0|false)," 1 python scripts/sweep_points.py 512,32,15
 cap smalld "svt_subspace_kernel<[^,]*56,[^,]*16," 1 python scripts/sweep_points.py 256,8,7
 ls -la gpurun_out/

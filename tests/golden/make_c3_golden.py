@@ -49,7 +49,7 @@ COILS50 = (0, 18)
 def pack50(d: str) -> None:
     """The 50-iteration run (round 2): the reference's images after iterations
     30, 40, 45 and 50 (two coils as complex64 + the root-sum-of-squares image
-    as float32, whichever dumps exist in DIR) and its log.  From iteration ~38
+    as float32, whichever dumps exist in DIR) and its log.  From iteration 42
     on more than 62 singular values per lifted matrix exceed the threshold,
     which is where the B200 path's deflation chain (level 3) takes over.
 

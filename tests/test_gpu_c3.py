@@ -51,9 +51,9 @@ GOLDEN50 = os.path.join(ROOT, "tests", "golden", "c3_ref50.npz")
 def test_c3_through_the_deflation_chain_vs_reference(gpu):
     """Config 3 to 50 iterations against the reference's own 50-iteration run
     (tests/golden/c3_ref50.npz: images after iterations 30 / 40 / 45 / 50).
-    From iteration ~38 on more than 62 singular values per lifted matrix exceed
-    the threshold, so level 2 deflates and the level-3 chain finishes those
-    matrices: the test asserts that it ran and that the image stays within
+    From iteration 42 on more than 62 singular values of some lifted matrices
+    exceed the threshold (212 of 512 at iteration 50), so level 2 deflates and
+    the level-3 chain finishes those matrices: the test asserts that it ran and that the image stays within
     1e-4 of the reference through it."""
     if not os.path.exists(GOLDEN50):
         pytest.skip("tests/golden/c3_ref50.npz missing (tests/golden/make_c3_golden.py pack50)")
@@ -76,4 +76,6 @@ def test_c3_through_the_deflation_chain_vs_reference(gpu):
         e2 = rel(np.sqrt((np.abs(x) ** 2).sum(axis=2)), g[f"rss{it}"].astype(np.float64))
         worst = max(worst, e1, e2)
         assert e1 < TOL and e2 < TOL, f"iteration {it}: {e1:.3e} / {e2:.3e}"
-    assert done >= 40 and chain > 0, f"deflation chain not exercised (iterations {done}, chain matrices {chain})"
+    # (the chain starts at iteration 42 and holds 212 of the 512 matrices at 50:
+    # scripts/probes/c3_levels.py)
+    assert done >= 45 and chain > 0, f"deflation chain not exercised (iterations {done}, chain matrices {chain})"
