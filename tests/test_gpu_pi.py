@@ -215,9 +215,14 @@ def test_tiny_images_and_extreme_pencils(gpu, m, n, pencil):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("spirit,vc,m,n", [(False, False, 32, 32), (False, True, 32, 40), (True, False, 32, 32),
-                                           (True, True, 24, 40), (True, True, 64, 64)])
-def test_gpu_normal_operator_alone_vs_oracle(gpu, spirit, vc, m, n):
+@pytest.mark.parametrize("spirit,vc,m,n,j", [(False, False, 32, 32, 3), (False, True, 32, 40, 3),
+                                             (True, False, 32, 32, 3), (True, True, 24, 40, 3),
+                                             (True, True, 64, 64, 3),
+                                             # 8 coils: the packed Hermitian P + bulk-copy column stage
+                                             # (k_spirit_cols_bulk), power-of-two and direct-DFT column lengths
+                                             (True, False, 32, 32, 8), (True, True, 24, 40, 8),
+                                             (True, False, 30, 20, 8), (True, False, 128, 64, 8)])
+def test_gpu_normal_operator_alone_vs_oracle(gpu, spirit, vc, m, n, j):
     """The X-update operator on its own (normal_apply, operators.cpp:213-248):
     lambda F* U F + beta (row + column lift normals, weighted, virtual coils)
     + lambda1 (G - I)^H (G - I), evaluated by the device's k-space diagonal
@@ -225,7 +230,6 @@ def test_gpu_normal_operator_alone_vs_oracle(gpu, spirit, vc, m, n):
     random image.  FP32 operator: bar 1e-5 relative L2."""
     import shlr_oracle as O
     A = gpu
-    j = 3
     rng = np.random.default_rng(m + n + 7 * spirit + 3 * vc)
     y = rng.standard_normal((m, n, j)) + 1j * rng.standard_normal((m, n, j))
     x = rng.standard_normal((m, n, j)) + 1j * rng.standard_normal((m, n, j))
@@ -242,3 +246,28 @@ def test_gpu_normal_operator_alone_vs_oracle(gpu, spirit, vc, m, n):
     want = O.normal_apply(x, O.SamplingMask(1, n, mask.bits), gop, cfg, acfg.lam, acfg.lambda1 if spirit else 0.0,
                           acfg.beta)
     assert rel(got, want) < 1e-5
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,n", [(32, 32), (24, 40)])
+def test_eight_coil_spirit_run_vs_oracle(gpu, m, n):
+    """SHLR-S with 8 coils at oracle-sized geometries: the CG loop runs the
+    bulk-prefetch column stage (packed Hermitian P) on power-of-two and
+    direct-DFT column lengths; image and per-iteration CG counts against the
+    oracle."""
+    A = gpu
+    y0 = phantom(m, n, 8, seed=m + n)
+    mk = A.mask_gauss_cartesian(n, 0.5, 8, 5)
+    y = np.where(mk.bits[0][None, :, None].astype(bool), y0, 0)
+    a0, a1 = A.acs_range(n, 8)
+    g = A.spirit_calibrate(y[:, a0:a1, :], 3)
+    iters = 6
+    acfg = A.AdmmConfig(max_outer=iters, tol=1e-300, enable_spirit=True)
+    pencil = 2 * min(m, n) // 3
+    log = []
+    x = A.shlr_pi_reconstruct(y, mk, g, A.HankelConfig(pencil=pencil), acfg, log=log)
+    xo, st = O.shlr_pi_reconstruct(y, O.SamplingMask(1, n, mk.bits), O.SpiritKernels(3, 8, g.weights),
+                                   O.HankelConfig(pencil=pencil),
+                                   O.AdmmConfig(max_outer=iters, tol=1e-300, enable_spirit=True))
+    assert rel(x, xo) < TOL
+    assert [l.split()[2] for l in log] == [l.split()[2] for l in st.log]
