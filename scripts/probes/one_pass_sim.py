@@ -3,6 +3,9 @@ the oracle's ADMM loop, against the exact SVT:
 
   A  (the kernel's scheme)   V' = orth(A^H A V), Rayleigh-Ritz on A V'
   B  (one pass)              Q = orth(A V), B = Q^H A, SVD of the small B
+  C  (carried power step)    V' = orth(W), W = A_old^H A_old V_old carried from the
+                             previous outer iteration; one pass Y1 = A V', X2 = A^H Y1,
+                             Rayleigh-Ritz on H = V'^H X2; W_next = X2 U
 
 Prints the relative image error of each scheme per outer iteration.  A design
 probe only: nothing in the product or the tests imports it.
@@ -60,6 +63,22 @@ class Approx:
                 vu = q @ u
                 z = ((y1 @ u) * f[..., None, :]) @ np.conj(np.swapaxes(vu, -1, -2))
                 self.V[key] = vu
+            elif self.scheme == "C":
+                # power step with the PREVIOUS matrix (carried W = G_old V_old), then a
+                # consistent Rayleigh-Ritz with the new matrix from ONE pass:
+                # Y1 = A V', X2 = A^H Y1, H = V'^H X2
+                q, _ = np.linalg.qr(v)
+                y1 = a @ q
+                x2 = np.conj(np.swapaxes(a, -1, -2)) @ y1
+                h = np.conj(np.swapaxes(q, -1, -2)) @ x2
+                h = 0.5 * (h + np.conj(np.swapaxes(h, -1, -2)))
+                lam, u = np.linalg.eigh(h)
+                lam, u = lam[..., ::-1], u[..., ::-1]
+                sig = np.sqrt(np.maximum(lam, 0))
+                f = np.where(sig > tau, 1 - tau / np.maximum(sig, 1e-300), 0.0)
+                vu = q @ u
+                z = ((y1 @ u) * f[..., None, :]) @ np.conj(np.swapaxes(vu, -1, -2))
+                self.V[key] = x2 @ u
             else:
                 y = a @ v
                 q, _ = np.linalg.qr(y)
@@ -96,7 +115,7 @@ def main():
     hcfg = O.HankelConfig(pencil=P)
     ref = run(exact_svt, y, mk, g, hcfg, acfg)
     print("exact done", flush=True)
-    for scheme in ("A", "B"):
+    for scheme in os.environ.get("SCHEMES", "A,B,C").split(","):
         ap = Approx(scheme)
         st = run(ap, y, mk, g, hcfg, acfg)
         errs = [np.linalg.norm(st.images[k] - ref.images[k]) / np.linalg.norm(ref.images[k])
