@@ -1,4 +1,6 @@
 // Subspace Hankel-SVT instantiations for 40 <= d <= 128 (svt_subspace.cuh).
+#include <cstdlib>
+
 #include "svt_subspace.cuh"
 #include "svt_subspace_launch.cuh"
 
@@ -22,6 +24,19 @@ bool dispatch_small(int dp, const SvtParams& prm, int total, size_t smem, cudaSt
 // 40 <= d < 72: 16-column level 1, 32-column level 2
 template <int KB, bool L2>
 bool dispatch_smalld(int dp, const SvtParams& prm, int total, size_t smem, cudaStream_t stream) {
+  // two CTAs per SM (64 registers per thread) when the shared memory allows it:
+  // one matrix's barrier-bound QR / Rayleigh-Ritz phases overlap the other's
+  // chunk products (SHLR_SMALLD_COLOC=0: one CTA per SM)
+  static const bool coloc = !std::getenv("SHLR_SMALLD_COLOC") || std::atoi(std::getenv("SHLR_SMALLD_COLOC")) != 0;
+  if (coloc && 2 * (smem + 1024) <= 227 * 1024) {
+    switch (dp) {
+      case 40: launch_sub<40, KB, false, L2, 2>(prm, total, smem, stream); return true;
+      case 48: launch_sub<48, KB, false, L2, 2>(prm, total, smem, stream); return true;
+      case 56: launch_sub<56, KB, false, L2, 2>(prm, total, smem, stream); return true;
+      case 64: launch_sub<64, KB, false, L2, 2>(prm, total, smem, stream); return true;
+      default: return false;
+    }
+  }
   switch (dp) {
     case 40: launch_sub<40, KB, false, L2>(prm, total, smem, stream); return true;
     case 48: launch_sub<48, KB, false, L2>(prm, total, smem, stream); return true;

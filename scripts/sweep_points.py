@@ -21,15 +21,18 @@ for arg in sys.argv[1:]:
     dv = torch.from_numpy(synth.sweep_vectors(n, nc, k, batch).astype(np.complex64)).cuda()
     do = torch.empty_like(dv)
     tau = synth.sweep_tau(n, nc, k)
-    A.hankel_svt_batched_device(dv.data_ptr(), batch, nc, n, p, tau, do.data_ptr())
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(3):
+    for _ in range(3):  # warm-up: lazy kernel loading of every level, clocks
         A.hankel_svt_batched_device(dv.data_ptr(), batch, nc, n, p, tau, do.data_ptr())
-    e1.record()
     torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / 3
+    times = []
+    for _ in range(10):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        A.hankel_svt_batched_device(dv.data_ptr(), batch, nc, n, p, tau, do.data_ptr())
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+    ms = float(np.median(times))
     tf = batch * bench.svt_flops(e, d) / (ms * 1e-3) / 1e12
-    print(f"{n}x{nc}x{k} ({p}x{nc * k}) batch {batch}: {ms:.3f} ms, {tf:.2f} TF/s = {tf / peak:.3f} of FP32 peak",
+    print(f"{n}x{nc}x{k} ({p}x{nc * k}) batch {batch}: median {ms:.3f} ms (min {min(times):.3f}, max {max(times):.3f}), {tf:.2f} TF/s = {tf / peak:.3f} of FP32 peak",
           flush=True)
