@@ -271,3 +271,21 @@ def test_eight_coil_spirit_run_vs_oracle(gpu, m, n):
                                    O.AdmmConfig(max_outer=iters, tol=1e-300, enable_spirit=True))
     assert rel(x, xo) < TOL
     assert [l.split()[2] for l in log] == [l.split()[2] for l in st.log]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape,axis", [((256, 256, 8), 0), ((256, 256, 8), 1), ((128, 512, 2), 1),
+                                        ((96, 242, 4), 1), ((45, 64, 3), 0)])
+def test_fft_cross_checked_against_cufft(gpu, shape, axis):
+    """north_star: the hand-written radix / direct-DFT kernels cross-checked
+    against cuFFT (torch.fft on the device, complex128), for correctness only:
+    the centred unitary transform of fft.cpp:100-140 is
+    fftshift(fft(ifftshift(x), norm='ortho')) along the axis."""
+    import torch
+    rng = np.random.default_rng(shape[0] + 7 * axis)
+    x = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+    xt = torch.from_numpy(x).cuda()
+    for inv in (False, True):
+        f = torch.fft.ifft if inv else torch.fft.fft
+        ref = torch.fft.fftshift(f(torch.fft.ifftshift(xt, dim=axis), dim=axis, norm="ortho"), dim=axis).cpu().numpy()
+        assert rel(gpu.fft_along_axis(x, axis, inv), ref) < 1e-6
