@@ -27,15 +27,17 @@
 
 namespace shlr_b200 {
 
-size_t svt_subspace_smem_bytes(int DP, int KB, int R, int maxB, int maxLen, int maxE, bool big) {
+size_t svt_subspace_smem_bytes(int DP, int KB, int R, int maxB, int maxLen, int maxE, bool big, bool coloc) {
   const int KS = KB + 1, CS = DP + 1;
+  // co-located layout: chunk buffer padded to hold the eigen-solver's work area (CROWS in the kernel)
+  const int crows = (coloc && 2 * R * CS < 3 * KB * KB) ? (3 * KB * KB / 2 + CS - 1) / CS : R;
   const size_t spectra = big ? 3ull * maxLen : 2ull * maxB * maxLen;
   const bool huge = big && R == 16;
   const bool nosplit = big && KB > kSubspaceKB;  // BIG level 2
   const size_t yreg = huge      ? (size_t)R * KS
                       : nosplit ? (size_t)std::max(R * KS, KB * KS + 3 * KB * KB / 2 - R * CS)
                                 : 2ull * R * KS;
-  return sizeof(float2) * ((big ? 1ull : 2ull) * DP * KS + (size_t)R * CS + yreg + spectra) +
+  return sizeof(float2) * ((big ? 1ull : 2ull) * DP * KS + (size_t)crows * CS + yreg + spectra) +
          sizeof(SlotRec) * KB + sizeof(double2) * KB + sizeof(double) * KB + 2 * sizeof(float) * KB +
          16 * sizeof(int) + sizeof(int) * KB + sizeof(int) * std::max(DP, maxE) + 64;
 }
@@ -392,6 +394,18 @@ bool launch_level(const SvtParams& prm, int total, cudaStream_t stream) {
     if (2 * (smem + 1024) <= 228 * 1024)
       return mma ? launch_sub_mma(120, kSubspaceKB, false, true, pm, total, smem, stream)
                  : launch_sub_big(120, false, prm, total, smem, stream);
+  }
+  // config 1 (256 lifts of 120 x 72): same layout with the chunk buffer padded to
+  // the eigen-solver's work area; 256 CTAs on 2 x 148 slots are one wave
+  // instead of 1.73 with one CTA per SM (tensor variant only)
+  static const bool coloc_c1 = std::getenv("SHLR_NO_COLOC_C1") == nullptr;
+  if (coloc && coloc_c1 && mma && !L2 && KB1 == kSubspaceKB && svt_padded_dim(g.dmax) == 72 && g.dmin >= 72 &&
+      g.maxLen <= 0xffff) {
+    bool vc_ok = true;
+    for (int f = 0; f < prm.nfam; ++f) vc_ok = vc_ok && !(prm.fam[f].vc && prm.mode != SVT_ADMM_WEIGHTED);
+    const size_t smem = svt_subspace_smem_bytes(72, kSubspaceKB, 32, g.maxB, g.maxLen, g.maxE, true, true);
+    if (vc_ok && 2 * (smem + 1024) <= 228 * 1024 && launch_sub_mma(72, kSubspaceKB, false, true, pm, total, smem, stream))
+      return true;
   }
   // the parameter path's PE lifts (config 4: 244 x 104, 32-column level 1): same layout, tensor variant only
   static const bool coloc_pe = std::getenv("SHLR_NO_COLOC_PE") == nullptr;

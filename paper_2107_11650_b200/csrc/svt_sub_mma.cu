@@ -19,6 +19,10 @@ bool launch_sub_mma(int dp, int kb, bool l2, bool coloc, const SvtParams& prm, i
       launch_sub<104, kSubspaceKB1, true, false, 2, true>(prm, total, smem, stream);
       return true;
     }
+    if (dp == 72 && kb == kSubspaceKB) {
+      launch_sub<72, kSubspaceKB, true, false, 2, true>(prm, total, smem, stream);
+      return true;
+    }
     return false;
   }
   if (dp == 120 && kb == kSubspaceKB && !l2) {

@@ -670,9 +670,12 @@ __global__ void __launch_bounds__(kSubNT, MINB) svt_subspace_kernel(const SvtPar
   static_assert(!COLOC || !L2, "the co-located layout is a level-1 variant");
   // the chunk buffer doubles as the eigen-solver's work area (3 KB^2 floats)
   // and the Cholesky QR's Gram matrix (KB x KS); in the large-d layout the
-  // Rayleigh-Ritz matrix sits right behind it (d = 72 with a 48-column block
-  // does not fit: config 1 stays in the resident layout)
-  static_assert(!COLOC || (2 * R * CS >= 3 * KB * KB && R * CS >= KB * KS), "chunk buffer too small for this block");
+  // Rayleigh-Ritz matrix sits right behind it, so the co-located layout pads
+  // the chunk buffer to CROWS >= R rows when R x CS is too small for the work
+  // area (d = 72 with a 48-column block, config 1: 48 rows)
+  constexpr int CROWS = (COLOC && 2 * R * CS < 3 * KB * KB) ? (3 * KB * KB / 2 + CS - 1) / CS : R;
+  static_assert(!COLOC || (2 * CROWS * CS >= 3 * KB * KB && CROWS * CS >= KB * KS),
+                "chunk buffer too small for this block");
   constexpr bool NOSPLIT = BIG && L2 && !HUGE;
   // MMA: the chunk contractions run as 3xTF32 on the tensor cores (svt_mma.cuh)
   static_assert(!MMA || (R == 32 && (KB == 48 || KB == 32) && !NOSPLIT && !HUGE && DP <= 128 && DP % 8 == 0),
@@ -716,7 +719,7 @@ __global__ void __launch_bounds__(kSubNT, MINB) svt_subspace_kernel(const SvtPar
   float2* V = reinterpret_cast<float2*>(smem_raw);  // DP x KS
   float2* X = BIG ? V : V + DP * KS;                 // DP x KS (non-BIG: also H for the Ritz solve)
   float2* C = BIG ? V + DP * KS : X + DP * KS;       // R x CS  (Ahat chunk / U / T)
-  float2* Yc = C + R * CS;                           // R x KS
+  float2* Yc = C + CROWS * CS;                       // R x KS
   float2* Yc2;                                       // R x KS (second k-half of the chunk GEMM)
   float2* wl;                                        // B x len  (BIG: len)
   float2* acc;                                       // B x len  (BIG: 2 x len)

@@ -8,7 +8,7 @@
 
 namespace shlr_b200 {
 
-size_t svt_subspace_smem_bytes(int DP, int KB, int R, int maxB, int maxLen, int maxE, bool big);
+size_t svt_subspace_smem_bytes(int DP, int KB, int R, int maxB, int maxLen, int maxE, bool big, bool coloc = false);
 // d <= 128 (svt_sub_small.cu): DP in {72, ..., 128}, KB in {32, 48}
 bool launch_sub_small(int dp, int kb, bool l2, const SvtParams& prm, int total, size_t smem, cudaStream_t stream);
 // 128 < d <= 248 (svt_sub_big.cu): DP in {160, 192, 248}; level 1 KB 48, level 2 / 3 KB 64
