@@ -471,6 +471,7 @@ int launch_hankel_svt_levels(const SvtParams& sp, int total, cudaStream_t stream
     SvtParams l2 = sp;
     l2.only_flagged = sp.fam[0].fallback;
     l2.q_cold = std::getenv("SHLR_L2_Q") ? std::atoi(std::getenv("SHLR_L2_Q")) : 8;
+    l2.l2_warm_passes = std::getenv("SHLR_L2_WARM_Q") ? std::atoi(std::getenv("SHLR_L2_WARM_Q")) : 2;
     launch_hankel_svt_level2(l2, total, stream);
     ++n;
   }

@@ -75,6 +75,7 @@ struct SvtParams {
   const int* warm;     // optional device flag: nonzero -> V holds a warm start
   int* sweeps_out;     // optional diagnostics: Jacobi sweeps used per matrix
   int q_cold, q_warm;  // subspace solver: iterations from a random / stored start
+  int l2_warm_passes;    // large-d level 2: warm passes per ADMM iteration (0 / 1: as q_warm)
   long long* phase_clk;  // optional diagnostics: kPhaseSlots clock64 stamps per matrix
   const int* only_flagged;  // nonzero pointer -> process only matrices whose fallback flag is
                             // set (fam[f].fallback); with only_flag_value != 0 (full solver):

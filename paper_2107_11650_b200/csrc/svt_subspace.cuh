@@ -861,6 +861,12 @@ __global__ void __launch_bounds__(kSubNT, MINB) svt_subspace_kernel(const SvtPar
     if (rc > (double)prm.relc_q3) iters = max(iters, 3);
     else if (rc > (double)prm.relc_q2) iters = max(iters, 2);
   }
+  // large-d level 2 (41 to 62 of its 64 columns above the threshold): the
+  // block has little margin over the rank, which is what sets the accuracy of
+  // a warm pass -- two passes (config 3 against the reference's own run at
+  // iteration 50, all 512 matrices at level 2 or in the chain: 1.04e-4 with
+  // one pass; more passes for the chain matrices alone changed nothing)
+  if (BIGLV && L2 && warm && prm.l2_warm_passes > 1) iters = max(iters, prm.l2_warm_passes);
   // inner passes are only normalised when the warm block is already near the
   // subspace (the default single pass); extra adaptive passes are QR'd
   const bool inner_norm = prm.inner_norm && iters == prm.q_warm;

@@ -56,7 +56,7 @@ def test_c3_through_the_deflation_chain_vs_reference(gpu):
     the level-3 chain finishes those matrices: the test asserts that it ran and that the image stays within
     1e-4 of the reference through it."""
     if not os.path.exists(GOLDEN50):
-        pytest.skip("tests/golden/c3_ref50.npz missing (tests/golden/make_c3_golden.py pack50)")
+        pytest.fail("tests/golden/c3_ref50.npz missing (tests/golden/make_c3_golden.py pack50)")
     sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
     import make_c3_golden as G
     g = np.load(GOLDEN50)
