@@ -537,7 +537,7 @@ def hankel_svt_batched(vecs: np.ndarray, p: int, tau: float, want_sv: bool = Tru
     (adjoint vectors (B, Nc, N), singular values (B, d) descending, or None
     with want_sv=False -- the exact singular values need the full eigen-solver,
     which covers d <= 128; without them the subspace levels run any d up to
-    248, tall or wide)."""
+    496, tall or wide, with the deflation chain behind them: no rank limit)."""
     v = _c128(vecs)
     b, nc, n = v.shape
     q = n - p + 1
