@@ -67,7 +67,9 @@ def main():
     open(os.path.join(PROF, "r02_launches.md"), "w").write(
         "Launch list of `python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu --no-extra` (plan setup\n"
         "+ 3 outer iterations of config 2, the first one cold) from `ncu --metrics gpu__time_duration.sum\n"
-        "--clock-control none` (cold-cache, serialised launches: compare shares, not absolute times).\n\n" + tab)
+        "--clock-control none` (cold-cache, serialised launches: compare shares, not absolute times).\n"
+        "`k_fma_probe` is the bench's FP32 peak measurement, not part of the step: without it the SVT kernel's\n"
+        "share of the listed time is its share of the step (bench: `hankel_svt.share_of_step`).\n\n" + tab)
     for k, v in summ.items():
         print(k, {m.split(".")[0][:40]: v.get(m) for m in METRICS[:9]})
 
