@@ -472,6 +472,7 @@ int launch_hankel_svt_levels(const SvtParams& sp, int total, cudaStream_t stream
     l2.only_flagged = sp.fam[0].fallback;
     l2.q_cold = std::getenv("SHLR_L2_Q") ? std::atoi(std::getenv("SHLR_L2_Q")) : 8;
     l2.l2_warm_passes = std::getenv("SHLR_L2_WARM_Q") ? std::atoi(std::getenv("SHLR_L2_WARM_Q")) : 2;
+    l2.l2_pass_margin = std::getenv("SHLR_L2_MARGIN") ? std::atoi(std::getenv("SHLR_L2_MARGIN")) : 16;
     launch_hankel_svt_level2(l2, total, stream);
     ++n;
   }

@@ -49,6 +49,7 @@ struct SvtFamily {
   float2* V;           // full solver: count x DP x DP eigenvector store (V1 spill and
                        // the ADMM warm start; DP = svt_padded_dim of the launch)
   float2* Vs;          // subspace solver: count x DP x KB dominant-subspace store
+  int* rank_prev;      // optional: Ritz values above the threshold in the previous solve of each matrix
   int* fallback;       // subspace solver: per-matrix flag, 1 = rank above threshold too
                        // close to KB, the full solver must redo this matrix
   float2* Z1;          // large d: count x e x d buffer for the deflation chain's Z1
@@ -76,6 +77,7 @@ struct SvtParams {
   int* sweeps_out;     // optional diagnostics: Jacobi sweeps used per matrix
   int q_cold, q_warm;  // subspace solver: iterations from a random / stored start
   int l2_warm_passes;    // large-d level 2: warm passes per ADMM iteration (0 / 1: as q_warm)
+  int l2_pass_margin;    // ... only for matrices whose previous rank is within this margin of the block (0: all)
   long long* phase_clk;  // optional diagnostics: kPhaseSlots clock64 stamps per matrix
   const int* only_flagged;  // nonzero pointer -> process only matrices whose fallback flag is
                             // set (fam[f].fallback); with only_flag_value != 0 (full solver):

@@ -1104,6 +1104,8 @@ PiPlan::PiPlan(const PiConfig& cfg, const double* y, const uint8_t* mask, size_t
     ycache_ = dalloc_s<float2>((size_t)(M + N) * std::max(er, ec) * kSubspaceKB, stream_);
   fallback_ = dalloc_s<int>((size_t)(M + N), stream_);
   SHLR_CUDA(cudaMemsetAsync(fallback_, 0, sizeof(int) * (M + N), stream_));
+  rank_prev_ = dalloc_s<int>((size_t)(M + N), stream_);
+  SHLR_CUDA(cudaMemsetAsync(rank_prev_, 0, sizeof(int) * (M + N), stream_));
   if (const char* s = std::getenv("SHLR_Q_COLD")) q_cold_ = std::atoi(s);
   if (const char* s = std::getenv("SHLR_Q_WARM")) q_warm_ = std::atoi(s);
   if (std::getenv("SHLR_FULL_SVT")) subspace_ = false;
@@ -1196,7 +1198,7 @@ PiPlan::~PiPlan() {
   void* bufs[] = {yk_, x_, xold_, r_, p_, ap_, bk_, tmp_, tmp2_, dg_, srow_, scol_, hrow_, hcol_,
                   hrow0_, hcol0_, drow_, dcol_, wcN_, wcM_, pmat_, twM_, twN_, sv_, partials_,
                   ctl_, log_, x0_, vrow_, vcol_, sweeps_, vsrow_, vscol_, vs2row_, vs2col_, z1row_, z1col_, vdrow_, vdcol_, ndefl_,
-                  fallback_, ycache_, ppack_};
+                  fallback_, ycache_, ppack_, rank_prev_};
   for (void* b : bufs)
     if (b) cudaFreeAsync(b, stream_);
   if (ev0_) cudaEventDestroy(ev0_);
@@ -1215,6 +1217,7 @@ void PiPlan::reset() {
   k_reset_ctl<<<1, 1, 0, stream_>>>(ctl_);
   SHLR_CUDA(cudaMemsetAsync(log_, 0, 3 * sizeof(double) * std::max(cfg_.max_outer, 1), stream_));
   SHLR_CUDA(cudaMemsetAsync(fallback_, 0, sizeof(int) * (M + N), stream_));  // solver levels
+  SHLR_CUDA(cudaMemsetAsync(rank_prev_, 0, sizeof(int) * (M + N), stream_));
   SHLR_LAUNCH_CHECK();
   iter_ = 0;
   subspace_used_ = false;
@@ -1363,6 +1366,7 @@ void PiPlan::enqueue_iteration(int k, bool record_events) {
       F.V = rows ? vrow_ : vcol_;
       F.Vs = rows ? vsrow_ : vscol_;
       F.fallback = rows ? fallback_ : fallback_ + M;
+      F.rank_prev = rows ? rank_prev_ : rank_prev_ + M;
       F.sv = (sv_ && k + 1 == cfg_.debug_sv_iter) ? (rows ? sv_ : sv_ + (size_t)M * d_sv_) : nullptr;
     }
     sp.q_cold = q_cold_;

@@ -109,6 +109,7 @@ class PiPlan {
   int svt_dp_ = 0;
   float2 *wcN_ = nullptr, *wcM_ = nullptr;
   float2* pmat_ = nullptr;  // SPIRiT (G-I)^H(G-I) per pixel, [M][N][J][J]
+  int* rank_prev_ = nullptr;  // Ritz values above the threshold per lifted matrix, previous iteration
   float2* ppack_ = nullptr;  // 8 coils: its packed Hermitian form, [N][M][36] (k_spirit_cols_bulk)
   size_t cols_bulk_smem_ = 0;
   float2 *twM_ = nullptr, *twN_ = nullptr;

@@ -866,7 +866,11 @@ __global__ void __launch_bounds__(kSubNT, MINB) svt_subspace_kernel(const SvtPar
   // a warm pass -- two passes (config 3 against the reference's own run at
   // iteration 50, all 512 matrices at level 2 or in the chain: 1.04e-4 with
   // one pass; more passes for the chain matrices alone changed nothing)
-  if (BIGLV && L2 && warm && prm.l2_warm_passes > 1) iters = max(iters, prm.l2_warm_passes);
+  if (BIGLV && L2 && warm && prm.l2_warm_passes > 1) {
+    // (with the previous rank known: only where the margin is small)
+    const int r_prev = (F.rank_prev && prm.l2_pass_margin > 0) ? F.rank_prev[mat] : KB;
+    if (r_prev > KB - prm.l2_pass_margin || prm.l2_pass_margin <= 0) iters = max(iters, prm.l2_warm_passes);
+  }
   // inner passes are only normalised when the warm block is already near the
   // subspace (the default single pass); extra adaptive passes are QR'd
   const bool inner_norm = prm.inner_norm && iters == prm.q_warm;
@@ -1173,6 +1177,7 @@ __global__ void __launch_bounds__(kSubNT, MINB) svt_subspace_kernel(const SvtPar
   const int r = *cnt;
   // diagnostics: Ritz values above the threshold (x1000) + Rayleigh-Ritz sweeps
   if (prm.sweeps_out && tid == 0) prm.sweeps_out[blockIdx.x] += 1000 * r;
+  if (F.rank_prev && !defl3 && tid == 0) F.rank_prev[mat] = r;
   // the last level accepts Ritz pairs up to KB - kSubspaceMarginLast: pairs
   // that close to the block edge converge slowest but sit near the threshold,
   // where the shrink factor 1 - tau / sigma is ~0.  It keeps a matrix until
