@@ -146,3 +146,22 @@ def test_c2_device_calibration_end_to_end(gpu, golden, inputs):
     g = A.spirit_calibrate(y[:, a0:a1, :], 5, 1e-4, device=True)
     x = A.shlr_pi_reconstruct(y, mask, g, hcfg, A.AdmmConfig(max_outer=50, tol=1e-300, enable_spirit=True))
     assert rel(x, golden["x50"]) < TOL
+
+
+@pytest.mark.gpu
+def test_c2_runs_are_bitwise_repeatable(gpu, inputs):
+    """Two independent plans at the headline size give bitwise-equal images
+    (test_solvers.cpp's determinism contract at full size): the co-located
+    SVT CTAs, the read-modify-written adjoints, the bulk-copy SPIRiT stage and
+    the last-CTA reductions leave no ordering to chance."""
+    A = gpu
+    y, mask, g, hcfg = inputs
+    out = []
+    for _ in range(2):
+        plan = A.PiPlan(y, mask, g, hcfg, A.AdmmConfig(max_outer=12, tol=1e-300, enable_spirit=True))
+        plan.run(12)
+        plan.sync()
+        x, _ = plan.download()
+        plan.close()
+        out.append(x)
+    assert np.array_equal(out[0], out[1])
