@@ -76,6 +76,7 @@ struct SvtParams {
   const int* warm;     // optional device flag: nonzero -> V holds a warm start
   int* sweeps_out;     // optional diagnostics: Jacobi sweeps used per matrix
   int q_cold, q_warm;  // subspace solver: iterations from a random / stored start
+  int rr_orth_mode;      // Rayleigh-Ritz eigenvectors: 0 first-order symmetric correction (Gram-Schmidt fallback), 2 Gram-Schmidt, 1 none
   int l2_warm_passes;    // large-d level 2: warm passes per ADMM iteration (0 / 1: as q_warm)
   int l2_pass_margin;    // ... only for matrices whose previous rank is within this margin of the block (0: all)
   long long* phase_clk;  // optional diagnostics: kPhaseSlots clock64 stamps per matrix

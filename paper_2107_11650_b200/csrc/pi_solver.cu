@@ -1370,6 +1370,7 @@ void PiPlan::enqueue_iteration(int k, bool record_events) {
       F.sv = (sv_ && k + 1 == cfg_.debug_sv_iter) ? (rows ? sv_ : sv_ + (size_t)M * d_sv_) : nullptr;
     }
     sp.q_cold = q_cold_;
+    sp.rr_orth_mode = std::getenv("SHLR_RR_ORTH") ? std::atoi(std::getenv("SHLR_RR_ORTH")) : 0;
     sp.q_warm = q_warm_;
     sp.rr_tol_rel = rr_tol_rel_;
     sp.rr_tol_abs = rr_tol_abs_;

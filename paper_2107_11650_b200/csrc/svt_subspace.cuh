@@ -230,7 +230,7 @@ __device__ void householder_qr(float2* M, float2* Q, int d, float* tau) {
 // written).  Runs on kSubNT threads; ~ (3 n + 60) barriers in total.
 template <int n, int KS>
 __device__ void hermitian_eig_tridiag(float2* H, float* scr, float* work, float2* U, double* evals,
-                                      float care = 0.f, long long* clk = nullptr) {
+                                      float care = 0.f, long long* clk = nullptr, int orth_mode = 0) {
 #define EIG_STAMP(k) \
   if (clk && threadIdx.x == 0) clk[k] = clock64()
   EIG_STAMP(0);
@@ -552,6 +552,40 @@ __device__ void hermitian_eig_tridiag(float2* H, float* scr, float* work, float2
     int nh = 1;
     for (int k = 1; k < n; ++k) nh += (float)evals[k] >= care;
     nh = min(n, nh + 1);
+    // orth_mode 0 (default): one symmetric first-order correction of the head,
+    // Y_h <- Y_h (I - E / 2), E = Y_h^T Y_h - I -- the twisted / cluster vectors
+    // are orthonormal to ~1e-4 at worst (close, unclustered pairs in early
+    // iterations), which the correction squares -- in two barrier-separated
+    // steps instead of nh; the Gram-Schmidt sweep below stays as the fallback
+    // when some |E| exceeds 1e-3.  2: Gram-Schmidt only; 1: neither (experiment).
+    if (orth_mode == 1) nh = 0;
+    if (orth_mode == 0) {
+      float* E = Dp;  // n x n floats, dead after the twisted factorisations
+      bool big = false;
+      for (int idx = tid; idx < nh * nh; idx += NT) {
+        const int a = idx / nh, b = idx - a * nh;
+        if (a <= b) {
+          float dot = 0.f;
+#pragma unroll 8
+          for (int i = 0; i < n; ++i) dot = fmaf(Y[i * n + a], Y[i * n + b], dot);
+          const float e = dot - (a == b ? 1.f : 0.f);
+          E[a * n + b] = e;
+          E[b * n + a] = e;
+          big = big || !(fabsf(e) <= 1e-3f);
+        }
+      }
+      if (!__syncthreads_or(big)) {
+        if (act && g < nh) {
+#pragma unroll
+          for (int t = 0; t < CU; ++t) {
+            float acc = 0.f;
+            for (int b = 0; b < nh; ++b) acc = fmaf(Y[(s + 8 * t) * n + b], E[b * n + g], acc);
+            y[t] = fmaf(-0.5f, acc, y[t]);
+          }
+        }
+        nh = 0;
+      }
+    }
     for (int k = 0; k < nh; ++k) {
       float ss = 0.f;
 #pragma unroll
@@ -1077,7 +1111,8 @@ __global__ void __launch_bounds__(kSubNT, MINB) svt_subspace_kernel(const SvtPar
     SUB_STAMP(4);
     hermitian_eig_tridiag<KB, KS>(Hm, reinterpret_cast<float*>(S.rec), reinterpret_cast<float*>(C), C, S.dg,
                                   0.25f * prm.thresh * prm.thresh,
-                                  prm.phase_clk ? prm.phase_clk + (long long)blockIdx.x * kPhaseSlots + 16 : nullptr);
+                                  prm.phase_clk ? prm.phase_clk + (long long)blockIdx.x * kPhaseSlots + 16 : nullptr,
+                                  prm.rr_orth_mode);
     SUB_STAMP(5);
     if (prm.sweeps_out && tid == 0) prm.sweeps_out[blockIdx.x] = ns_steps;
   } else {
