@@ -210,12 +210,20 @@ def _pi_args(y: np.ndarray, mask: SamplingMask, g: Optional[SpiritKernels], hcfg
 def shlr_pi_reconstruct(y: np.ndarray, mask: SamplingMask, g: Optional[SpiritKernels],
                         hcfg: HankelConfig, acfg: AdmmConfig,
                         log: Optional[List[str]] = None, stats: Optional[SolveStats] = None,
-                        debug_sv_iter: int = 0, sv_out: Optional[list] = None) -> np.ndarray:
-    """``shlr::shlr_pi_reconstruct`` (``solvers.hpp:64-70``) on the GPU."""
+                        debug_sv_iter: int = 0, sv_out: Optional[list] = None,
+                        out: Optional[np.ndarray] = None) -> np.ndarray:
+    """``shlr::shlr_pi_reconstruct`` (``solvers.hpp:64-70``) on the GPU.
+    out: optional caller-owned result buffer (complex128, C-contiguous,
+    M x N x J; e.g. pinned host memory that is reused across calls)."""
     keep: list = []
     a = _pi_args(y, mask, g, hcfg, acfg, debug_sv_iter, keep)
     m, n, j = y.shape
-    x = np.empty((m, n, j), np.complex128)
+    if out is not None:
+        if out.dtype != np.complex128 or out.shape != (m, n, j) or not out.flags.c_contiguous:
+            raise ValueError("shlr_pi_reconstruct: out must be a C-contiguous complex128 M x N x J array")
+        x = out
+    else:
+        x = np.empty((m, n, j), np.complex128)
     st = ShlrStats()
     lines: List[str] = []
 
